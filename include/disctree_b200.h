@@ -1,0 +1,202 @@
+/*
+ * disctree_b200.h -- C ABI of the B200 (sm_100a) disc-field treecode.
+ *
+ * This is the drop-in boundary for the reference's hot path
+ * (/root/reference/pkg/src/disctree).  The reference is a Python package
+ * whose native layer is a set of numba-jitted kernels called from
+ * tree.py / direct.py / charges.py; every entry point below names the
+ * reference routine it replaces.  INTEGRATION.md shows the ctypes binding a
+ * maintainer would add to the reference.
+ *
+ * Conventions (all entry points):
+ *   - Array arguments are DEVICE pointers (CUDA global memory on the current
+ *     device) unless the parameter name ends in _host.  Scalars by value.
+ *   - Work is enqueued on `stream` (a cudaStream_t, NULL = legacy default
+ *     stream) and is asynchronous: results are valid once the stream is
+ *     synchronised.  No entry point synchronises the device.
+ *   - The caller owns every buffer, including outputs and workspaces; the
+ *     library never allocates device memory.  `*_workspace()` functions give
+ *     the required workspace size in bytes.
+ *   - Return value: DT_OK (0) or a negative DT_ERR_* code; dt_last_error()
+ *     returns a thread-local message for the last failure.  The reference's
+ *     numba kernels have no error returns; its Python wrappers validate first
+ *     (SURVEY.md §8(b)).  Validation here is limited to what is checkable
+ *     without reading device memory.
+ *   - Reentrant; no global mutable state besides the thread-local error text.
+ *   - Indices inside the library are 32-bit: n_src, n_nodes < 2^31.
+ */
+#ifndef DISCTREE_B200_H
+#define DISCTREE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DT_OK 0
+#define DT_ERR_INVALID (-1)   /* bad argument */
+#define DT_ERR_CUDA (-2)      /* CUDA runtime error (message in dt_last_error) */
+#define DT_ERR_WORKSPACE (-3) /* workspace too small */
+#define DT_ERR_DEVICE (-4)    /* current device is not sm_100 */
+
+/* tree.py:32 MAX_DEPTH; levels are 0..DT_MAX_DEPTH */
+#define DT_MAX_DEPTH 60
+#define DT_MAX_LEVELS (DT_MAX_DEPTH + 1)
+
+/* Tree metadata block (int64, device memory, DT_META_WORDS words) written by
+ * dt_build_tree and read by dt_moments.  Level l occupies node indices
+ * [meta[DT_META_LEVEL0 + l], meta[DT_META_LEVEL0 + l + 1]) (BFS order). */
+#define DT_META_NODES 0    /* number of nodes                          */
+#define DT_META_DEPTH 1    /* deepest level (Tree.depth)               */
+#define DT_META_LEAVES 2   /* Tree.leaf_count                          */
+#define DT_META_OVERFLOW 3 /* nonzero: node_capacity was too small     */
+#define DT_META_CURLEVEL 4 /* internal                                 */
+#define DT_META_LEVEL0 8
+#define DT_META_WORDS 72
+
+/* Direct-sum arithmetic (direct.py:52-88) */
+#define DT_DIRECT_FP64 0  /* fp64 pairs, fp64 accumulation (phi_sum_plain)        */
+#define DT_DIRECT_FP32 1  /* fp32 pair evaluation, fp64 accumulation (bench only)  */
+#define DT_DIRECT_KAHAN 2 /* IEEE pairs, Kahan in ascending order (phi_sum_kahan)  */
+
+/* Adaptive truncation-order selection mode (dt_choose_p_batch, eval) */
+#define DT_PSEL_FAST 0  /* fp32 bound estimate, exact replica inside the margin */
+#define DT_PSEL_EXACT 1 /* always the exact replica of the compiled reference   */
+
+const char *dt_version(void);
+const char *dt_last_error(void);
+/* DT_OK iff the current CUDA device is compute capability 10.0 (B200). */
+int dt_device_check(void);
+
+/* ---------------------------------------------------------------- (a) */
+
+/* Inclusive prefix sum prefix[i] = sum_{j<=i} qs[j] (replaces the sequential
+ * np.cumsum of charges.py:130).  Deterministic (fixed reduction tree); it
+ * differs from the sequential sum by round-off only. */
+size_t dt_prefix_scan_workspace(int64_t n);
+int dt_prefix_scan(const double *qs, double *prefix, int64_t n, void *workspace,
+                   size_t workspace_bytes, void *stream);
+
+/* e(y) = 2 * prefix_excl[lower_bound(xs, y)] - total, total = prefix[n-1]
+ * (charges.py:183-187 _sign_terms; a source exactly at y counts on the minus
+ * side).  Targets in any order.  n == 0 gives e = 0. */
+int dt_sign_terms(const double *xs, const double *prefix, int64_t n, const double *ys,
+                  double *e_out, int64_t n_targets, void *stream);
+
+/* ---------------------------------------------------------------- (b) */
+
+/* Level-synchronous breadth-first bisection tree over sorted xs[0..n)
+ * (tree.py:156-222): bit-identical node arrays (BFS order, -1 = no child),
+ * depth and leaf_count.  The padded root interval is computed on the device
+ * exactly as tree.py:173-175 (pad = 1e-12 * max(1, |x_0|, |x_{n-1}|)).
+ * `packed` (optional, may be NULL) receives node_capacity 32-byte records
+ * for the traversal.
+ * If the tree needs more than node_capacity nodes, meta[DT_META_OVERFLOW]
+ * is set and the arrays are incomplete: enlarge and call again. */
+size_t dt_build_workspace(int64_t n, int64_t node_capacity);
+int dt_build_tree(const double *xs, int64_t n, int64_t leaf_capacity, int64_t max_depth,
+                  int64_t node_capacity, double *lo, double *hi, double *center, double *half,
+                  int64_t *level, int64_t *start, int64_t *end, int64_t *left, int64_t *right,
+                  void *packed, int64_t *meta, void *workspace, size_t workspace_bytes,
+                  void *stream);
+
+/* ---------------------------------------------------------------- (c) */
+
+/* Node moments m_k = sum_j q_j (x_j - c)^k / k!, k = 0..order, row-major
+ * [n_nodes][order + 1] (tree.py:224-238): P2M at every leaf from its sources,
+ * then M2M (binomial shift) bottom-up level by level.  Reads the tree
+ * produced by dt_build_tree (meta gives n_nodes, depth and level ranges). */
+int dt_moments(const double *xs, const double *qs, const double *center, const int64_t *start,
+               const int64_t *end, const int64_t *left, const int64_t *right,
+               const int64_t *meta, int64_t order, double *moments, void *stream);
+
+/* ---------------------------------------------------------------- (d)+(e) */
+
+typedef struct dt_eval_stats {
+    uint64_t *hash;      /* FNV-1a over interaction events in DFS order         */
+    int64_t *near_pairs; /* near-field (source, target) pairs                    */
+    int64_t *n_far;      /* accepted far nodes                                   */
+    int64_t *sum_p;      /* sum of truncation orders over accepted far nodes     */
+    int64_t *n_p0;       /* accepted far nodes with p_use == 0                   */
+    int64_t *n_exact;    /* far nodes whose order came from the exact replica    */
+} dt_eval_stats;
+
+/* Interleave (x_j, q_j) into xq[2n] for the traversal kernel. */
+int dt_pack_sources(const double *xs, const double *qs, int64_t n, double *xq, void *stream);
+/* Pack the SoA node arrays into 32-byte records (`packed`, n_nodes). */
+int dt_pack_tree(const double *centers, const double *halves, const int64_t *starts,
+                 const int64_t *ends, const int64_t *lefts, const int64_t *rights,
+                 int64_t n_nodes, void *packed, void *stream);
+
+size_t dt_tree_eval_workspace(int64_t n_nodes, int64_t n_src);
+
+/* Mirror of the numba seam _kernels.tree_phi_sum (_kernels.py:163-266):
+ * far-field/near-field traversal for targets ys[i0:i1]; writes out[i0:i1]
+ * (out[i] += phi if accumulate != 0).  The MAC and the adaptive truncation
+ * order are bit-identical to the compiled reference; cos_tab/sin_tab are the
+ * n_samples contour tables (tree.py:342, from host numpy).  Targets may be
+ * in any order; sorted targets traverse coherently (fast). */
+int dt_tree_phi_sum(const double *centers, const double *halves, const int64_t *starts,
+                    const int64_t *ends, const int64_t *lefts, const int64_t *rights,
+                    const double *moments, int64_t moment_stride, int64_t n_nodes,
+                    const double *xs, const double *qs, int64_t n_src, double rd2, double theta,
+                    int64_t p, int adaptive, double tol_share, int64_t p_cap,
+                    const double *cos_tab, const double *sin_tab, int64_t n_samples,
+                    const double *ys, double *out, int64_t i0, int64_t i1, int accumulate,
+                    void *workspace, size_t workspace_bytes, void *stream);
+
+/* Same, on pre-packed nodes/sources (what the Python layer uses).  `stats`
+ * (host struct of device pointers, indexed by target) may be NULL; psel_mode
+ * is DT_PSEL_FAST or DT_PSEL_EXACT. */
+int dt_tree_phi_sum_packed(const void *packed_nodes, int64_t n_nodes, const double *moments,
+                           int64_t moment_stride, const double *xq, int64_t n_src, double rd2,
+                           double theta, int64_t p, int adaptive, double tol_share,
+                           int64_t p_cap, const double *cos_tab, const double *sin_tab,
+                           int64_t n_samples, const double *ys, double *out, int64_t i0,
+                           int64_t i1, int accumulate, int psel_mode,
+                           const dt_eval_stats *stats, void *workspace,
+                           size_t workspace_bytes, void *stream);
+
+/* Same traversal on a tree fresh from dt_build_tree without any host
+ * round trip: the tree depth (and so tol_share = tolerance / (3 max(depth,1)),
+ * tree.py:268-270) is read from `meta` on the device.  node_capacity bounds
+ * the node arrays.  Used by the pipelined (CUDA-graph capturable) step. */
+int dt_tree_eval_device(const void *packed_nodes, const int64_t *meta, int64_t node_capacity,
+                        const double *moments, int64_t moment_stride, const double *xq,
+                        int64_t n_src, double rd2, double theta, int64_t p, int adaptive,
+                        double tolerance, int64_t p_cap, const double *cos_tab,
+                        const double *sin_tab, int64_t n_samples, const double *ys, double *out,
+                        int64_t i0, int64_t i1, int accumulate, void *workspace,
+                        size_t workspace_bytes, void *stream);
+
+/* Adaptive order for n (R, h) pairs (test hook for _kernels.py:212-231):
+ * p_out[i] = order chosen; tier_out[i] (may be NULL) = 0 fast path, 1 exact. */
+int dt_choose_p_batch(const double *big_r, const double *h, int64_t n, double rd2,
+                      double tol_share, int64_t p_cap, const double *cos_tab,
+                      const double *sin_tab, int64_t n_samples, int psel_mode, int64_t *p_out,
+                      int32_t *tier_out, void *stream);
+
+/* ---------------------------------------------------------------- (f) */
+
+/* out[i] (+)= sum_j qs[j] (xs[j] - ys[i]) / sqrt((xs[j] - ys[i])^2 + rd2),
+ * i in [i0, i1): _kernels.phi_sum_plain (mode DT_DIRECT_FP64),
+ * _kernels.phi_sum_kahan (DT_DIRECT_KAHAN, bit-identical), or the
+ * fp32-evaluation / fp64-accumulation bench variant (DT_DIRECT_FP32). */
+int dt_phi_sum_direct(const double *xs, const double *qs, int64_t n, const double *ys,
+                      double rd2, double *out, int64_t i0, int64_t i1, int mode, int accumulate,
+                      void *stream);
+
+/* ---------------------------------------------------------------- diagnostics */
+
+/* FP64 FMA throughput probe for the roofline denominator: `blocks` x 256
+ * threads, each running 8 independent DFMA chains for `iters` steps; writes
+ * one value per thread to out (keeps the work live).  Flops = 16 * iters *
+ * blocks * 256. */
+int dt_fp64_probe(double *out, int64_t iters, int blocks, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DISCTREE_B200_H */

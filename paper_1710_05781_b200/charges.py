@@ -1,0 +1,158 @@
+"""Charge systems on the GPU: sorted sources, prefix sums, the sign term e(y).
+
+Mirror of disctree.charges (charges.py:16-54, 114-132, 183-202): same names,
+argument meaning and errors.  Arrays live on the current CUDA device as
+float64 torch tensors; the prefix sum and the sign term run in
+csrc/dt_scan.cu (stage (a) of the hot path).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Iterator
+
+import numpy as np
+import torch
+
+from . import _lib
+
+
+@dataclass(frozen=True)
+class Charge:
+    x: float
+    q: float
+
+
+def _to_device(a, dtype=torch.float64) -> torch.Tensor:
+    dev = _lib.require_device()
+    if isinstance(a, torch.Tensor):
+        return a.to(device=dev, dtype=dtype, non_blocking=a.is_pinned()).contiguous()
+    arr = np.ascontiguousarray(np.asarray(a, dtype=np.float64))
+    return torch.from_numpy(arr).to(dev).to(dtype).contiguous()
+
+
+def prefix_sum(qs: torch.Tensor) -> torch.Tensor:
+    """Inclusive scan of q on the device (replaces np.cumsum, charges.py:130)."""
+    n = qs.numel()
+    out = torch.empty_like(qs)
+    if n == 0:
+        return out
+    L = _lib.load()
+    ws_bytes = L.dt_prefix_scan_workspace(n)
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device=qs.device)
+    _lib.check(
+        L.dt_prefix_scan(_lib.ptr(qs), _lib.ptr(out), n, _lib.ptr(ws), ws_bytes,
+                         _lib.stream_handle()),
+        "dt_prefix_scan",
+    )
+    return out
+
+
+@dataclass(frozen=True, eq=False)
+class ChargeSystem:
+    """Charges sorted ascending by position (charges.py:28-54).
+
+    ``xs``, ``qs``, ``prefix`` are float64 CUDA tensors; ``prefix[m]`` is the
+    sum of the first m + 1 strengths and ``total == prefix[-1]``.
+    """
+
+    xs: torch.Tensor
+    qs: torch.Tensor
+    prefix: torch.Tensor
+    total: float
+
+    def __post_init__(self) -> None:
+        for name in ("xs", "qs", "prefix"):
+            v = getattr(self, name)
+            if not (isinstance(v, torch.Tensor) and v.is_cuda and v.dtype == torch.float64):
+                object.__setattr__(self, name, _to_device(v))
+
+    def __len__(self) -> int:
+        return int(self.xs.shape[0])
+
+    def __getitem__(self, m: int) -> Charge:
+        return Charge(float(self.xs[m]), float(self.qs[m]))
+
+    def __iter__(self) -> Iterator[Charge]:
+        for x, q in zip(self.xs.cpu().tolist(), self.qs.cpu().tolist()):
+            yield Charge(float(x), float(q))
+
+    def numpy(self) -> tuple[np.ndarray, np.ndarray]:
+        return self.xs.cpu().numpy(), self.qs.cpu().numpy()
+
+
+def from_sorted(xs, qs) -> ChargeSystem:
+    """ChargeSystem from positions already sorted ascending (no sort, no copy
+    if they are float64 CUDA tensors)."""
+    x = _to_device(xs)
+    q = _to_device(qs)
+    pre = prefix_sum(q)
+    total = float(pre[-1]) if pre.numel() else 0.0
+    return ChargeSystem(xs=x, qs=q, prefix=pre, total=total)
+
+
+def from_particles(raw) -> ChargeSystem:
+    """Sorted ChargeSystem from (x, q) pairs (charges.py:114-132).
+
+    Duplicates are kept in input order (stable sort); NaN/inf rejected.
+    """
+    if not isinstance(raw, torch.Tensor):
+        raw = np.asarray(raw, dtype=np.float64)
+    if raw.size == 0 if isinstance(raw, np.ndarray) else raw.numel() == 0:
+        raw = raw.reshape(0, 2)
+    if raw.ndim != 2 or raw.shape[1] != 2:
+        raise ValueError(f"expected (x, q) pairs, got array of shape {tuple(raw.shape)}")
+    arr = _to_device(raw)
+    if not bool(torch.isfinite(arr).all()):
+        raise ValueError("positions and strengths must all be finite")
+    x = arr[:, 0].contiguous()
+    q = arr[:, 1].contiguous()
+    if x.numel() > 1 and not bool((x[1:] >= x[:-1]).all()):
+        x, order = torch.sort(x, stable=True)
+        q = q[order].contiguous()
+    return from_sorted(x, q)
+
+
+def _sign_terms(system: ChargeSystem, targets: torch.Tensor) -> torch.Tensor:
+    """e(y) for targets in any order (charges.py:183-187), on the device."""
+    out = torch.empty_like(targets)
+    T = targets.numel()
+    if T == 0:
+        return out
+    L = _lib.load()
+    _lib.check(
+        L.dt_sign_terms(_lib.ptr(system.xs), _lib.ptr(system.prefix), len(system),
+                        _lib.ptr(targets), _lib.ptr(out), T, _lib.stream_handle()),
+        "dt_sign_terms",
+    )
+    return out
+
+
+def sign_term_all(system: ChargeSystem, targets):
+    """e(y) = sum(q_j, x_j < y) - sum(q_j, x_j >= y) for ascending targets
+    (charges.py:190-202).  Returns the same kind of array as ``targets``."""
+    t, kind = as_targets(targets, check_finite=False)
+    if t.numel() > 1 and not bool((t[1:] >= t[:-1]).all()):
+        raise ValueError("targets must be sorted ascending")
+    return kind(_sign_terms(system, t))
+
+
+def as_targets(targets, check_finite: bool = True):
+    """Validate targets (direct.py:43-49) -> (float64 CUDA tensor, converter back).
+
+    The shape check runs on the host before any device work; finiteness is
+    checked on the device."""
+    if isinstance(targets, torch.Tensor):
+        if targets.ndim != 1:
+            raise ValueError(f"targets must be one-dimensional, got shape {tuple(targets.shape)}")
+        back = (lambda v: v) if targets.is_cuda else (lambda v: v.cpu())  # noqa: E731
+        t = _to_device(targets)
+    else:
+        arr = np.asarray(targets, dtype=np.float64)
+        if arr.ndim != 1:
+            raise ValueError(f"targets must be one-dimensional, got shape {arr.shape}")
+        back = lambda v: v.cpu().numpy()  # noqa: E731
+        t = _to_device(arr)
+    if check_finite and t.numel() and not bool(torch.isfinite(t).all()):
+        raise ValueError("targets must all be finite")
+    return t, back

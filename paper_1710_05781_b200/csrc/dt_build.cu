@@ -1,0 +1,382 @@
+// (b) Tree construction: level-synchronous, breadth-first, bit-exact.
+//
+// Reference: tree.py:156-222 (build, structure part).  The reference walks
+// the frontier in Python, one np.searchsorted per node.  Here one cooperative
+// persistent kernel processes a level per step:
+//   phase A  every frontier node decides leaf/split (count <= leaf_capacity or
+//            level >= max_depth), finds split = lower_bound(xs[start:end], mid)
+//            and counts its non-empty children; block-local exclusive scan.
+//   phase B  block offsets (fixed-order sum of the block totals) give every
+//            child its breadth-first index f1 + offset; children are written
+//            and the parent's left/right slots are set with the reference's
+//            rule "left iff child_hi == mid" (tree.py:205-208).
+// BFS numbering equals level offset + spatial rank within the level, because
+// the reference appends left-then-right children of an in-order frontier.
+// Levels with few nodes run inside block 0 alone (no grid barrier).
+// mid/center/half use explicit round-to-nearest intrinsics so that nvcc can
+// never contract them: 0.5*(lo+hi) and 0.5*(hi-lo) exactly as numpy does.
+#include <cooperative_groups.h>
+
+#include "dt_common.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace {
+
+constexpr int BUILD_THREADS = 512;
+constexpr int SMALL_LEVEL = 4 * BUILD_THREADS;  // nodes handled by block 0 alone
+
+struct BuildArgs {
+    const double *xs;
+    int64_t n;
+    int64_t leaf_capacity;
+    int64_t max_depth;
+    int64_t capacity;
+    double *lo, *hi, *center, *half;
+    int64_t *level, *start, *end, *left, *right;
+    dt_node *packed;
+    int64_t *meta;
+    int32_t *scratch_off;    // [capacity] local exclusive offset within the block chunk
+    int64_t *block_total;    // [gridDim]
+};
+
+__device__ __forceinline__ double mid_of(double lo, double hi)
+{
+    return __dmul_rn(0.5, __dadd_rn(lo, hi));
+}
+
+__device__ void write_node(const BuildArgs &a, int64_t c, double lo, double hi, int64_t lev,
+                           int64_t s, int64_t e)
+{
+    double ctr = __dmul_rn(0.5, __dadd_rn(lo, hi));
+    double hw = __dmul_rn(0.5, __dsub_rn(hi, lo));
+    a.lo[c] = lo;
+    a.hi[c] = hi;
+    a.center[c] = ctr;
+    a.half[c] = hw;
+    a.level[c] = lev;
+    a.start[c] = s;
+    a.end[c] = e;
+    a.left[c] = -1;
+    a.right[c] = -1;
+    if (a.packed) {
+        dt_node nd;
+        nd.center = ctr;
+        nd.half = hw;
+        nd.left = -1;
+        nd.right = -1;
+        nd.start = (int32_t)s;
+        nd.end = (int32_t)e;
+        a.packed[c] = nd;
+    }
+}
+
+// Node fields written earlier in this launch by other blocks are read with
+// ld.global.cg (L2, never a stale L1 line).
+__device__ __forceinline__ int64_t ld_cg(const int64_t *p) { return __ldcg(p); }
+__device__ __forceinline__ double ld_cg(const double *p) { return __ldcg(p); }
+
+// Number of children of frontier node `node` (0 if it is a leaf) and split.
+__device__ __forceinline__ int node_children(const BuildArgs &a, int64_t node, int64_t lev,
+                                             int64_t *split_out)
+{
+    int64_t s = ld_cg(a.start + node), e = ld_cg(a.end + node);
+    if (e - s <= a.leaf_capacity || lev >= a.max_depth)
+        return 0;
+    double mid = mid_of(ld_cg(a.lo + node), ld_cg(a.hi + node));
+    int64_t split = dt_lower_bound(a.xs, s, e, mid);
+    *split_out = split;
+    return (split > s) + (e > split);
+}
+
+__device__ void emit_children(const BuildArgs &a, int64_t node, int64_t lev, int64_t first_child)
+{
+    int64_t s = ld_cg(a.start + node), e = ld_cg(a.end + node);
+    double lo = ld_cg(a.lo + node), hi = ld_cg(a.hi + node);
+    double mid = mid_of(lo, hi);
+    int64_t split = dt_lower_bound(a.xs, s, e, mid);
+    int64_t c = first_child;
+    int64_t l_slot = -1, r_slot = -1;
+    if (split > s) {  // (lo, mid): child_hi == mid -> left
+        write_node(a, c, lo, mid, lev + 1, s, split);
+        l_slot = c;
+        ++c;
+    }
+    if (e > split) {  // (mid, hi): left iff hi == mid (tree.py:205-208)
+        write_node(a, c, mid, hi, lev + 1, split, e);
+        if (hi == mid)
+            l_slot = c;
+        else
+            r_slot = c;
+    }
+    a.left[node] = l_slot;
+    a.right[node] = r_slot;
+    if (a.packed) {
+        a.packed[node].left = (int32_t)l_slot;
+        a.packed[node].right = (int32_t)r_slot;
+    }
+}
+
+// Block-wide exclusive scan of ints; returns the block total.
+__device__ int block_excl_scan(int v, int *excl, int *warp_sums)
+{
+    const int lane = dt_lane(), warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    int x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        int t = __shfl_up_sync(DT_FULL, x, o);
+        if (lane >= o)
+            x += t;
+    }
+    if (lane == 31)
+        warp_sums[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+        int w = lane < nw ? warp_sums[lane] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            int t = __shfl_up_sync(DT_FULL, w, o);
+            if (lane >= o)
+                w += t;
+        }
+        if (lane < nw)
+            warp_sums[lane] = w;
+    }
+    __syncthreads();
+    int base = warp > 0 ? warp_sums[warp - 1] : 0;
+    int total = warp_sums[nw - 1];
+    __syncthreads();
+    *excl = base + x - v;
+    return total;
+}
+
+// Process frontier [f0, f1) of level `lev` entirely inside the calling block.
+// Returns the number of children written (or -1 on capacity overflow).
+__device__ int64_t level_in_block(const BuildArgs &a, int64_t f0, int64_t f1, int64_t lev,
+                                  int *warp_sums, int64_t *leaves)
+{
+    int64_t next = f1;
+    int64_t leaf_acc = 0;
+    for (int64_t t0 = f0; t0 < f1; t0 += blockDim.x) {
+        int64_t node = t0 + threadIdx.x;
+        int64_t split = 0;
+        int nc = node < f1 ? node_children(a, node, lev, &split) : 0;
+        if (node < f1 && nc == 0)
+            ++leaf_acc;
+        int excl;
+        int tot = block_excl_scan(nc, &excl, warp_sums);
+        if (next + tot > a.capacity)
+            return -1;
+        if (nc)
+            emit_children(a, node, lev, next + excl);
+        next += tot;
+    }
+    *leaves += leaf_acc;
+    return next - f1;
+}
+
+__global__ void __launch_bounds__(BUILD_THREADS) build_kernel(BuildArgs a)
+{
+    cg::grid_group grid = cg::this_grid();
+    __shared__ int warp_sums[BUILD_THREADS / 32];
+    __shared__ int64_t sh_i64[4];
+    volatile int64_t *meta = a.meta;
+    const int G = gridDim.x;
+
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        for (int i = 0; i < DT_META_WORDS; ++i)
+            a.meta[i] = 0;
+        a.meta[DT_META_LEVEL0 + 0] = 0;
+        a.meta[DT_META_LEVEL0 + 1] = 1;
+        a.meta[DT_META_NODES] = 1;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        // tree.py:173-175: pad = 1e-12 * max(1.0, |x0|, |x_last|)
+        const double x0 = a.xs[0], xl = a.xs[a.n - 1];
+        const double m = fmax(1.0, fmax(fabs(x0), fabs(xl)));
+        const double pad = __dmul_rn(1e-12, m);
+        write_node(a, 0, __dsub_rn(x0, pad), __dadd_rn(xl, pad), 0, 0, a.n);
+    }
+    grid.sync();
+
+    int64_t lev = 0;
+    while (lev <= a.max_depth) {
+        int64_t f0 = meta[DT_META_LEVEL0 + lev];
+        int64_t f1 = meta[DT_META_LEVEL0 + lev + 1];
+        int64_t F = f1 - f0;
+        if (F == 0 || meta[DT_META_OVERFLOW])
+            break;
+        if (F <= SMALL_LEVEL) {
+            // block 0 runs consecutive small levels; the others wait at the barrier
+            if (blockIdx.x == 0) {
+                int64_t leaves = 0;
+                int64_t l = lev;
+                while (true) {
+                    int64_t g0 = meta[DT_META_LEVEL0 + l];
+                    int64_t g1 = meta[DT_META_LEVEL0 + l + 1];
+                    int64_t Fl = g1 - g0;
+                    if (Fl == 0 || Fl > SMALL_LEVEL || l > a.max_depth)
+                        break;
+                    int64_t made = level_in_block(a, g0, g1, l, warp_sums, &leaves);
+                    __syncthreads();
+                    if (made < 0) {
+                        if (threadIdx.x == 0)
+                            a.meta[DT_META_OVERFLOW] = 1;
+                        break;
+                    }
+                    if (threadIdx.x == 0) {
+                        a.meta[DT_META_LEVEL0 + l + 2] = g1 + made;
+                        a.meta[DT_META_NODES] = g1 + made;
+                        if (made > 0)
+                            a.meta[DT_META_DEPTH] = l + 1;
+                    }
+                    __threadfence_block();
+                    __syncthreads();
+                    ++l;
+                }
+                // leaves counted per thread: reduce
+                int64_t lv = leaves;
+                for (int o = 16; o > 0; o >>= 1)
+                    lv += __shfl_xor_sync(DT_FULL, lv, o);
+                if (dt_lane() == 0 && lv)
+                    atomicAdd((unsigned long long *)&a.meta[DT_META_LEAVES],
+                              (unsigned long long)lv);
+                if (threadIdx.x == 0)
+                    a.meta[DT_META_CURLEVEL] = l;
+                __threadfence();
+            }
+            grid.sync();
+            lev = meta[DT_META_CURLEVEL];
+            continue;
+        }
+        // ---- big level: all blocks, contiguous chunk per block
+        const int64_t chunk = (F + G - 1) / G;
+        const int64_t b0 = f0 + (int64_t)blockIdx.x * chunk;
+        const int64_t b1 = min(f1, b0 + chunk);
+        int64_t run = 0, leaves = 0;
+        for (int64_t t0 = b0; t0 < b1; t0 += blockDim.x) {
+            int64_t node = t0 + threadIdx.x;
+            int64_t split = 0;
+            int nc = node < b1 ? node_children(a, node, lev, &split) : 0;
+            if (node < b1 && nc == 0)
+                ++leaves;
+            int excl;
+            int tot = block_excl_scan(nc, &excl, warp_sums);
+            if (node < b1)
+                a.scratch_off[node - f0] = (int32_t)(run + excl);
+            run += tot;
+        }
+        if (threadIdx.x == 0)
+            a.block_total[blockIdx.x] = run;
+        {
+            int64_t lv = leaves;
+            for (int o = 16; o > 0; o >>= 1)
+                lv += __shfl_xor_sync(DT_FULL, lv, o);
+            if (dt_lane() == 0 && lv)
+                atomicAdd((unsigned long long *)&a.meta[DT_META_LEAVES], (unsigned long long)lv);
+        }
+        grid.sync();
+        // block base and level total, fixed-order sums
+        if (threadIdx.x < 32) {
+            int64_t base = 0, total = 0;
+            for (int b = threadIdx.x; b < G; b += 32) {
+                int64_t v = ((volatile int64_t *)a.block_total)[b];
+                total += v;
+                if (b < (int)blockIdx.x)
+                    base += v;
+            }
+            for (int o = 16; o > 0; o >>= 1) {
+                base += __shfl_xor_sync(DT_FULL, base, o);
+                total += __shfl_xor_sync(DT_FULL, total, o);
+            }
+            if (threadIdx.x == 0) {
+                sh_i64[0] = base;
+                sh_i64[1] = total;
+            }
+        }
+        __syncthreads();
+        const int64_t base = sh_i64[0], total = sh_i64[1];
+        if (f1 + total > a.capacity) {
+            if (blockIdx.x == 0 && threadIdx.x == 0)
+                a.meta[DT_META_OVERFLOW] = 1;
+            break;  // every block sees the same total
+        }
+        for (int64_t node = b0 + threadIdx.x; node < b1; node += blockDim.x) {
+            int64_t s = ld_cg(a.start + node), e = ld_cg(a.end + node);
+            if (e - s <= a.leaf_capacity || lev >= a.max_depth)
+                continue;
+            emit_children(a, node, lev, f1 + base + __ldcg(a.scratch_off + (node - f0)));
+        }
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            a.meta[DT_META_LEVEL0 + lev + 2] = f1 + total;
+            a.meta[DT_META_NODES] = f1 + total;
+            if (total > 0)
+                a.meta[DT_META_DEPTH] = lev + 1;
+        }
+        grid.sync();
+        ++lev;
+    }
+}
+
+}  // namespace
+
+extern "C" size_t dt_build_workspace(int64_t n, int64_t node_capacity)
+{
+    (void)n;
+    return (size_t)node_capacity * sizeof(int32_t) + 4096 * sizeof(int64_t);
+}
+
+extern "C" int dt_build_tree(const double *xs, int64_t n, int64_t leaf_capacity, int64_t max_depth, int64_t node_capacity,
+                             double *lo, double *hi, double *center, double *half,
+                             int64_t *level, int64_t *start, int64_t *end, int64_t *left,
+                             int64_t *right, void *packed, int64_t *meta, void *workspace,
+                             size_t workspace_bytes, void *stream)
+{
+    DT_CHECK_ARG(n > 0, "cannot build a tree over an empty charge system");
+    DT_CHECK_ARG(n < (int64_t)1 << 31, "n must be < 2^31");
+    DT_CHECK_ARG(leaf_capacity >= 1, "leaf_capacity must be >= 1");
+    DT_CHECK_ARG(max_depth >= 0 && max_depth <= DT_MAX_DEPTH, "max_depth must be in [0, 60]");
+    DT_CHECK_ARG(node_capacity >= 1 && node_capacity < (int64_t)1 << 31,
+                 "node_capacity must be in [1, 2^31)");
+    DT_CHECK_ARG(xs && lo && hi && center && half && level && start && end && left && right &&
+                     meta,
+                 "null pointer");
+    if (!workspace || workspace_bytes < dt_build_workspace(n, node_capacity))
+        return dt_set_error(DT_ERR_WORKSPACE, "build workspace too small");
+
+    BuildArgs a;
+    a.xs = xs;
+    a.n = n;
+    a.leaf_capacity = leaf_capacity;
+    a.max_depth = max_depth;
+    a.capacity = node_capacity;
+    a.lo = lo;
+    a.hi = hi;
+    a.center = center;
+    a.half = half;
+    a.level = level;
+    a.start = start;
+    a.end = end;
+    a.left = left;
+    a.right = right;
+    a.packed = (dt_node *)packed;
+    a.meta = meta;
+    a.scratch_off = (int32_t *)workspace;
+    a.block_total = (int64_t *)((char *)workspace + (size_t)node_capacity * sizeof(int32_t));
+    // 8-byte align block_total
+    a.block_total = (int64_t *)(((uintptr_t)a.block_total + 7) & ~(uintptr_t)7);
+
+    int dev = 0, per_sm = 0;
+    DT_CUDA_TRY(cudaGetDevice(&dev));
+    DT_CUDA_TRY(
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, build_kernel, BUILD_THREADS, 0));
+    if (per_sm < 1)
+        return dt_set_error(DT_ERR_CUDA, "build kernel cannot be resident");
+    int grid = dt_num_sms() * (per_sm > 2 ? 2 : per_sm);
+    if (grid > 3000)
+        grid = 3000;
+    void *args[] = {&a};
+    DT_CUDA_TRY(cudaLaunchCooperativeKernel((const void *)build_kernel, grid, BUILD_THREADS, args,
+                                            0, (cudaStream_t)stream));
+    return DT_OK;
+}

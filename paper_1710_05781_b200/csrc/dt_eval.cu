@@ -1,0 +1,767 @@
+// (d)+(e) Tree field evaluation: warp-coherent traversal, far field with
+// adaptive truncation order, near field by direct summation.
+//
+// Reference: _kernels.py:163-266 (tree_phi_sum), the numba kernel behind
+// evaluate_all (tree.py:318-373).  Per target the reference walks the tree
+// depth-first (left subtree first): a node with R = |c - y| > 0 and
+// h <= theta*R contributes sum_k Phi^(k)(c, y) m_k, k <= p_use (Eq. 10
+// recurrence); an unaccepted leaf contributes its direct pair sum; anything
+// else descends.
+//
+// B200 mapping: one warp owns 32 consecutive (sorted) targets and walks the
+// UNION of their traversals with a per-entry lane mask (stack in shared
+// memory).  Each lane applies the reference's MAC to its own target, so the
+// per-target interaction lists -- and their DFS order -- are exactly the
+// reference's.  Warps pull 32-target chunks from a global counter
+// (persistent grid, 148 x k CTAs).
+//   far   accepting lanes evaluate the recurrence together up to the warp's
+//         largest order; the moment row is a broadcast load.
+//   near  lanes that reach an unaccepted leaf sum its (x, q) pairs, read as
+//         one broadcast 16-byte load per source; rsqrt = MUFU seed + one
+//         cubic Newton step.
+// Adaptive order (reference lines 212-231): the reference samples
+// |f| = |w / sqrt(w^2 + r_d^2)| at 64 contour points per accepted pair with
+// complex arithmetic.  On the contour |f|^4 = 1 / ((1 - s*/s_t)^2 + s*) with
+// s_t = |e^{i theta_t} - 1|^2 and s* = r_d^2 / R^2, unimodal in t, so the
+// sampled maximum sits at the samples bracketing s_t = s*.  Tier 1 evaluates
+// that closed form in fp32 and solves the bound scan for p directly (two
+// logarithms); when the result lies within DT_PSEL_MARGIN of an integer
+// decision boundary, tier 2 re-runs the reference's exact double-precision
+// operation sequence (numpy csqrt, CPython complex quotient, glibc's
+// hypot, the fused forms LLVM emitted) on the bracketing samples and their
+// mirrors, and tier 3 (tiny s*, out-of-range inputs or DT_PSEL_EXACT) on all
+// samples.  The chosen orders are bit-identical to the reference's.
+#include "dt_common.cuh"
+
+namespace {
+
+constexpr int EVAL_THREADS = 256;
+constexpr int EVAL_WARPS = EVAL_THREADS / 32;
+constexpr int STACK_DEPTH = 64;         // >= max_depth + 2
+constexpr int MAX_SAMPLES = 256;
+constexpr float PSEL_MARGIN = 5e-5f;    // in units of the order axis
+constexpr double CONTOUR_SAFETY = 1.1;  // kernel.py:27
+
+struct EvalArgs {
+    const dt_node *nodes;
+    int64_t n_nodes;
+    const double *moments;
+    int64_t stride;
+    const double2 *xq;
+    double rd2, theta;
+    int p;
+    int p_cap;
+    double tol_share;
+    const double *cos_tab, *sin_tab;
+    int n_samples;
+    const double *ys;
+    double *out;
+    int64_t i0, i1;
+    int accumulate;
+    int psel_mode;
+    dt_eval_stats stats;
+    unsigned long long *counter;
+    const int64_t *meta;  // if set: tol_share = tolerance / (3 max(depth, 1)) on device
+    double tolerance;
+};
+
+// tree.py:268-270 _tol_share, evaluated from the device-side tree depth.
+__device__ __forceinline__ double tol_share_of(const EvalArgs &a)
+{
+    if (!a.meta)
+        return a.tol_share;
+    const int64_t depth = __ldg(a.meta + DT_META_DEPTH);
+    return __ddiv_rn(a.tolerance, __dmul_rn(3.0, (double)(depth > 1 ? depth : 1)));
+}
+
+// ------------------------------------------------------------------ exact tier
+
+// hypot(a, b): the corrected algorithm of C. F. Borges, "An improved
+// algorithm for hypot(a, b)" (2019), non-FMA variant -- what glibc 2.35+
+// libm computes on x86-64 (checked bit-for-bit against glibc 2.39 on 2e7
+// random pairs, including near-equal arguments).  The reference reaches it
+// through numba's abs(complex) and cmath.sqrt.  Arguments in this kernel
+// are far from the overflow/underflow ranges where libm rescales.
+__device__ double dt_hypot(double a, double b)
+{
+    double ax = fabs(a), ay = fabs(b);
+    if (ax < ay) {
+        double t = ax;
+        ax = ay;
+        ay = t;
+    }
+    if (ay <= __dmul_rn(ax, 0x1p-54))
+        return __dadd_rn(ax, ay);
+    double h = __dsqrt_rn(__dadd_rn(__dmul_rn(ax, ax), __dmul_rn(ay, ay)));
+    double t1, t2;
+    if (h <= __dmul_rn(2.0, ay)) {
+        const double delta = __dsub_rn(h, ay);
+        t1 = __dmul_rn(ax, __dsub_rn(__dmul_rn(2.0, delta), ax));
+        t2 = __dmul_rn(__dsub_rn(delta, __dmul_rn(2.0, __dsub_rn(ax, ay))), delta);
+    } else {
+        const double delta = __dsub_rn(h, ax);
+        t1 = __dmul_rn(__dmul_rn(2.0, delta), __dsub_rn(ax, __dmul_rn(2.0, ay)));
+        t2 = __dadd_rn(__dmul_rn(__dsub_rn(__dmul_rn(4.0, delta), ay), ay),
+                       __dmul_rn(delta, delta));
+    }
+    return __dsub_rn(h, __ddiv_rn(__dadd_rn(t1, t2), __dmul_rn(2.0, h)));
+}
+
+// numpy npy_csqrt / numba cmathimpl.sqrt_impl (CACM 312), finite inputs.
+__device__ void np_csqrt(double a, double b, double *re, double *im)
+{
+    const double thres = 0x1.a827999fcef32p+1021;
+    bool scale = false;
+    if (fabs(a) >= thres || fabs(b) >= thres) {
+        a = __dmul_rn(a, 0.25);
+        b = __dmul_rn(b, 0.25);
+        scale = true;
+    }
+    double r, i;
+    double hyp = dt_hypot(a, b);
+    if (a >= 0.0) {
+        double t = __dsqrt_rn(__dmul_rn(__dadd_rn(a, hyp), 0.5));
+        r = t;
+        i = __ddiv_rn(b, __dadd_rn(t, t));
+    } else {
+        double t = __dsqrt_rn(__dmul_rn(__dsub_rn(hyp, a), 0.5));
+        r = __ddiv_rn(fabs(b), __dadd_rn(t, t));
+        i = copysign(t, b);
+    }
+    if (scale)
+        r = __dadd_rn(r, r);
+    *re = r;
+    *im = i;
+}
+
+// |f| at one contour sample, exactly as the compiled reference computes it.
+__device__ double contour_sample(double big_r, double c, double s, double rd2)
+{
+    double wr = __fma_rn(big_r, c, -big_r);
+    double wi = __dmul_rn(big_r, s);
+    double wi2 = __dmul_rn(wi, wi);
+    double zr = __fma_rn(wr, wr, -wi2);
+    double pr = __dmul_rn(wr, wi);
+    double zi = __dadd_rn(pr, pr);
+    double a = __dadd_rn(zr, rd2);
+    double b = __dadd_rn(zi, 0.0);
+    double sr, si;
+    np_csqrt(a, b, &sr, &si);
+    double re, im;
+    if (fabs(sr) >= fabs(si)) {
+        double ratio = __ddiv_rn(si, sr);
+        double denom = __fma_rn(ratio, si, sr);
+        re = __ddiv_rn(__fma_rn(wi, ratio, wr), denom);
+        im = __ddiv_rn(__fma_rn(-wr, ratio, wi), denom);
+    } else {
+        double ratio = __ddiv_rn(sr, si);
+        double denom = __fma_rn(ratio, sr, si);
+        re = __ddiv_rn(__fma_rn(wr, ratio, wi), denom);
+        im = __ddiv_rn(__fma_rn(wi, ratio, -wr), denom);
+    }
+    return dt_hypot(re, im);
+}
+
+// value -> order scan (reference lines 224-231, value reassociated as compiled)
+__device__ int exact_scan(double m_max, double big_r, double h, double tol, int p_cap)
+{
+    double ratio = __ddiv_rn(h, big_r);
+    double m1 = __dmul_rn(m_max, CONTOUR_SAFETY);
+    double value = __ddiv_rn(__dmul_rn(__dmul_rn(big_r, m1), ratio), __dsub_rn(big_r, h));
+    for (int cand = 0; cand < p_cap; ++cand) {
+        if (value <= tol)
+            return cand;
+        value = __dmul_rn(value, ratio);
+    }
+    return p_cap;
+}
+
+__device__ int psel_exact_all(double big_r, double h, const EvalArgs &a, const double *cs,
+                              const double *sn)
+{
+    double m = 0.0;
+    for (int t = 0; t < a.n_samples; ++t) {
+        double fv = contour_sample(big_r, cs[t], sn[t], a.rd2);
+        if (fv > m)
+            m = fv;
+    }
+    return exact_scan(m, big_r, h, a.tol_share, a.p_cap);
+}
+
+__device__ int psel_exact_bracket(double big_r, double h, int t0, const EvalArgs &a,
+                                  const double *cs, const double *sn)
+{
+    double m = 0.0;
+#pragma unroll 1
+    for (int c = -1; c <= 2; ++c) {
+        int t = min(max(t0 + c, 1), 32);
+        double fv = contour_sample(big_r, cs[t], sn[t], a.rd2);
+        if (fv > m)
+            m = fv;
+        int tm = 64 - t;
+        if (tm != t) {
+            fv = contour_sample(big_r, cs[tm], sn[tm], a.rd2);
+            if (fv > m)
+                m = fv;
+        }
+    }
+    return exact_scan(m, big_r, h, a.tol_share, a.p_cap);
+}
+
+// ------------------------------------------------------------------ fast tier
+
+// log2(x) = e + f for normal x > 0, f = log2(mantissa) in [0, 1).
+__device__ __forceinline__ void split_log2(float x, int *e, float *f)
+{
+    int bits = __float_as_int(x);
+    *e = ((bits >> 23) & 0xff) - 127;
+    *f = log2f(__int_as_float((bits & 0x007fffff) | 0x3f800000));
+}
+
+// Returns p >= 0 on a confident decision, or -(t0 + 2) (<= -2) when the
+// decision is within the margin (tier 2 with bracket t0), or -1 for tier 3.
+__device__ int psel_fast(double big_r, double h, const EvalArgs &a, const float *isig,
+                         float rd2f, float inv_tol_f)
+{
+    if (h == 0.0)
+        return 0;  // value == 0 <= tol at cand 0
+    const float Rf = (float)big_r;
+    const float hf = (float)h;
+    if (!(Rf > 1e-15f && Rf < 1e15f && hf > 1e-30f))
+        return -1;
+    const float ratio = hf / Rf;
+    const float sstar = rd2f / (Rf * Rf);
+    if (!(sstar > 1e-12f) || !(sstar < 1e30f))
+        return -1;
+    // bracket: s_t = 4 sin^2(pi t / 64) = s*  ->  t* = (64/pi) asin(sqrt(s*)/2)
+    const float z = fminf(1.0f, 0.5f * sqrtf(sstar));
+    const int t0 = (int)floorf(asinf(z) * 20.371832715762604f);
+    float emin = 3.0e38f;
+#pragma unroll
+    for (int c = -1; c <= 2; ++c) {
+        int t = min(max(t0 + c, 1), 32);
+        float u = sstar * isig[t];
+        float e = (1.0f - u) * (1.0f - u);
+        emin = fminf(emin, e);
+    }
+    const float Q = emin + sstar;        // M^-4
+    const float M = rsqrtf(sqrtf(Q));    // sampled contour maximum of |f|
+    const float X = 1.1f * M * (ratio / (1.0f - ratio)) * inv_tol_f;  // value_0 / tol
+    if (!(X > 1e-37f && X < 1e37f))
+        return -1;
+    int ex, er;
+    float fx, fr;
+    split_log2(X, &ex, &fx);
+    split_log2(ratio, &er, &fr);
+    const float L = -((float)er + fr);   // -log2(ratio) > 0
+    const float pstar_approx = ((float)ex + fx) / L;
+    if (pstar_approx < -1.0f)
+        return 0;
+    if (pstar_approx > (float)a.p_cap + 1.0f)
+        return a.p_cap;
+    const int n = __float2int_rn(pstar_approx);
+    // residual N - n L with the integer parts kept exact
+    const float resid = (float)(ex + n * er) + fmaf((float)n, fr, fx);
+    const float dist = resid / L;  // pstar - n
+    if (fabsf(dist) < PSEL_MARGIN && n >= 0 && n <= a.p_cap - 1)
+        return -(t0 + 2);
+    int p = dist > 0.0f ? n + 1 : n;
+    p = max(p, 0);
+    return min(p, a.p_cap);
+}
+
+// ------------------------------------------------------------------ far / near
+
+__device__ __forceinline__ double far_field(double d, double rd2, const double *__restrict__ m,
+                                            int pu, int pmax)
+{
+    const double s2 = __fma_rn(d, d, rd2);
+    const double r = dt_rsqrt(s2);
+    const double f0 = d * r;
+    double acc = f0 * __ldg(m);
+    if (pmax < 1)
+        return acc;
+    const double ir2 = r * r;              // 1 / s2
+    double f1 = rd2 * r * ir2;             // rd2 / s2^(3/2)
+    if (pu >= 1)
+        acc = __fma_rn(f1, __ldg(m + 1), acc);
+    if (pmax < 2)
+        return acc;
+    const double inv = ir2 * dt_rcp(d);    // 1 / (d s2)
+    const double ir3 = 3.0 * ir2;          // 3 d / (d s2)
+    const double ci = __fma_rn(3.0 * d, d, rd2) * inv;  // (3 d^2 + rd2) / (d s2)
+    double ak = rd2 * inv;                 // A_k / (d s2), A_k = rd2 - (k-1) C
+    double f2 = f0, f3 = 0.0;
+#pragma unroll 2
+    for (int k = 2; k <= pmax; ++k) {
+        ak -= ci;
+        const double km1 = (double)(k - 1);
+        double t = ak * f1;
+        if (k >= 3)
+            t = __fma_rn(-(km1 * (double)(k - 2)) * ir3, f2, t);
+        if (k >= 4)
+            t = __fma_rn(-(km1 * (double)((k - 2) * (k - 3))) * inv, f3, t);
+        f3 = f2;
+        f2 = f1;
+        f1 = t;
+        if (k <= pu)
+            acc = __fma_rn(t, __ldg(m + k), acc);
+    }
+    return acc;
+}
+
+__device__ __forceinline__ double near_field(const double2 *__restrict__ xq, int s, int e,
+                                             double y, double rd2)
+{
+    double a0 = 0.0, a1 = 0.0;
+    int j = s;
+    for (; j + 1 < e; j += 2) {
+        const double2 u = __ldg(xq + j);
+        const double2 v = __ldg(xq + j + 1);
+        const double du = u.x - y, dv = v.x - y;
+        const double ru = dt_rsqrt(__fma_rn(du, du, rd2));
+        const double rv = dt_rsqrt(__fma_rn(dv, dv, rd2));
+        a0 = __fma_rn(u.y * du, ru, a0);
+        a1 = __fma_rn(v.y * dv, rv, a1);
+    }
+    if (j < e) {
+        const double2 u = __ldg(xq + j);
+        const double du = u.x - y;
+        a0 = __fma_rn(u.y * du, dt_rsqrt(__fma_rn(du, du, rd2)), a0);
+    }
+    return a0 + a1;
+}
+
+#define FNV_OFF 1469598103934665603ULL
+#define FNV_MUL 1099511628211ULL
+
+template <bool ADAPTIVE, bool STATS>
+__global__ void __launch_bounds__(EVAL_THREADS) tree_eval_kernel(EvalArgs a)
+{
+    if (ADAPTIVE)
+        a.tol_share = tol_share_of(a);
+    __shared__ int2 stack_s[EVAL_WARPS][STACK_DEPTH];
+    __shared__ float isig_s[33];
+    __shared__ double cos_s[MAX_SAMPLES], sin_s[MAX_SAMPLES];
+    const int lane = dt_lane(), warp = threadIdx.x >> 5;
+    const bool tables_in_smem = a.n_samples <= MAX_SAMPLES;
+    if (ADAPTIVE) {
+        if (tables_in_smem) {
+            for (int t = threadIdx.x; t < a.n_samples; t += blockDim.x) {
+                cos_s[t] = a.cos_tab[t];
+                sin_s[t] = a.sin_tab[t];
+            }
+        }
+        if (threadIdx.x <= 32) {
+            int t = threadIdx.x;
+            // s_t = (cos - 1)^2 + sin^2, the |w|^2 / R^2 of the reference's samples
+            double c = a.n_samples == 64 ? a.cos_tab[t] : 1.0;
+            double s = a.n_samples == 64 ? a.sin_tab[t] : 0.0;
+            double sig = (c - 1.0) * (c - 1.0) + s * s;
+            isig_s[t] = sig > 0.0 ? (float)(1.0 / sig) : 3.0e38f;
+        }
+        __syncthreads();
+    }
+    const double *cs = tables_in_smem ? cos_s : a.cos_tab;
+    const double *sn = tables_in_smem ? sin_s : a.sin_tab;
+    const bool fast_ok = a.n_samples == 64 && a.psel_mode == DT_PSEL_FAST;
+    const float rd2f = (float)a.rd2;
+    const float inv_tol_f = (float)(1.0 / a.tol_share);
+    int2 *stack = stack_s[warp];
+
+    while (true) {
+        unsigned long long base = 0;
+        if (lane == 0)
+            base = atomicAdd(a.counter, 32ull);
+        base = __shfl_sync(DT_FULL, base, 0);
+        const int64_t i_first = a.i0 + (int64_t)base;
+        if (i_first >= a.i1)
+            break;
+        const int64_t i = i_first + lane;
+        const bool valid = i < a.i1;
+        const double y = valid ? __ldg(a.ys + i) : 0.0;
+        double acc = 0.0;
+        uint64_t hh = FNV_OFF;
+        int64_t c_near = 0, c_far = 0, c_sump = 0, c_p0 = 0, c_exact = 0;
+
+        int top = 0;
+        const unsigned vmask = __ballot_sync(DT_FULL, valid);
+        if (lane == 0)
+            stack[0] = make_int2(0, (int)vmask);
+        __syncwarp();
+        while (top >= 0) {
+            const int2 ent = stack[top];
+            --top;
+            __syncwarp();
+            const int node = ent.x;
+            const unsigned mask = (unsigned)ent.y;
+            const double4 raw0 = *reinterpret_cast<const double4 *>(a.nodes + node);
+            const double center = raw0.x, half = raw0.y;
+            const int2 lr = make_int2(__double2loint(raw0.z), __double2hiint(raw0.z));
+            const int2 se = make_int2(__double2loint(raw0.w), __double2hiint(raw0.w));
+            const bool act = (mask >> lane) & 1u;
+            const double d = center - y;
+            const double big_r = fabs(d);
+            const bool far = act && big_r > 0.0 && half <= __dmul_rn(a.theta, big_r);
+            const unsigned fm = __ballot_sync(DT_FULL, far);
+            if (fm) {
+                int pu = -1;
+                if (far) {
+                    if (ADAPTIVE) {
+                        int r = fast_ok ? psel_fast(big_r, half, a, isig_s, rd2f, inv_tol_f) : -1;
+                        if (r < 0) {
+                            if (r <= -2 && fast_ok)
+                                r = psel_exact_bracket(big_r, half, -r - 2, a, cs, sn);
+                            else
+                                r = psel_exact_all(big_r, half, a, cs, sn);
+                            if (STATS)
+                                ++c_exact;
+                        }
+                        pu = r;
+                    } else {
+                        pu = a.p;
+                    }
+                }
+                const int pmax = __reduce_max_sync(DT_FULL, pu);
+                if (far) {
+                    acc += far_field(d, a.rd2, a.moments + (int64_t)node * a.stride, pu, pmax);
+                    if (STATS) {
+                        hh = (hh ^ ((uint64_t)node * 256u + (uint64_t)pu)) * FNV_MUL;
+                        ++c_far;
+                        c_sump += pu;
+                        c_p0 += pu == 0;
+                    }
+                }
+            }
+            const unsigned rest = mask & ~fm;
+            if (rest) {
+                if (lr.x < 0 && lr.y < 0) {
+                    if ((rest >> lane) & 1u) {
+                        acc += near_field(a.xq, se.x, se.y, y, a.rd2);
+                        if (STATS) {
+                            hh = (hh ^ ((uint64_t)node * 256u + 255u)) * FNV_MUL;
+                            c_near += se.y - se.x;
+                        }
+                    }
+                } else {
+                    if (lane == 0) {
+                        if (lr.y >= 0)
+                            stack[++top] = make_int2(lr.y, (int)rest);
+                        if (lr.x >= 0)
+                            stack[++top] = make_int2(lr.x, (int)rest);
+                    } else {
+                        top += (lr.y >= 0) + (lr.x >= 0);
+                    }
+                    __syncwarp();
+                }
+            }
+        }
+        if (valid) {
+            a.out[i] = a.accumulate ? a.out[i] + acc : acc;
+            if (STATS) {
+                if (a.stats.hash)
+                    a.stats.hash[i] = hh;
+                if (a.stats.near_pairs)
+                    a.stats.near_pairs[i] = c_near;
+                if (a.stats.n_far)
+                    a.stats.n_far[i] = c_far;
+                if (a.stats.sum_p)
+                    a.stats.sum_p[i] = c_sump;
+                if (a.stats.n_p0)
+                    a.stats.n_p0[i] = c_p0;
+                if (a.stats.n_exact)
+                    a.stats.n_exact[i] = c_exact;
+            }
+        }
+    }
+}
+
+__global__ void pack_tree_kernel(const double *__restrict__ c, const double *__restrict__ h,
+                                 const int64_t *__restrict__ s, const int64_t *__restrict__ e,
+                                 const int64_t *__restrict__ l, const int64_t *__restrict__ r,
+                                 int64_t n, dt_node *__restrict__ out)
+{
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n)
+        return;
+    dt_node nd;
+    nd.center = c[i];
+    nd.half = h[i];
+    nd.left = (int32_t)l[i];
+    nd.right = (int32_t)r[i];
+    nd.start = (int32_t)s[i];
+    nd.end = (int32_t)e[i];
+    out[i] = nd;
+}
+
+__global__ void pack_sources_kernel(const double *__restrict__ xs, const double *__restrict__ qs,
+                                    int64_t n, double2 *__restrict__ xq)
+{
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n)
+        xq[i] = make_double2(xs[i], qs[i]);
+}
+
+__global__ void choose_p_kernel(const double *__restrict__ R, const double *__restrict__ H,
+                                int64_t n, EvalArgs a, int64_t *__restrict__ p_out,
+                                int32_t *__restrict__ tier_out)
+{
+    __shared__ float isig_s[33];
+    if (threadIdx.x <= 32) {
+        int t = threadIdx.x;
+        double c = a.n_samples == 64 ? a.cos_tab[t] : 1.0;
+        double s = a.n_samples == 64 ? a.sin_tab[t] : 0.0;
+        double sig = (c - 1.0) * (c - 1.0) + s * s;
+        isig_s[t] = sig > 0.0 ? (float)(1.0 / sig) : 3.0e38f;
+    }
+    __syncthreads();
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n)
+        return;
+    const bool fast_ok = a.n_samples == 64 && a.psel_mode == DT_PSEL_FAST;
+    int r = fast_ok ? psel_fast(R[i], H[i], a, isig_s, (float)a.rd2, (float)(1.0 / a.tol_share))
+                    : -1;
+    int tier = 0;
+    if (r < 0) {
+        if (r <= -2 && fast_ok) {
+            r = psel_exact_bracket(R[i], H[i], -r - 2, a, a.cos_tab, a.sin_tab);
+            tier = 1;
+        } else {
+            r = psel_exact_all(R[i], H[i], a, a.cos_tab, a.sin_tab);
+            tier = 2;
+        }
+    }
+    p_out[i] = r;
+    if (tier_out)
+        tier_out[i] = tier;
+}
+
+int launch_eval(EvalArgs &a, bool adaptive, bool stats, cudaStream_t s)
+{
+    DT_CUDA_TRY(cudaMemsetAsync(a.counter, 0, sizeof(unsigned long long), s));
+    int per_sm = 0;
+    const void *fn;
+    if (adaptive)
+        fn = stats ? (const void *)tree_eval_kernel<true, true>
+                   : (const void *)tree_eval_kernel<true, false>;
+    else
+        fn = stats ? (const void *)tree_eval_kernel<false, true>
+                   : (const void *)tree_eval_kernel<false, false>;
+    DT_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, EVAL_THREADS, 0));
+    if (per_sm < 1)
+        per_sm = 1;
+    int64_t warps_needed = (a.i1 - a.i0 + 31) / 32;
+    int64_t grid = (int64_t)dt_num_sms() * per_sm;
+    int64_t max_useful = (warps_needed + EVAL_WARPS - 1) / EVAL_WARPS;
+    if (grid > max_useful)
+        grid = max_useful;
+    if (grid < 1)
+        grid = 1;
+    void *args[] = {&a};
+    DT_CUDA_TRY(cudaLaunchKernel(fn, dim3((unsigned)grid), dim3(EVAL_THREADS), args, 0, s));
+    return DT_OK;
+}
+
+}  // namespace
+
+extern "C" int dt_pack_sources(const double *xs, const double *qs, int64_t n, double *xq,
+                               void *stream)
+{
+    DT_CHECK_ARG(n >= 0, "negative size");
+    if (n == 0)
+        return DT_OK;
+    DT_CHECK_ARG(xs && qs && xq, "null pointer");
+    pack_sources_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+        xs, qs, n, (double2 *)xq);
+    DT_CUDA_TRY(cudaGetLastError());
+    return DT_OK;
+}
+
+extern "C" int dt_pack_tree(const double *centers, const double *halves, const int64_t *starts,
+                            const int64_t *ends, const int64_t *lefts, const int64_t *rights,
+                            int64_t n_nodes, void *packed, void *stream)
+{
+    DT_CHECK_ARG(n_nodes >= 0 && n_nodes < (int64_t)1 << 31, "bad node count");
+    if (n_nodes == 0)
+        return DT_OK;
+    DT_CHECK_ARG(centers && halves && starts && ends && lefts && rights && packed, "null pointer");
+    pack_tree_kernel<<<(unsigned)((n_nodes + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+        centers, halves, starts, ends, lefts, rights, n_nodes, (dt_node *)packed);
+    DT_CUDA_TRY(cudaGetLastError());
+    return DT_OK;
+}
+
+extern "C" size_t dt_tree_eval_workspace(int64_t n_nodes, int64_t n_src)
+{
+    return 256 + (size_t)n_nodes * sizeof(dt_node) + (size_t)n_src * 2 * sizeof(double);
+}
+
+static int check_eval_args(int64_t n_nodes, int64_t n_src, int64_t p, int adaptive,
+                           double tol_share, int64_t p_cap, int64_t n_samples, double rd2,
+                           double theta, int64_t i0, int64_t i1, int64_t stride)
+{
+    DT_CHECK_ARG(n_nodes >= 1 && n_nodes < (int64_t)1 << 31, "bad node count");
+    DT_CHECK_ARG(n_src >= 0 && n_src < (int64_t)1 << 31, "bad source count");
+    DT_CHECK_ARG(i0 >= 0 && i1 >= i0, "bad target range");
+    DT_CHECK_ARG(p >= 0 && p < stride, "p must be >= 0 and < moment_stride");
+    DT_CHECK_ARG(rd2 > 0.0, "rd2 must be > 0");
+    DT_CHECK_ARG(theta > 0.0 && theta < 1.0, "theta must lie in (0, 1)");
+    if (adaptive) {
+        DT_CHECK_ARG(tol_share > 0.0, "tol_share must be > 0");
+        DT_CHECK_ARG(p_cap >= 0 && p_cap < stride, "p_cap must be < moment_stride");
+        DT_CHECK_ARG(n_samples >= 1, "n_samples must be >= 1");
+    }
+    return DT_OK;
+}
+
+extern "C" int dt_tree_phi_sum_packed(const void *packed_nodes, int64_t n_nodes,
+                                      const double *moments, int64_t moment_stride,
+                                      const double *xq, int64_t n_src, double rd2, double theta,
+                                      int64_t p, int adaptive, double tol_share, int64_t p_cap,
+                                      const double *cos_tab, const double *sin_tab,
+                                      int64_t n_samples, const double *ys, double *out,
+                                      int64_t i0, int64_t i1, int accumulate, int psel_mode,
+                                      const dt_eval_stats *stats, void *workspace,
+                                      size_t workspace_bytes, void *stream)
+{
+    int rc = check_eval_args(n_nodes, n_src, p, adaptive, tol_share, p_cap, n_samples, rd2,
+                             theta, i0, i1, moment_stride);
+    if (rc != DT_OK)
+        return rc;
+    if (i1 == i0)
+        return DT_OK;
+    DT_CHECK_ARG(packed_nodes && moments && ys && out && (n_src == 0 || xq), "null pointer");
+    DT_CHECK_ARG(!adaptive || (cos_tab && sin_tab), "null contour tables");
+    if (!workspace || workspace_bytes < 64)
+        return dt_set_error(DT_ERR_WORKSPACE, "eval workspace too small");
+    EvalArgs a{};
+    a.nodes = (const dt_node *)packed_nodes;
+    a.n_nodes = n_nodes;
+    a.moments = moments;
+    a.stride = moment_stride;
+    a.xq = (const double2 *)xq;
+    a.rd2 = rd2;
+    a.theta = theta;
+    a.p = (int)p;
+    a.p_cap = (int)p_cap;
+    a.tol_share = adaptive ? tol_share : 1.0;
+    a.cos_tab = cos_tab;
+    a.sin_tab = sin_tab;
+    a.n_samples = (int)n_samples;
+    a.ys = ys;
+    a.out = out;
+    a.i0 = i0;
+    a.i1 = i1;
+    a.accumulate = accumulate;
+    a.psel_mode = psel_mode;
+    if (stats)
+        a.stats = *stats;
+    else
+        a.stats = dt_eval_stats{nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+    a.counter = (unsigned long long *)workspace;
+    return launch_eval(a, adaptive != 0, stats != nullptr, (cudaStream_t)stream);
+}
+
+extern "C" int dt_tree_eval_device(const void *packed_nodes, const int64_t *meta,
+                                   int64_t node_capacity, const double *moments,
+                                   int64_t moment_stride, const double *xq, int64_t n_src,
+                                   double rd2, double theta, int64_t p, int adaptive,
+                                   double tolerance, int64_t p_cap, const double *cos_tab,
+                                   const double *sin_tab, int64_t n_samples, const double *ys,
+                                   double *out, int64_t i0, int64_t i1, int accumulate,
+                                   void *workspace, size_t workspace_bytes, void *stream)
+{
+    DT_CHECK_ARG(meta != nullptr, "null meta");
+    int rc = check_eval_args(node_capacity, n_src, p, adaptive, tolerance, p_cap, n_samples, rd2,
+                             theta, i0, i1, moment_stride);
+    if (rc != DT_OK)
+        return rc;
+    if (i1 == i0)
+        return DT_OK;
+    DT_CHECK_ARG(packed_nodes && moments && ys && out && (n_src == 0 || xq), "null pointer");
+    DT_CHECK_ARG(!adaptive || (cos_tab && sin_tab), "null contour tables");
+    if (!workspace || workspace_bytes < 64)
+        return dt_set_error(DT_ERR_WORKSPACE, "eval workspace too small");
+    EvalArgs a{};
+    a.nodes = (const dt_node *)packed_nodes;
+    a.n_nodes = node_capacity;
+    a.moments = moments;
+    a.stride = moment_stride;
+    a.xq = (const double2 *)xq;
+    a.rd2 = rd2;
+    a.theta = theta;
+    a.p = (int)p;
+    a.p_cap = (int)p_cap;
+    a.tol_share = 1.0;
+    a.tolerance = tolerance;
+    a.meta = adaptive ? meta : nullptr;
+    a.cos_tab = cos_tab;
+    a.sin_tab = sin_tab;
+    a.n_samples = (int)n_samples;
+    a.ys = ys;
+    a.out = out;
+    a.i0 = i0;
+    a.i1 = i1;
+    a.accumulate = accumulate;
+    a.psel_mode = DT_PSEL_FAST;
+    a.stats = dt_eval_stats{nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+    a.counter = (unsigned long long *)workspace;
+    return launch_eval(a, adaptive != 0, false, (cudaStream_t)stream);
+}
+
+extern "C" int dt_tree_phi_sum(const double *centers, const double *halves, const int64_t *starts,
+                               const int64_t *ends, const int64_t *lefts, const int64_t *rights,
+                               const double *moments, int64_t moment_stride, int64_t n_nodes,
+                               const double *xs, const double *qs, int64_t n_src, double rd2,
+                               double theta, int64_t p, int adaptive, double tol_share,
+                               int64_t p_cap, const double *cos_tab, const double *sin_tab,
+                               int64_t n_samples, const double *ys, double *out, int64_t i0,
+                               int64_t i1, int accumulate, void *workspace,
+                               size_t workspace_bytes, void *stream)
+{
+    int rc = check_eval_args(n_nodes, n_src, p, adaptive, tol_share, p_cap, n_samples, rd2,
+                             theta, i0, i1, moment_stride);
+    if (rc != DT_OK)
+        return rc;
+    if (i1 == i0)
+        return DT_OK;
+    if (!workspace || workspace_bytes < dt_tree_eval_workspace(n_nodes, n_src))
+        return dt_set_error(DT_ERR_WORKSPACE, "eval workspace too small");
+    char *ws = (char *)workspace;
+    void *packed = ws + 256;
+    double *xq = (double *)(ws + 256 + (size_t)n_nodes * sizeof(dt_node));
+    rc = dt_pack_tree(centers, halves, starts, ends, lefts, rights, n_nodes, packed, stream);
+    if (rc != DT_OK)
+        return rc;
+    rc = dt_pack_sources(xs, qs, n_src, xq, stream);
+    if (rc != DT_OK)
+        return rc;
+    return dt_tree_phi_sum_packed(packed, n_nodes, moments, moment_stride, xq, n_src, rd2, theta,
+                                  p, adaptive, tol_share, p_cap, cos_tab, sin_tab, n_samples, ys,
+                                  out, i0, i1, accumulate, DT_PSEL_FAST, nullptr, ws, 256,
+                                  stream);
+}
+
+extern "C" int dt_choose_p_batch(const double *big_r, const double *h, int64_t n, double rd2,
+                                 double tol_share, int64_t p_cap, const double *cos_tab,
+                                 const double *sin_tab, int64_t n_samples, int psel_mode,
+                                 int64_t *p_out, int32_t *tier_out, void *stream)
+{
+    DT_CHECK_ARG(n >= 0, "negative size");
+    if (n == 0)
+        return DT_OK;
+    DT_CHECK_ARG(big_r && h && p_out && cos_tab && sin_tab, "null pointer");
+    DT_CHECK_ARG(tol_share > 0.0 && rd2 > 0.0 && p_cap >= 0 && n_samples >= 1, "bad argument");
+    EvalArgs a{};
+    a.rd2 = rd2;
+    a.tol_share = tol_share;
+    a.p_cap = (int)p_cap;
+    a.cos_tab = cos_tab;
+    a.sin_tab = sin_tab;
+    a.n_samples = (int)n_samples;
+    a.psel_mode = psel_mode;
+    choose_p_kernel<<<(unsigned)((n + 127) / 128), 128, 0, (cudaStream_t)stream>>>(
+        big_r, h, n, a, p_out, tier_out);
+    DT_CUDA_TRY(cudaGetLastError());
+    return DT_OK;
+}

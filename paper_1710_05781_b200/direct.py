@@ -1,0 +1,74 @@
+"""O(N*T) direct evaluator: sign term + full pair sum (stage (f)).
+
+Mirror of disctree.direct (direct.py:23-88).  The pair sum runs in
+csrc/dt_direct.cu: fp64 (phi_sum_plain), Kahan (phi_sum_kahan, bit-identical)
+or the fp32-evaluation / fp64-accumulation bench variant.
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass
+
+import torch
+
+from . import _lib
+
+
+@dataclass(frozen=True)
+class FieldResult:
+    """Field values plus timings (direct.py:23-40)."""
+
+    values: object
+    build_time: float
+    eval_time: float
+    method: str
+
+    def __post_init__(self) -> None:
+        if self.method not in ("tree", "direct"):
+            raise ValueError(f"method must be 'tree' or 'direct', got {self.method!r}")
+        if self.build_time < 0 or self.eval_time < 0:
+            raise ValueError("timings must be nonnegative")
+
+
+def phi_sum_direct(xs: torch.Tensor, qs: torch.Tensor, ys: torch.Tensor, rd2: float,
+                   out: torch.Tensor, mode: int = _lib.DT_DIRECT_FP64, accumulate: bool = True,
+                   i0: int = 0, i1: int | None = None) -> None:
+    """out[i] (+)= sum_j q_j (x_j - y_i)/sqrt((x_j - y_i)^2 + rd2), i in [i0, i1)."""
+    if i1 is None:
+        i1 = ys.numel()
+    if i1 <= i0:
+        return
+    p = _lib.ptr
+    _lib.check(
+        _lib.load().dt_phi_sum_direct(p(xs), p(qs), xs.numel(), p(ys), float(rd2), p(out),
+                                      int(i0), int(i1), int(mode), int(bool(accumulate)),
+                                      _lib.stream_handle()),
+        "dt_phi_sum_direct",
+    )
+
+
+def evaluate_direct(system, kernel, targets, threads: int | None = 1,
+                    compensated: bool = False, *, precision: str = "fp64"):
+    """Field at every target by direct summation (direct.py:52-88).
+
+    ``compensated=True`` selects the Kahan kernel (bit-identical to the
+    reference's).  ``precision="fp32"`` selects fp32 pair evaluation with
+    fp64 accumulation (bench variant; not in the reference).  ``threads`` is
+    accepted for API compatibility; results do not depend on it.
+    """
+    from .charges import _sign_terms, as_targets
+
+    t, back = as_targets(targets)
+    if precision not in ("fp64", "fp32"):
+        raise ValueError(f"precision must be 'fp64' or 'fp32', got {precision!r}")
+    dev = t.device
+    torch.cuda.synchronize(dev)
+    start = time.perf_counter()
+    values = _sign_terms(system, t)
+    mode = _lib.DT_DIRECT_KAHAN if compensated else (
+        _lib.DT_DIRECT_FP32 if precision == "fp32" else _lib.DT_DIRECT_FP64)
+    phi_sum_direct(system.xs, system.qs, t, kernel.r_d * kernel.r_d, values, mode)
+    torch.cuda.synchronize(dev)
+    elapsed = time.perf_counter() - start
+    return FieldResult(values=back(values), build_time=0.0, eval_time=elapsed, method="direct")

@@ -1,0 +1,114 @@
+"""Device-resident evaluation step with no host round trips.
+
+One ``step`` is the whole hot path on inputs already in HBM:
+    (a) prefix scan of q and the sign term e(y)      dt_prefix_scan, dt_sign_terms
+    (b) tree build                                   dt_build_tree (cooperative)
+    (c) P2M / M2M moments                            dt_moments (cooperative)
+        interleave (x, q) for the traversal          dt_pack_sources
+    (d)+(e) traversal, far + near field, += e(y)     dt_tree_eval_device
+All launches are stream-ordered and read sizes (node count, depth, level
+ranges, tol_share) from device memory, so the step can be timed back to back
+or captured in a CUDA graph.  Buffers are sized once (node capacity from a
+planning build); a step whose tree overflows the capacity is detected by
+``check()``.  Used by bench.py and by the multi-GPU driver (contiguous target
+slices [i0, i1) per rank, sources replicated).
+"""
+
+from __future__ import annotations
+
+import torch
+
+from . import _lib
+from .kernel import DiscKernel
+from .tree import (
+    EvalConfig,
+    TreeBuffers,
+    contour_tables,
+    initial_node_capacity,
+    launch_moments,
+    moment_order_for,
+    pack_sources,
+)
+
+# kernels launched per step (memset of the work counter not counted)
+LAUNCHES_PER_STEP = 3 + 1 + 1 + 1 + 1 + 1  # scan(3) sign build moments pack eval
+
+
+class TreePipeline:
+    def __init__(self, n: int, n_targets: int, kernel: DiscKernel, config: EvalConfig,
+                 node_capacity: int | None = None, device=None):
+        self.dev = device or _lib.require_device()
+        self.n, self.T = int(n), int(n_targets)
+        self.kernel, self.config = kernel, config
+        self.order = moment_order_for(config)
+        cap = node_capacity or initial_node_capacity(n, config.leaf_capacity)
+        self.bufs = TreeBuffers(self.n, cap, self.dev)
+        self.moments = torch.empty((cap, self.order + 1), dtype=torch.float64, device=self.dev)
+        self.prefix = torch.empty(self.n, dtype=torch.float64, device=self.dev)
+        L = _lib.load()
+        self.scan_ws_bytes = int(L.dt_prefix_scan_workspace(self.n))
+        self.scan_ws = torch.empty(self.scan_ws_bytes, dtype=torch.uint8, device=self.dev)
+        self.xq = torch.empty(2 * self.n, dtype=torch.float64, device=self.dev)
+        self.eval_ws = torch.empty(256, dtype=torch.uint8, device=self.dev)
+        self.cos_t, self.sin_t = contour_tables(self.dev)
+
+    @classmethod
+    def planned(cls, xs: torch.Tensor, n_targets: int, kernel: DiscKernel,
+                config: EvalConfig, slack: float = 1.25) -> "TreePipeline":
+        """Size the node capacity from one synchronous build of these sources."""
+        n = xs.numel()
+        cap = initial_node_capacity(n, config.leaf_capacity)
+        while True:
+            probe = TreeBuffers(n, cap, _lib.require_device())
+            probe.launch(xs, config.leaf_capacity)
+            meta = probe.meta[:8].cpu().tolist()
+            if not meta[_lib.DT_META_OVERFLOW]:
+                break
+            cap *= 4
+        need = int(meta[_lib.DT_META_NODES] * slack) + 64
+        del probe
+        return cls(n, n_targets, kernel, config, node_capacity=need)
+
+    def step(self, xs: torch.Tensor, qs: torch.Tensor, ys: torch.Tensor, out: torch.Tensor,
+             i0: int = 0, i1: int | None = None, eval_events=None) -> None:
+        """out[i0:i1] = E(ys[i0:i1]) for sorted sources (xs, qs); async.
+
+        ``eval_events`` = (start, end) CUDA events recorded on the launching
+        stream around the traversal kernel (roofline timing)."""
+        if i1 is None:
+            i1 = ys.numel()
+        L = _lib.load()
+        p = _lib.ptr
+        s = _lib.stream_handle()
+        cfg = self.config
+        _lib.check(L.dt_prefix_scan(p(qs), p(self.prefix), self.n, p(self.scan_ws),
+                                    self.scan_ws_bytes, s), "dt_prefix_scan")
+        ys_part = ys[i0:i1]
+        out_part = out[i0:i1]
+        _lib.check(L.dt_sign_terms(p(xs), p(self.prefix), self.n, p(ys_part), p(out_part),
+                                   i1 - i0, s), "dt_sign_terms")
+        self.bufs.launch(xs, cfg.leaf_capacity)
+        launch_moments(self.bufs, xs, qs, self.order, self.moments)
+        pack_sources(xs, qs, self.xq)
+        if eval_events is not None:
+            eval_events[0].record()
+        _lib.check(
+            L.dt_tree_eval_device(
+                p(self.bufs.packed), p(self.bufs.meta), self.bufs.capacity, p(self.moments),
+                self.order + 1, p(self.xq), self.n, self.kernel.r_d * self.kernel.r_d,
+                float(cfg.theta), int(cfg.p), int(bool(cfg.adaptive)), float(cfg.tolerance),
+                self.order, p(self.cos_t), p(self.sin_t), self.cos_t.numel(), p(ys), p(out),
+                int(i0), int(i1), 1, p(self.eval_ws), self.eval_ws.numel(), s,
+            ),
+            "dt_tree_eval_device",
+        )
+        if eval_events is not None:
+            eval_events[1].record()
+
+    def check(self) -> dict:
+        """Synchronise and report the last step's tree (raises on overflow)."""
+        meta = self.bufs.meta[:8].cpu().tolist()
+        if meta[_lib.DT_META_OVERFLOW]:
+            raise RuntimeError("tree exceeded the pipeline's node capacity")
+        return {"nodes": int(meta[_lib.DT_META_NODES]), "depth": int(meta[_lib.DT_META_DEPTH]),
+                "leaves": int(meta[_lib.DT_META_LEAVES])}

@@ -1,0 +1,352 @@
+"""Binary source tree, node moments and tree field evaluation on the B200.
+
+Mirror of disctree.tree (tree.py:35-373): EvalConfig, Tree, TreeNode, build,
+well_separated, evaluate_point, evaluate_all with the reference's names,
+argument meaning and errors.  build() runs stages (b) and (c) of the hot
+path (csrc/dt_build.cu, csrc/dt_moments.cu); evaluate_all() runs (a) and
+(d)+(e) (csrc/dt_scan.cu, csrc/dt_eval.cu).  Node arrays are CUDA tensors
+in the reference's breadth-first layout and are bit-identical to it.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib
+from .charges import ChargeSystem, _sign_terms, as_targets
+from .direct import FieldResult
+from .kernel import DEFAULT_CONTOUR_SAMPLES, DEFAULT_P_MAX, DiscKernel
+
+MAX_DEPTH = 60  # tree.py:32
+
+
+@dataclass(frozen=True)
+class EvalConfig:
+    """Truncation order, separation ratio, leaf size, adaptive tolerance
+    (tree.py:35-59)."""
+
+    p: int = 10
+    theta: float = 1.0 / 3.0
+    leaf_capacity: int = 40
+    adaptive: bool = False
+    tolerance: float = 1e-9
+
+    def __post_init__(self) -> None:
+        if self.p < 0:
+            raise ValueError(f"p must be >= 0, got {self.p!r}")
+        if not 0.0 < self.theta < 1.0:
+            raise ValueError(f"theta must lie in (0, 1), got {self.theta!r}")
+        if self.leaf_capacity < 1:
+            raise ValueError(f"leaf_capacity must be >= 1, got {self.leaf_capacity!r}")
+        if self.tolerance <= 0:
+            raise ValueError(f"tolerance must be positive, got {self.tolerance!r}")
+
+
+def moment_order_for(config: EvalConfig) -> int:
+    """tree.py:224-226: p, raised to the adaptive cap when adaptive."""
+    return max(config.p, DEFAULT_P_MAX) if config.adaptive else config.p
+
+
+@dataclass
+class Tree:
+    """Breadth-first node arrays (CUDA tensors; child -1 = absent) and moments
+    [nodes, moment_order + 1] (tree.py:62-99)."""
+
+    system: ChargeSystem
+    lo: torch.Tensor
+    hi: torch.Tensor
+    center: torch.Tensor
+    half: torch.Tensor
+    level: torch.Tensor
+    start: torch.Tensor
+    end: torch.Tensor
+    left: torch.Tensor
+    right: torch.Tensor
+    moments: torch.Tensor
+    moment_order: int
+    depth: int
+    leaf_count: int
+    build_seconds: float
+    # device-side extras for the traversal kernel
+    packed: torch.Tensor = field(repr=False, default=None)
+    xq: torch.Tensor = field(repr=False, default=None)
+    meta: torch.Tensor = field(repr=False, default=None)
+
+    def __len__(self) -> int:
+        return int(self.lo.shape[0])
+
+    def node(self, index: int) -> "TreeNode":
+        return TreeNode(self, index)
+
+    @property
+    def root(self) -> "TreeNode":
+        return TreeNode(self, 0)
+
+    @property
+    def mean_leaf_occupancy(self) -> float:
+        return len(self.system) / self.leaf_count
+
+    def numpy(self) -> dict:
+        """Host copies of the node arrays (reference dtypes)."""
+        names = ("lo", "hi", "center", "half", "level", "start", "end", "left", "right",
+                 "moments")
+        return {k: getattr(self, k).cpu().numpy() for k in names}
+
+
+@dataclass(frozen=True)
+class TreeNode:
+    """Read-only view of one node (tree.py:102-147)."""
+
+    tree: Tree
+    index: int
+
+    @property
+    def interval(self) -> tuple[float, float]:
+        return (float(self.tree.lo[self.index]), float(self.tree.hi[self.index]))
+
+    @property
+    def center(self) -> float:
+        return float(self.tree.center[self.index])
+
+    @property
+    def half_width(self) -> float:
+        return float(self.tree.half[self.index])
+
+    @property
+    def level(self) -> int:
+        return int(self.tree.level[self.index])
+
+    @property
+    def source_range(self) -> tuple[int, int]:
+        return (int(self.tree.start[self.index]), int(self.tree.end[self.index]))
+
+    @property
+    def source_count(self) -> int:
+        s, e = self.source_range
+        return e - s
+
+    @property
+    def moments(self) -> np.ndarray:
+        return self.tree.moments[self.index].cpu().numpy()
+
+    @property
+    def children(self) -> tuple["TreeNode", ...]:
+        kids = []
+        for c in (int(self.tree.left[self.index]), int(self.tree.right[self.index])):
+            if c >= 0:
+                kids.append(TreeNode(self.tree, c))
+        return tuple(kids)
+
+    @property
+    def is_leaf(self) -> bool:
+        return int(self.tree.left[self.index]) < 0 and int(self.tree.right[self.index]) < 0
+
+
+def initial_node_capacity(n: int, leaf_capacity: int) -> int:
+    return int(4 * (n // max(1, leaf_capacity) + 1) + 256)
+
+
+class TreeBuffers:
+    """Device buffers for one build at a fixed node capacity (reusable)."""
+
+    F64 = ("lo", "hi", "center", "half")
+    I64 = ("level", "start", "end", "left", "right")
+
+    def __init__(self, n: int, capacity: int, device):
+        self.n = n
+        self.capacity = capacity
+        for k in self.F64:
+            setattr(self, k, torch.empty(capacity, dtype=torch.float64, device=device))
+        for k in self.I64:
+            setattr(self, k, torch.empty(capacity, dtype=torch.int64, device=device))
+        self.packed = torch.empty(capacity * 32, dtype=torch.uint8, device=device)
+        self.meta = torch.zeros(_lib.DT_META_WORDS, dtype=torch.int64, device=device)
+        L = _lib.load()
+        self.ws_bytes = int(L.dt_build_workspace(n, capacity))
+        self.ws = torch.empty(self.ws_bytes, dtype=torch.uint8, device=device)
+
+    def launch(self, xs: torch.Tensor, leaf_capacity: int, max_depth: int = MAX_DEPTH) -> None:
+        L = _lib.load()
+        p = _lib.ptr
+        _lib.check(
+            L.dt_build_tree(
+                p(xs), self.n, int(leaf_capacity), int(max_depth), self.capacity, p(self.lo),
+                p(self.hi), p(self.center), p(self.half), p(self.level), p(self.start),
+                p(self.end), p(self.left), p(self.right), p(self.packed), p(self.meta),
+                p(self.ws), self.ws_bytes, _lib.stream_handle(),
+            ),
+            "dt_build_tree",
+        )
+
+
+def launch_moments(bufs: TreeBuffers, xs, qs, order: int, moments: torch.Tensor) -> None:
+    L = _lib.load()
+    p = _lib.ptr
+    _lib.check(
+        L.dt_moments(p(xs), p(qs), p(bufs.center), p(bufs.start), p(bufs.end), p(bufs.left),
+                     p(bufs.right), p(bufs.meta), int(order), p(moments),
+                     _lib.stream_handle()),
+        "dt_moments",
+    )
+
+
+def pack_sources(xs: torch.Tensor, qs: torch.Tensor, out: torch.Tensor | None = None):
+    n = xs.numel()
+    if out is None:
+        out = torch.empty(2 * n, dtype=torch.float64, device=xs.device)
+    if n:
+        _lib.check(
+            _lib.load().dt_pack_sources(_lib.ptr(xs), _lib.ptr(qs), n, _lib.ptr(out),
+                                        _lib.stream_handle()),
+            "dt_pack_sources",
+        )
+    return out
+
+
+def build(system: ChargeSystem, kernel: DiscKernel, config: EvalConfig) -> Tree:
+    """Build the tree and all node moments on the GPU (tree.py:156-257).
+
+    Bit-identical node arrays, depth and leaf_count; moments agree with the
+    reference to round-off.  ``kernel`` is unused, as in the reference.
+    """
+    if len(system) == 0:
+        raise ValueError("cannot build a tree over an empty charge system")
+    dev = _lib.require_device()
+    torch.cuda.synchronize(dev)
+    t0 = time.perf_counter()
+    n = len(system)
+    cap = initial_node_capacity(n, config.leaf_capacity)
+    while True:
+        bufs = TreeBuffers(n, cap, dev)
+        bufs.launch(system.xs, config.leaf_capacity)
+        meta = bufs.meta[:8].cpu().tolist()
+        if not meta[_lib.DT_META_OVERFLOW]:
+            break
+        cap *= 4
+    n_nodes = int(meta[_lib.DT_META_NODES])
+    order = moment_order_for(config)
+    moments = torch.empty((n_nodes, order + 1), dtype=torch.float64, device=dev)
+    launch_moments(bufs, system.xs, system.qs, order, moments)
+    xq = pack_sources(system.xs, system.qs)
+    torch.cuda.synchronize(dev)
+    elapsed = time.perf_counter() - t0
+    return Tree(
+        system=system,
+        lo=bufs.lo[:n_nodes], hi=bufs.hi[:n_nodes], center=bufs.center[:n_nodes],
+        half=bufs.half[:n_nodes], level=bufs.level[:n_nodes], start=bufs.start[:n_nodes],
+        end=bufs.end[:n_nodes], left=bufs.left[:n_nodes], right=bufs.right[:n_nodes],
+        moments=moments, moment_order=order, depth=int(meta[_lib.DT_META_DEPTH]),
+        leaf_count=int(meta[_lib.DT_META_LEAVES]), build_seconds=elapsed,
+        packed=bufs.packed[: n_nodes * 32], xq=xq, meta=bufs.meta,
+    )
+
+
+def well_separated(node: TreeNode, y: float, theta: float) -> bool:
+    """half / |y - center| <= theta, false at distance 0 (tree.py:260-265)."""
+    dist = abs(y - node.center)
+    if dist == 0.0:
+        return False
+    return node.half_width <= theta * dist
+
+
+def _tol_share(tree: Tree, config: EvalConfig) -> float:
+    return config.tolerance / (3.0 * max(tree.depth, 1))  # tree.py:268-270
+
+
+_TABLES: dict = {}
+
+
+def contour_tables(device, samples: int = DEFAULT_CONTOUR_SAMPLES):
+    """cos/sin of linspace(0, 2 pi, 64, endpoint=False) from host numpy
+    (tree.py:342), cached on the device."""
+    key = (str(device), samples)
+    if key not in _TABLES:
+        ang = np.linspace(0.0, 2.0 * np.pi, samples, endpoint=False)
+        _TABLES[key] = (
+            torch.from_numpy(np.cos(ang)).to(device),
+            torch.from_numpy(np.sin(ang)).to(device),
+        )
+    return _TABLES[key]
+
+
+def tree_phi_sum(tree: Tree, kernel: DiscKernel, config: EvalConfig, ys: torch.Tensor,
+                 out: torch.Tensor, i0: int = 0, i1: int | None = None,
+                 accumulate: bool = True, psel_mode: int = _lib.DT_PSEL_FAST,
+                 stats: _lib.EvalStats | None = None,
+                 workspace: torch.Tensor | None = None) -> None:
+    """Stage (d)+(e) on device targets ys[i0:i1] (the _kernels.tree_phi_sum
+    seam); out[i] (+)= phi(y_i)."""
+    if i1 is None:
+        i1 = ys.numel()
+    if i1 <= i0:
+        return
+    cos_t, sin_t = contour_tables(ys.device)
+    if workspace is None:
+        workspace = torch.empty(256, dtype=torch.uint8, device=ys.device)
+    p = _lib.ptr
+    _lib.check(
+        _lib.load().dt_tree_phi_sum_packed(
+            p(tree.packed), len(tree), p(tree.moments), tree.moment_order + 1, p(tree.xq),
+            len(tree.system), kernel.r_d * kernel.r_d, float(config.theta), int(config.p),
+            int(bool(config.adaptive)), _tol_share(tree, config), int(tree.moment_order),
+            p(cos_t), p(sin_t), cos_t.numel(), p(ys), p(out), int(i0), int(i1),
+            int(bool(accumulate)), int(psel_mode), C.byref(stats) if stats is not None else None,
+            p(workspace), workspace.numel(), _lib.stream_handle(),
+        ),
+        "dt_tree_phi_sum_packed",
+    )
+
+
+def _check_order(tree: Tree, config: EvalConfig) -> None:
+    if tree.moment_order < config.p:
+        raise ValueError(
+            f"tree was built with moment order {tree.moment_order}, "
+            f"config.p = {config.p} requires at least that"
+        )
+
+
+def evaluate_point(tree: Tree, kernel: DiscKernel, config: EvalConfig, y: float) -> float:
+    """Kernel-sum part of the field at one target (tree.py:273-315); the sign
+    term is not included.  Runs the same GPU traversal as evaluate_all."""
+    _check_order(tree, config)
+    dev = _lib.require_device()
+    ys = torch.tensor([float(y)], dtype=torch.float64, device=dev)
+    out = torch.zeros(1, dtype=torch.float64, device=dev)
+    tree_phi_sum(tree, kernel, config, ys, out, accumulate=False)
+    return float(out[0])
+
+
+def evaluate_all(tree: Tree, kernel: DiscKernel, config: EvalConfig, system: ChargeSystem,
+                 targets, threads: int | None = 1) -> FieldResult:
+    """Field at every target: sign term + tree-accelerated kernel sum
+    (tree.py:318-373).
+
+    ``targets`` may be a numpy array / sequence (numpy values returned) or a
+    torch tensor (returned on the same device).  Per-target results are
+    bit-identical for any ``threads`` value and any target order; ``threads``
+    is accepted for API compatibility (the GPU grid replaces the CPU pool).
+    """
+    t, back = as_targets(targets)
+    _check_order(tree, config)
+    dev = t.device
+    torch.cuda.synchronize(dev)
+    start = time.perf_counter()
+    values = _sign_terms(system, t)
+    T = t.numel()
+    if T:
+        if T > 1 and not bool((t[1:] >= t[:-1]).all()):
+            ys, perm = torch.sort(t)
+            vs = values[perm].contiguous()
+            tree_phi_sum(tree, kernel, config, ys.contiguous(), vs)
+            values[perm] = vs
+        else:
+            tree_phi_sum(tree, kernel, config, t, values)
+    torch.cuda.synchronize(dev)
+    elapsed = time.perf_counter() - start
+    return FieldResult(values=back(values), build_time=tree.build_seconds, eval_time=elapsed,
+                       method="tree")

@@ -81,6 +81,27 @@ def tree_case(name, pairs, r_d, config: dt.EvalConfig, targets, direct=True):
     }
     for f in NODE_FIELDS:
         out[f] = getattr(tree, f)
+    # kernel-sum parts straight from the reference's numba seams (the e term
+    # is compared separately: it rests on the sequential np.cumsum)
+    t = np.ascontiguousarray(targets, dtype=np.float64)
+    rd2 = kernel.r_d * kernel.r_d
+    if len(t):
+        angles = np.linspace(0.0, 2.0 * np.pi, 64, endpoint=False)
+        phi = np.empty_like(t)
+        _kernels.tree_phi_sum(
+            tree.center, tree.half, tree.start, tree.end, tree.left, tree.right, tree.moments,
+            tree.system.xs, tree.system.qs, rd2, config.theta, config.p, config.adaptive,
+            config.tolerance / (3.0 * max(tree.depth, 1)), tree.moment_order, np.cos(angles),
+            np.sin(angles), t, phi, 0, len(t),
+        )
+        out["phi_tree"] = phi
+        if direct:
+            plain = np.empty_like(t)
+            _kernels.phi_sum_plain(system.xs, system.qs, t, rd2, plain, 0, len(t))
+            kahan = np.empty_like(t)
+            _kernels.phi_sum_kahan(system.xs, system.qs, t, rd2, kahan, 0, len(t))
+            out["phi_plain"] = plain
+            out["phi_kahan"] = kahan
     if direct:
         out["E_direct"] = dt.evaluate_direct(system, kernel, targets, threads=1).values
         out["E_kahan"] = dt.evaluate_direct(system, kernel, targets, compensated=True).values

@@ -81,6 +81,24 @@ def test_tree_field(name):
     assert np.max(np.abs(E - g["E_tree"])) <= 1e-13 * scale
 
 
+@pytest.mark.parametrize("name", [n for n in TREE_CASES if "phi_tree" in load_case(n)])
+def test_tree_phi_seam(name):
+    """Oracle kernel-sum part vs the reference's tree_phi_sum output."""
+    g = load_case(name)
+    tree = O.build(g["xs"], g["qs"], int(g["p"]), int(g["leaf_capacity"]), bool(g["adaptive"]))
+    phi = O.tree_phi_sum(tree, g["xs"], g["qs"], float(g["r_d"]) ** 2, float(g["theta"]),
+                         int(g["p"]), bool(g["adaptive"]),
+                         O.tol_share(float(g["tolerance"]), tree.depth), g["targets"])
+    scale = np.abs(g["qs"]).sum()
+    assert np.max(np.abs(phi - g["phi_tree"])) <= 1e-13 * scale
+    if "phi_kahan" in g:
+        rd2 = float(g["r_d"]) ** 2
+        np.testing.assert_array_equal(O.phi_sum_kahan(g["xs"], g["qs"], g["targets"], rd2),
+                                      g["phi_kahan"])
+        plain = O.phi_sum_plain(g["xs"], g["qs"], g["targets"], rd2)
+        assert np.max(np.abs(plain - g["phi_plain"])) <= 1e-13 * scale
+
+
 @pytest.mark.parametrize("name", [n for n in TREE_CASES if "E_direct" in load_case(n)])
 def test_direct_field(name):
     g = load_case(name)
