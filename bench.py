@@ -316,7 +316,7 @@ def run_ours(args):
     # spot-check the pipelined result against the public API on a sample
     res = dtp.evaluate_all(dtp.build(dtp.from_sorted(xs, qs), kernel, cfg), kernel, cfg,
                            dtp.from_sorted(xs, qs), ys[i0:i1][::997])
-    diff = float(np.max(np.abs(out[i0:i1][::997].cpu().numpy() - res.values)))
+    diff = float((out[i0:i1][::997] - res.values).abs().max())
     scale = float(np.abs(w.qs).sum())
 
     # end to end through the public API, pinned host buffers, copies timed

@@ -107,10 +107,14 @@ int dt_build_tree(const double *xs, int64_t n, int64_t leaf_capacity, int64_t ma
 /* Node moments m_k = sum_j q_j (x_j - c)^k / k!, k = 0..order, row-major
  * [n_nodes][order + 1] (tree.py:224-238): P2M at every leaf from its sources,
  * then M2M (binomial shift) bottom-up level by level.  Reads the tree
- * produced by dt_build_tree (meta gives n_nodes, depth and level ranges). */
+ * produced by dt_build_tree (meta gives n_nodes, depth and level ranges).
+ * moments_eval (optional) receives the traversal layout used by the *_packed
+ * and *_device evaluators: M'_0 = m_0, M'_k = (k-1)! m_k, row stride
+ * eval_stride (even, >= order + 1; padding zeroed). */
 int dt_moments(const double *xs, const double *qs, const double *center, const int64_t *start,
                const int64_t *end, const int64_t *left, const int64_t *right,
-               const int64_t *meta, int64_t order, double *moments, void *stream);
+               const int64_t *meta, int64_t order, double *moments, double *moments_eval,
+               int64_t eval_stride, void *stream);
 
 /* ---------------------------------------------------------------- (d)+(e) */
 
@@ -130,7 +134,7 @@ int dt_pack_tree(const double *centers, const double *halves, const int64_t *sta
                  const int64_t *ends, const int64_t *lefts, const int64_t *rights,
                  int64_t n_nodes, void *packed, void *stream);
 
-size_t dt_tree_eval_workspace(int64_t n_nodes, int64_t n_src);
+size_t dt_tree_eval_workspace(int64_t n_nodes, int64_t n_src, int64_t moment_stride);
 
 /* Mirror of the numba seam _kernels.tree_phi_sum (_kernels.py:163-266):
  * far-field/near-field traversal for targets ys[i0:i1]; writes out[i0:i1]
@@ -147,7 +151,9 @@ int dt_tree_phi_sum(const double *centers, const double *halves, const int64_t *
                     const double *ys, double *out, int64_t i0, int64_t i1, int accumulate,
                     void *workspace, size_t workspace_bytes, void *stream);
 
-/* Same, on pre-packed nodes/sources (what the Python layer uses).  `stats`
+/* Same, on pre-packed nodes/sources and traversal-layout moments (dt_moments
+ * moments_eval: M'_k = (k-1)! m_k, even stride); what the Python layer uses.
+ * `stats`
  * (host struct of device pointers, indexed by target) may be NULL; psel_mode
  * is DT_PSEL_FAST or DT_PSEL_EXACT. */
 int dt_tree_phi_sum_packed(const void *packed_nodes, int64_t n_nodes, const double *moments,

@@ -39,7 +39,7 @@ constexpr int EVAL_THREADS = 256;
 constexpr int EVAL_WARPS = EVAL_THREADS / 32;
 constexpr int STACK_DEPTH = 64;         // >= max_depth + 2
 constexpr int MAX_SAMPLES = 256;
-constexpr float PSEL_MARGIN = 5e-5f;    // in units of the order axis
+constexpr float PSEL_MARGIN = 1e-4f;    // in units of the order axis
 constexpr double CONTOUR_SAFETY = 1.1;  // kernel.py:27
 
 struct EvalArgs {
@@ -210,16 +210,20 @@ __device__ int psel_exact_bracket(double big_r, double h, int t0, const EvalArgs
 
 // ------------------------------------------------------------------ fast tier
 
-// log2(x) = e + f for normal x > 0, f = log2(mantissa) in [0, 1).
+// log2(x) = e + f for normal x > 0, f = log2(mantissa) in [0, 1) (MUFU.LG2,
+// absolute error ~2^-22 on [1, 2)).
 __device__ __forceinline__ void split_log2(float x, int *e, float *f)
 {
     int bits = __float_as_int(x);
     *e = ((bits >> 23) & 0xff) - 127;
-    *f = log2f(__int_as_float((bits & 0x007fffff) | 0x3f800000));
+    *f = __log2f(__int_as_float((bits & 0x007fffff) | 0x3f800000));
 }
 
 // Returns p >= 0 on a confident decision, or -(t0 + 2) (<= -2) when the
 // decision is within the margin (tier 2 with bracket t0), or -1 for tier 3.
+// Error budget of the order estimate (in units of p): MUFU logs 2^-22 each
+// (x up to 31 for the ratio term), approximate fp32 divisions/roots (a few
+// ulp of the factors of X) -> below 2e-5; PSEL_MARGIN is 5x that.
 __device__ int psel_fast(double big_r, double h, const EvalArgs &a, const float *isig,
                          float rd2f, float inv_tol_f)
 {
@@ -229,32 +233,40 @@ __device__ int psel_fast(double big_r, double h, const EvalArgs &a, const float 
     const float hf = (float)h;
     if (!(Rf > 1e-15f && Rf < 1e15f && hf > 1e-30f))
         return -1;
-    const float ratio = hf / Rf;
-    const float sstar = rd2f / (Rf * Rf);
+    const float ratio = __fdividef(hf, Rf);
+    const float sstar = __fdividef(rd2f, Rf * Rf);
     if (!(sstar > 1e-12f) || !(sstar < 1e30f))
         return -1;
-    // bracket: s_t = 4 sin^2(pi t / 64) = s*  ->  t* = (64/pi) asin(sqrt(s*)/2)
-    const float z = fminf(1.0f, 0.5f * sqrtf(sstar));
-    const int t0 = (int)floorf(asinf(z) * 20.371832715762604f);
+    // bracket: s_t = 4 sin^2(pi t / 64) = s*  ->  t* = (64/pi) asin(sqrt(s*)/2);
+    // asin via Abramowitz-Stegun 4.4.45 (|err| < 7e-5 rad), enough to place
+    // s* within the 4 candidate samples t0-1 .. t0+2.
+    const float z = fminf(1.0f, 0.5f * sstar * rsqrtf(sstar));
+    const float om = 1.0f - z;
+    const float poly = fmaf(fmaf(fmaf(-0.0187293f, z, 0.0742610f), z, -0.2121144f), z,
+                            1.5707288f);
+    const float asz = 1.57079633f - om * rsqrtf(fmaxf(om, 1e-30f)) * poly;
+    const int t0 = (int)floorf(asz * 20.371832715762604f);
     float emin = 3.0e38f;
 #pragma unroll
     for (int c = -1; c <= 2; ++c) {
-        int t = min(max(t0 + c, 1), 32);
-        float u = sstar * isig[t];
-        float e = (1.0f - u) * (1.0f - u);
+        const int t = min(max(t0 + c, 1), 32);
+        const float u = sstar * isig[t];
+        const float e = (1.0f - u) * (1.0f - u);
         emin = fminf(emin, e);
     }
-    const float Q = emin + sstar;        // M^-4
-    const float M = rsqrtf(sqrtf(Q));    // sampled contour maximum of |f|
-    const float X = 1.1f * M * (ratio / (1.0f - ratio)) * inv_tol_f;  // value_0 / tol
+    const float Q = emin + sstar;         // M^-4
+    const float rq = rsqrtf(Q);
+    const float M = rq * rsqrtf(rq);      // Q^(-1/4): sampled contour maximum of |f|
+    const float X = 1.1f * M * __fdividef(ratio, 1.0f - ratio) * inv_tol_f;  // value_0 / tol
     if (!(X > 1e-37f && X < 1e37f))
         return -1;
     int ex, er;
     float fx, fr;
     split_log2(X, &ex, &fx);
     split_log2(ratio, &er, &fr);
-    const float L = -((float)er + fr);   // -log2(ratio) > 0
-    const float pstar_approx = ((float)ex + fx) / L;
+    const float L = -((float)er + fr);    // -log2(ratio) > 0
+    const float iL = __frcp_rn(L);
+    const float pstar_approx = ((float)ex + fx) * iL;
     if (pstar_approx < -1.0f)
         return 0;
     if (pstar_approx > (float)a.p_cap + 1.0f)
@@ -262,50 +274,126 @@ __device__ int psel_fast(double big_r, double h, const EvalArgs &a, const float 
     const int n = __float2int_rn(pstar_approx);
     // residual N - n L with the integer parts kept exact
     const float resid = (float)(ex + n * er) + fmaf((float)n, fr, fx);
-    const float dist = resid / L;  // pstar - n
+    const float dist = resid * iL;        // pstar - n
     if (fabsf(dist) < PSEL_MARGIN && n >= 0 && n <= a.p_cap - 1)
         return -(t0 + 2);
-    int p = dist > 0.0f ? n + 1 : n;
-    p = max(p, 0);
+    const int p = max(dist > 0.0f ? n + 1 : n, 0);
     return min(p, a.p_cap);
 }
 
 // ------------------------------------------------------------------ far / near
 
-__device__ __forceinline__ double far_field(double d, double rd2, const double *__restrict__ m,
+__constant__ double c_rcp[128] = {  // 1/k (k >= 1)
+    0.0, 0x1.0000000000000p+0, 0x1.0000000000000p-1, 0x1.5555555555555p-2,
+    0x1.0000000000000p-2, 0x1.999999999999ap-3, 0x1.5555555555555p-3, 0x1.2492492492492p-3,
+    0x1.0000000000000p-3, 0x1.c71c71c71c71cp-4, 0x1.999999999999ap-4, 0x1.745d1745d1746p-4,
+    0x1.5555555555555p-4, 0x1.3b13b13b13b14p-4, 0x1.2492492492492p-4, 0x1.1111111111111p-4,
+    0x1.0000000000000p-4, 0x1.e1e1e1e1e1e1ep-5, 0x1.c71c71c71c71cp-5, 0x1.af286bca1af28p-5,
+    0x1.999999999999ap-5, 0x1.8618618618618p-5, 0x1.745d1745d1746p-5, 0x1.642c8590b2164p-5,
+    0x1.5555555555555p-5, 0x1.47ae147ae147bp-5, 0x1.3b13b13b13b14p-5, 0x1.2f684bda12f68p-5,
+    0x1.2492492492492p-5, 0x1.1a7b9611a7b96p-5, 0x1.1111111111111p-5, 0x1.0842108421084p-5,
+    0x1.0000000000000p-5, 0x1.f07c1f07c1f08p-6, 0x1.e1e1e1e1e1e1ep-6, 0x1.d41d41d41d41dp-6,
+    0x1.c71c71c71c71cp-6, 0x1.bacf914c1bad0p-6, 0x1.af286bca1af28p-6, 0x1.a41a41a41a41ap-6,
+    0x1.999999999999ap-6, 0x1.8f9c18f9c18fap-6, 0x1.8618618618618p-6, 0x1.7d05f417d05f4p-6,
+    0x1.745d1745d1746p-6, 0x1.6c16c16c16c17p-6, 0x1.642c8590b2164p-6, 0x1.5c9882b931057p-6,
+    0x1.5555555555555p-6, 0x1.4e5e0a72f0539p-6, 0x1.47ae147ae147bp-6, 0x1.4141414141414p-6,
+    0x1.3b13b13b13b14p-6, 0x1.3521cfb2b78c1p-6, 0x1.2f684bda12f68p-6, 0x1.29e4129e4129ep-6,
+    0x1.2492492492492p-6, 0x1.1f7047dc11f70p-6, 0x1.1a7b9611a7b96p-6, 0x1.15b1e5f75270dp-6,
+    0x1.1111111111111p-6, 0x1.0c9714fbcda3bp-6, 0x1.0842108421084p-6, 0x1.0410410410410p-6,
+    0x1.0000000000000p-6, 0x1.f81f81f81f820p-7, 0x1.f07c1f07c1f08p-7, 0x1.e9131abf0b767p-7,
+    0x1.e1e1e1e1e1e1ep-7, 0x1.dae6076b981dbp-7, 0x1.d41d41d41d41dp-7, 0x1.cd85689039b0bp-7,
+    0x1.c71c71c71c71cp-7, 0x1.c0e070381c0e0p-7, 0x1.bacf914c1bad0p-7, 0x1.b4e81b4e81b4fp-7,
+    0x1.af286bca1af28p-7, 0x1.a98ef606a63bep-7, 0x1.a41a41a41a41ap-7, 0x1.9ec8e951033d9p-7,
+    0x1.999999999999ap-7, 0x1.948b0fcd6e9e0p-7, 0x1.8f9c18f9c18fap-7, 0x1.8acb90f6bf3aap-7,
+    0x1.8618618618618p-7, 0x1.8181818181818p-7, 0x1.7d05f417d05f4p-7, 0x1.78a4c8178a4c8p-7,
+    0x1.745d1745d1746p-7, 0x1.702e05c0b8170p-7, 0x1.6c16c16c16c17p-7, 0x1.6816816816817p-7,
+    0x1.642c8590b2164p-7, 0x1.6058160581606p-7, 0x1.5c9882b931057p-7, 0x1.58ed2308158edp-7,
+    0x1.5555555555555p-7, 0x1.51d07eae2f815p-7, 0x1.4e5e0a72f0539p-7, 0x1.4afd6a052bf5bp-7,
+    0x1.47ae147ae147bp-7, 0x1.446f86562d9fbp-7, 0x1.4141414141414p-7, 0x1.3e22cbce4a902p-7,
+    0x1.3b13b13b13b14p-7, 0x1.3813813813814p-7, 0x1.3521cfb2b78c1p-7, 0x1.323e34a2b10bfp-7,
+    0x1.2f684bda12f68p-7, 0x1.2c9fb4d812ca0p-7, 0x1.29e4129e4129ep-7, 0x1.27350b8812735p-7,
+    0x1.2492492492492p-7, 0x1.21fb78121fb78p-7, 0x1.1f7047dc11f70p-7, 0x1.1cf06ada2811dp-7,
+    0x1.1a7b9611a7b96p-7, 0x1.1811811811812p-7, 0x1.15b1e5f75270dp-7, 0x1.135c81135c811p-7,
+    0x1.1111111111111p-7, 0x1.0ecf56be69c90p-7, 0x1.0c9714fbcda3bp-7, 0x1.0a6810a6810a7p-7,
+    0x1.0842108421084p-7, 0x1.0624dd2f1a9fcp-7, 0x1.0410410410410p-7, 0x1.0204081020408p-7,
+};
+
+// sum_k Phi^(k)(c, y) m_k, k <= pu (lanes share pmax = max pu over the warp).
+// Phi^(k) follows the reference's recurrence (kernel.py:92-127, Eq. 10) in the
+// scaled variable g_k = Phi^(k) / (k-1)!:
+//   g_k = (a0/(k-1) - ci) g_{k-1} - ir3 g_{k-2} - inv g_{k-3},   k >= 4,
+//   a0 = rd2/(d s2), ci = (3d^2 + rd2)/(d s2), ir3 = 3/s2, inv = 1/(d s2),
+// with g_2, g_3 from the same formula without the vanishing terms.  The
+// matching moments M'_k = (k-1)! m_k come from dt_moments (row stride even,
+// 16-byte aligned, read two at a time).  5 FP64 instructions per order.
+template <bool WIDE>
+__device__ __forceinline__ double far_field(double d, double rd2, const double2 *__restrict__ M2,
                                             int pu, int pmax)
 {
     const double s2 = __fma_rn(d, d, rd2);
     const double r = dt_rsqrt(s2);
-    const double f0 = d * r;
-    double acc = f0 * __ldg(m);
+    const double g0 = d * r;
+    const double2 m01 = __ldg(M2);
+    double acc = g0 * m01.x;
     if (pmax < 1)
         return acc;
-    const double ir2 = r * r;              // 1 / s2
-    double f1 = rd2 * r * ir2;             // rd2 / s2^(3/2)
+    const double ir2 = r * r;
+    const double g1 = rd2 * r * ir2;
     if (pu >= 1)
-        acc = __fma_rn(f1, __ldg(m + 1), acc);
+        acc = __fma_rn(g1, m01.y, acc);
     if (pmax < 2)
         return acc;
-    const double inv = ir2 * dt_rcp(d);    // 1 / (d s2)
-    const double ir3 = 3.0 * ir2;          // 3 d / (d s2)
-    const double ci = __fma_rn(3.0 * d, d, rd2) * inv;  // (3 d^2 + rd2) / (d s2)
-    double ak = rd2 * inv;                 // A_k / (d s2), A_k = rd2 - (k-1) C
-    double f2 = f0, f3 = 0.0;
-#pragma unroll 2
-    for (int k = 2; k <= pmax; ++k) {
-        ak -= ci;
-        const double km1 = (double)(k - 1);
-        double t = ak * f1;
-        if (k >= 3)
-            t = __fma_rn(-(km1 * (double)(k - 2)) * ir3, f2, t);
-        if (k >= 4)
-            t = __fma_rn(-(km1 * (double)((k - 2) * (k - 3))) * inv, f3, t);
-        f3 = f2;
-        f2 = f1;
-        f1 = t;
-        if (k <= pu)
-            acc = __fma_rn(t, __ldg(m + k), acc);
+    const double inv = ir2 * dt_rcp(d);
+    const double a0 = rd2 * inv;
+    const double ci = __fma_rn(3.0 * d, d, rd2) * inv;
+    const double ir3 = 3.0 * ir2;
+    const double2 m23 = __ldg(M2 + 1);
+    const double g2 = (a0 - ci) * g1;
+    if (pu >= 2)
+        acc = __fma_rn(g2, m23.x, acc);
+    if (pmax < 3)
+        return acc;
+    const double g3 = __fma_rn(-ir3, g1, __fma_rn(a0, 0.5, -ci) * g2);
+    if (pu >= 3)
+        acc = __fma_rn(g3, m23.y, acc);
+    double gm3 = g1, gm2 = g2, gm1 = g3;
+    if (!WIDE) {
+#pragma unroll
+        for (int k = 4; k < 32; k += 2) {
+            if (k > pmax)
+                break;
+            const double2 mm = __ldg(M2 + k / 2);
+            double t = __fma_rn(a0, 1.0 / (k - 1), -ci) * gm1;
+            t = __fma_rn(-ir3, gm2, t);
+            t = __fma_rn(-inv, gm3, t);
+            if (k <= pu)
+                acc = __fma_rn(t, mm.x, acc);
+            gm3 = gm2;
+            gm2 = gm1;
+            gm1 = t;
+            if (k + 1 > pmax)
+                break;
+            double u = __fma_rn(a0, 1.0 / k, -ci) * gm1;
+            u = __fma_rn(-ir3, gm2, u);
+            u = __fma_rn(-inv, gm3, u);
+            if (k + 1 <= pu)
+                acc = __fma_rn(u, mm.y, acc);
+            gm3 = gm2;
+            gm2 = gm1;
+            gm1 = u;
+        }
+    } else {
+        const double *M = reinterpret_cast<const double *>(M2);
+        for (int k = 4; k <= pmax; ++k) {
+            double t = __fma_rn(a0, c_rcp[k - 1], -ci) * gm1;
+            t = __fma_rn(-ir3, gm2, t);
+            t = __fma_rn(-inv, gm3, t);
+            if (k <= pu)
+                acc = __fma_rn(t, __ldg(M + k), acc);
+            gm3 = gm2;
+            gm2 = gm1;
+            gm1 = t;
+        }
     }
     return acc;
 }
@@ -335,7 +423,7 @@ __device__ __forceinline__ double near_field(const double2 *__restrict__ xq, int
 #define FNV_OFF 1469598103934665603ULL
 #define FNV_MUL 1099511628211ULL
 
-template <bool ADAPTIVE, bool STATS>
+template <bool ADAPTIVE, bool STATS, bool WIDE>
 __global__ void __launch_bounds__(EVAL_THREADS) tree_eval_kernel(EvalArgs a)
 {
     if (ADAPTIVE)
@@ -424,7 +512,10 @@ __global__ void __launch_bounds__(EVAL_THREADS) tree_eval_kernel(EvalArgs a)
                 }
                 const int pmax = __reduce_max_sync(DT_FULL, pu);
                 if (far) {
-                    acc += far_field(d, a.rd2, a.moments + (int64_t)node * a.stride, pu, pmax);
+                    acc += far_field<WIDE>(
+                        d, a.rd2,
+                        reinterpret_cast<const double2 *>(a.moments + (int64_t)node * a.stride),
+                        pu, pmax);
                     if (STATS) {
                         hh = (hh ^ ((uint64_t)node * 256u + (uint64_t)pu)) * FNV_MUL;
                         ++c_far;
@@ -494,6 +585,28 @@ __global__ void pack_tree_kernel(const double *__restrict__ c, const double *__r
     out[i] = nd;
 }
 
+// Reference-semantics moments [n][stride] -> traversal layout M'_0 = m_0,
+// M'_k = (k-1)! m_k, even stride (for the seam mirror dt_tree_phi_sum).
+__global__ void scale_moments_kernel(const double *__restrict__ m, int64_t stride, int64_t n,
+                                     double *__restrict__ out, int64_t estride)
+{
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n * estride)
+        return;
+    int64_t node = i / estride;
+    int k = (int)(i - node * estride);
+    double v = 0.0;
+    if (k < stride) {
+        v = m[node * stride + k];
+        double f = 1.0;
+        for (int j = 2; j < k; ++j)
+            f *= (double)j;
+        if (k >= 1)
+            v = __dmul_rn(v, f);
+    }
+    out[i] = v;
+}
+
 __global__ void pack_sources_kernel(const double *__restrict__ xs, const double *__restrict__ qs,
                                     int64_t n, double2 *__restrict__ xq)
 {
@@ -536,17 +649,22 @@ __global__ void choose_p_kernel(const double *__restrict__ R, const double *__re
         tier_out[i] = tier;
 }
 
+template <bool A, bool S>
+const void *pick_kernel(bool wide)
+{
+    return wide ? (const void *)tree_eval_kernel<A, S, true>
+                : (const void *)tree_eval_kernel<A, S, false>;
+}
+
 int launch_eval(EvalArgs &a, bool adaptive, bool stats, cudaStream_t s)
 {
     DT_CUDA_TRY(cudaMemsetAsync(a.counter, 0, sizeof(unsigned long long), s));
     int per_sm = 0;
-    const void *fn;
-    if (adaptive)
-        fn = stats ? (const void *)tree_eval_kernel<true, true>
-                   : (const void *)tree_eval_kernel<true, false>;
-    else
-        fn = stats ? (const void *)tree_eval_kernel<false, true>
-                   : (const void *)tree_eval_kernel<false, false>;
+    const bool wide = a.stride > 32;
+    const void *fn = adaptive ? (stats ? pick_kernel<true, true>(wide)
+                                       : pick_kernel<true, false>(wide))
+                              : (stats ? pick_kernel<false, true>(wide)
+                                       : pick_kernel<false, false>(wide));
     DT_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, EVAL_THREADS, 0));
     if (per_sm < 1)
         per_sm = 1;
@@ -591,9 +709,12 @@ extern "C" int dt_pack_tree(const double *centers, const double *halves, const i
     return DT_OK;
 }
 
-extern "C" size_t dt_tree_eval_workspace(int64_t n_nodes, int64_t n_src)
+static inline int64_t even_stride(int64_t stride) { return (stride + 1) & ~(int64_t)1; }
+
+extern "C" size_t dt_tree_eval_workspace(int64_t n_nodes, int64_t n_src, int64_t moment_stride)
 {
-    return 256 + (size_t)n_nodes * sizeof(dt_node) + (size_t)n_src * 2 * sizeof(double);
+    return 256 + (size_t)n_nodes * sizeof(dt_node) + (size_t)n_src * 2 * sizeof(double) +
+           (size_t)n_nodes * even_stride(moment_stride) * sizeof(double);
 }
 
 static int check_eval_args(int64_t n_nodes, int64_t n_src, int64_t p, int adaptive,
@@ -725,19 +846,25 @@ extern "C" int dt_tree_phi_sum(const double *centers, const double *halves, cons
         return rc;
     if (i1 == i0)
         return DT_OK;
-    if (!workspace || workspace_bytes < dt_tree_eval_workspace(n_nodes, n_src))
+    if (!workspace || workspace_bytes < dt_tree_eval_workspace(n_nodes, n_src, moment_stride))
         return dt_set_error(DT_ERR_WORKSPACE, "eval workspace too small");
     char *ws = (char *)workspace;
     void *packed = ws + 256;
     double *xq = (double *)(ws + 256 + (size_t)n_nodes * sizeof(dt_node));
+    double *meval = xq + 2 * n_src;
+    const int64_t estride = even_stride(moment_stride);
     rc = dt_pack_tree(centers, halves, starts, ends, lefts, rights, n_nodes, packed, stream);
     if (rc != DT_OK)
         return rc;
     rc = dt_pack_sources(xs, qs, n_src, xq, stream);
     if (rc != DT_OK)
         return rc;
-    return dt_tree_phi_sum_packed(packed, n_nodes, moments, moment_stride, xq, n_src, rd2, theta,
-                                  p, adaptive, tol_share, p_cap, cos_tab, sin_tab, n_samples, ys,
+    const int64_t total = n_nodes * estride;
+    scale_moments_kernel<<<(unsigned)((total + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+        moments, moment_stride, n_nodes, meval, estride);
+    DT_CUDA_TRY(cudaGetLastError());
+    return dt_tree_phi_sum_packed(packed, n_nodes, meval, estride, xq, n_src, rd2, theta, p,
+                                  adaptive, tol_share, p_cap, cos_tab, sin_tab, n_samples, ys,
                                   out, i0, i1, accumulate, DT_PSEL_FAST, nullptr, ws, 256,
                                   stream);
 }

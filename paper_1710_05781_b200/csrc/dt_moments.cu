@@ -31,6 +31,8 @@ struct MomArgs {
     const int64_t *start, *end, *left, *right, *meta;
     int64_t order;
     double *moments;
+    double *meval;     // optional traversal copy: M'_0 = m_0, M'_k = (k-1)! m_k
+    int64_t estride;   // its row stride (even, >= order + 1; pad entries are 0)
 };
 
 __constant__ double c_inv_k[MAX_ORDER1] = {  // 1/k rounded to nearest (k >= 1)
@@ -68,7 +70,53 @@ __constant__ double c_inv_k[MAX_ORDER1] = {  // 1/k rounded to nearest (k >= 1)
     0x1.0842108421084p-7, 0x1.0624dd2f1a9fcp-7, 0x1.0410410410410p-7, 0x1.0204081020408p-7,
 };
 
+__constant__ double c_fact_km1[MAX_ORDER1] = {  // (k-1)! rounded (k >= 1)
+    0.0, 0x1.0000000000000p+0, 0x1.0000000000000p+0, 0x1.0000000000000p+1,
+    0x1.8000000000000p+2, 0x1.8000000000000p+4, 0x1.e000000000000p+6, 0x1.6800000000000p+9,
+    0x1.3b00000000000p+12, 0x1.3b00000000000p+15, 0x1.6260000000000p+18, 0x1.baf8000000000p+21,
+    0x1.308a800000000p+25, 0x1.c8cfc00000000p+28, 0x1.7328cc0000000p+32, 0x1.44c3b28000000p+36,
+    0x1.3077775800000p+40, 0x1.3077775800000p+44, 0x1.437eeecd80000p+48, 0x1.6beecca730000p+52,
+    0x1.b02b930689000p+56, 0x1.0e1b3be415a00p+61, 0x1.6283be9b5c620p+65, 0x1.e77526159f06cp+69,
+    0x1.5e5c335f8a4cep+74, 0x1.06c52687a7b9ap+79, 0x1.9a940c33f6121p+83, 0x1.4d9849ea37eebp+88,
+    0x1.19787e5d9f316p+93, 0x1.ec92dd23d6967p+97, 0x1.be6518687a785p+102, 0x1.a27ec6e1f2d0dp+107,
+    0x1.956ad0aae33a4p+112, 0x1.956ad0aae33a4p+117, 0x1.a21627303a541p+122, 0x1.bc3789a33df96p+127,
+    0x1.e5dcbe8a8bc8cp+132, 0x1.114c2b2deea0fp+138, 0x1.3c0011ed1bea1p+143, 0x1.774015499125fp+148,
+    0x1.c95619f1a8e64p+153, 0x1.1dd5d037098fep+159, 0x1.6e39f2c684406p+164, 0x1.e0ac0ea48d948p+169,
+    0x1.42f399d68f1fcp+175, 0x1.bc0ef38704cbbp+180, 0x1.383a833aef5f3p+186, 0x1.c0d41ca4b818ep+191,
+    0x1.499bc508f7324p+197, 0x1.ee69a78d72cb6p+202, 0x1.7a88e4484be3bp+208, 0x1.27baf2587b49ep+214,
+    0x1.d751f23d047dcp+219, 0x1.7ef294d193a63p+225, 0x1.3d20e33d8e45ap+231, 0x1.0b93bfbbf00acp+237,
+    0x1.cbe5f18b04928p+242, 0x1.92693359a4003p+248, 0x1.6665b1bbd6102p+254, 0x1.44cc291239feap+260,
+    0x1.2b6c35dccd76cp+266, 0x1.18b5727f009f5p+272, 0x1.0b8cf1210c97ep+278, 0x1.0330899804332p+284,
+    0x1.fe478ee34844ap+289, 0x1.fe478ee34844ap+295, 0x1.0320568f6ab2ep+302, 0x1.0b395943e6087p+308,
+    0x1.17c0097314d0dp+314, 0x1.293c0a0a461dep+320, 0x1.4074bad313983p+326, 0x1.5e7fac56dd6e8p+332,
+    0x1.84d5a3305da69p+338, 0x1.b5705796695b6p+344, 0x1.f2f423e7902c4p+350, 0x1.207524c1df599p+357,
+    0x1.5209471331bd0p+363, 0x1.916b0466cb107p+369, 0x1.e2f4c14bac4fcp+375, 0x1.264d25ca1d009p+382,
+    0x1.6b473aa57bcccp+388, 0x1.c619094edabffp+394, 0x1.1f5bd7e3e66d7p+401, 0x1.702dac9bff3c4p+407,
+    0x1.dd7b3bda4f022p+413, 0x1.3958df4743d96p+420, 0x1.a02a088aa61cbp+426, 0x1.179c3dbd279b5p+433,
+    0x1.7c1863ed21d72p+439, 0x1.0550c4b30743ep+446, 0x1.6b645188f61a6p+452, 0x1.ff0512a89a152p+458,
+    0x1.6b4d9b43dd8b0p+465, 0x1.051fc798c73bfp+472, 0x1.7b722e0a01831p+478, 0x1.16a7d9cf591c4p+485,
+    0x1.9da1274fc845fp+491, 0x1.3638dd7bd6347p+498, 0x1.d62e2fafb0a78p+504, 0x1.67fb5c8283404p+511,
+    0x1.166c698cf183bp+518, 0x1.b30964ec395dcp+524, 0x1.574569a265440p+531, 0x1.118b502d68b23p+538,
+    0x1.b83c3509147ecp+544, 0x1.65b0eb1760a70p+551, 0x1.256b20d92d490p+558, 0x1.e5f96e67b300ep+564,
+    0x1.963e824aafa2cp+571, 0x1.56c4bdef04315p+578, 0x1.23e389bd89920p+585, 0x1.f5af14bdc472fp+591,
+    0x1.b30dd3fc905bap+598, 0x1.7cac197cfe503p+605, 0x1.500fee805882dp+612, 0x1.2b4e306a4ed48p+619,
+    0x1.0ce83f7f82d2fp+626, 0x1.e764f3171d1e4p+632, 0x1.bd824633209dbp+639, 0x1.9ab418b722116p+646,
+    0x1.7dd36efa41ac2p+653, 0x1.65f6380a9d916p+660, 0x1.5262c0fa08f37p+667, 0x1.42861fee50880p+674,
+    0x1.35ece2af0162bp+681, 0x1.2c3d7b998957ap+688, 0x1.25340ab3f01f9p+695, 0x1.209f3a89205f1p+702,
+};
+
 __device__ __forceinline__ double inv_k(int k) { return c_inv_k[k]; }
+
+// Store m_k of `node` (and its scaled traversal copy).
+__device__ __forceinline__ void put_moment(const MomArgs &a, int64_t node, int k, double m)
+{
+    a.moments[node * (a.order + 1) + k] = m;
+    if (a.meval) {
+        a.meval[node * a.estride + k] = k == 0 ? m : __dmul_rn(m, c_fact_km1[k]);
+        if (k == a.order && a.estride > a.order + 1)
+            a.meval[node * a.estride + k + 1] = 0.0;
+    }
+}
 
 // P2M for one leaf, order + 1 <= 32, one warp.
 __device__ void p2m_leaf_reg(const MomArgs &a, int64_t node, double (*tr)[33])
@@ -102,7 +150,7 @@ __device__ void p2m_leaf_reg(const MomArgs &a, int64_t node, double (*tr)[33])
 #pragma unroll 8
         for (int l = 0; l < 32; ++l)
             sum += tr[lane][l];
-        a.moments[node * o1 + lane] = sum;
+        put_moment(a, node, lane, sum);
     }
     __syncwarp();
 }
@@ -134,7 +182,7 @@ __device__ void p2m_leaf_generic(const MomArgs &a, int64_t node, double *row_sme
     }
     __syncwarp();
     for (int k = lane; k < o1; k += 32)
-        a.moments[node * o1 + k] = row_smem[k];
+        put_moment(a, node, k, row_smem[k]);
     __syncwarp();
 }
 
@@ -189,7 +237,7 @@ __device__ void m2m_node(const MomArgs &a, int64_t node, double *pw, double *mro
     for (int i = 0; i < MAX_ORDER1 / 32; ++i) {
         int k = lane + 32 * i;
         if (k < o1)
-            a.moments[node * o1 + k] = out[i];
+            put_moment(a, node, k, out[i]);
     }
 }
 
@@ -235,12 +283,16 @@ __global__ void __launch_bounds__(MOM_THREADS) moments_kernel(MomArgs a)
 extern "C" int dt_moments(const double *xs, const double *qs, const double *center,
                           const int64_t *start, const int64_t *end, const int64_t *left,
                           const int64_t *right, const int64_t *meta, int64_t order,
-                          double *moments, void *stream)
+                          double *moments, double *moments_eval, int64_t eval_stride,
+                          void *stream)
 {
+    DT_CHECK_ARG(!moments_eval || (eval_stride >= order + 1 && eval_stride % 2 == 0),
+                 "eval_stride must be even and >= order + 1");
     DT_CHECK_ARG(order >= 0 && order < MAX_ORDER1, "moment order must be in [0, 127]");
     DT_CHECK_ARG(xs && qs && center && start && end && left && right && meta && moments,
                  "null pointer");
-    MomArgs a{xs, qs, center, start, end, left, right, meta, order, moments};
+    MomArgs a{xs, qs, center, start, end, left, right, meta, order, moments, moments_eval,
+              eval_stride};
     int per_sm = 0;
     DT_CUDA_TRY(
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, moments_kernel, MOM_THREADS, 0));

@@ -24,6 +24,7 @@ from .tree import (
     EvalConfig,
     TreeBuffers,
     contour_tables,
+    eval_stride,
     initial_node_capacity,
     launch_moments,
     moment_order_for,
@@ -44,6 +45,8 @@ class TreePipeline:
         cap = node_capacity or initial_node_capacity(n, config.leaf_capacity)
         self.bufs = TreeBuffers(self.n, cap, self.dev)
         self.moments = torch.empty((cap, self.order + 1), dtype=torch.float64, device=self.dev)
+        self.estride = eval_stride(self.order)
+        self.meval = torch.empty((cap, self.estride), dtype=torch.float64, device=self.dev)
         self.prefix = torch.empty(self.n, dtype=torch.float64, device=self.dev)
         L = _lib.load()
         self.scan_ws_bytes = int(L.dt_prefix_scan_workspace(self.n))
@@ -88,14 +91,14 @@ class TreePipeline:
         _lib.check(L.dt_sign_terms(p(xs), p(self.prefix), self.n, p(ys_part), p(out_part),
                                    i1 - i0, s), "dt_sign_terms")
         self.bufs.launch(xs, cfg.leaf_capacity)
-        launch_moments(self.bufs, xs, qs, self.order, self.moments)
+        launch_moments(self.bufs, xs, qs, self.order, self.moments, self.meval)
         pack_sources(xs, qs, self.xq)
         if eval_events is not None:
             eval_events[0].record()
         _lib.check(
             L.dt_tree_eval_device(
-                p(self.bufs.packed), p(self.bufs.meta), self.bufs.capacity, p(self.moments),
-                self.order + 1, p(self.xq), self.n, self.kernel.r_d * self.kernel.r_d,
+                p(self.bufs.packed), p(self.bufs.meta), self.bufs.capacity, p(self.meval),
+                self.estride, p(self.xq), self.n, self.kernel.r_d * self.kernel.r_d,
                 float(cfg.theta), int(cfg.p), int(bool(cfg.adaptive)), float(cfg.tolerance),
                 self.order, p(self.cos_t), p(self.sin_t), self.cos_t.numel(), p(ys), p(out),
                 int(i0), int(i1), 1, p(self.eval_ws), self.eval_ws.numel(), s,

@@ -73,6 +73,7 @@ class Tree:
     leaf_count: int
     build_seconds: float
     # device-side extras for the traversal kernel
+    meval: torch.Tensor = field(repr=False, default=None)
     packed: torch.Tensor = field(repr=False, default=None)
     xq: torch.Tensor = field(repr=False, default=None)
     meta: torch.Tensor = field(repr=False, default=None)
@@ -184,13 +185,19 @@ class TreeBuffers:
         )
 
 
-def launch_moments(bufs: TreeBuffers, xs, qs, order: int, moments: torch.Tensor) -> None:
+def eval_stride(order: int) -> int:
+    """Row stride of the traversal moment layout (even, >= order + 1)."""
+    return (order + 2) & ~1
+
+
+def launch_moments(bufs: TreeBuffers, xs, qs, order: int, moments: torch.Tensor,
+                   meval: torch.Tensor | None = None) -> None:
     L = _lib.load()
     p = _lib.ptr
     _lib.check(
         L.dt_moments(p(xs), p(qs), p(bufs.center), p(bufs.start), p(bufs.end), p(bufs.left),
-                     p(bufs.right), p(bufs.meta), int(order), p(moments),
-                     _lib.stream_handle()),
+                     p(bufs.right), p(bufs.meta), int(order), p(moments), p(meval),
+                     eval_stride(order), _lib.stream_handle()),
         "dt_moments",
     )
 
@@ -231,7 +238,8 @@ def build(system: ChargeSystem, kernel: DiscKernel, config: EvalConfig) -> Tree:
     n_nodes = int(meta[_lib.DT_META_NODES])
     order = moment_order_for(config)
     moments = torch.empty((n_nodes, order + 1), dtype=torch.float64, device=dev)
-    launch_moments(bufs, system.xs, system.qs, order, moments)
+    meval = torch.empty((n_nodes, eval_stride(order)), dtype=torch.float64, device=dev)
+    launch_moments(bufs, system.xs, system.qs, order, moments, meval)
     xq = pack_sources(system.xs, system.qs)
     torch.cuda.synchronize(dev)
     elapsed = time.perf_counter() - t0
@@ -242,7 +250,7 @@ def build(system: ChargeSystem, kernel: DiscKernel, config: EvalConfig) -> Tree:
         end=bufs.end[:n_nodes], left=bufs.left[:n_nodes], right=bufs.right[:n_nodes],
         moments=moments, moment_order=order, depth=int(meta[_lib.DT_META_DEPTH]),
         leaf_count=int(meta[_lib.DT_META_LEAVES]), build_seconds=elapsed,
-        packed=bufs.packed[: n_nodes * 32], xq=xq, meta=bufs.meta,
+        meval=meval, packed=bufs.packed[: n_nodes * 32], xq=xq, meta=bufs.meta,
     )
 
 
@@ -291,7 +299,7 @@ def tree_phi_sum(tree: Tree, kernel: DiscKernel, config: EvalConfig, ys: torch.T
     p = _lib.ptr
     _lib.check(
         _lib.load().dt_tree_phi_sum_packed(
-            p(tree.packed), len(tree), p(tree.moments), tree.moment_order + 1, p(tree.xq),
+            p(tree.packed), len(tree), p(tree.meval), tree.meval.shape[1], p(tree.xq),
             len(tree.system), kernel.r_d * kernel.r_d, float(config.theta), int(config.p),
             int(bool(config.adaptive)), _tol_share(tree, config), int(tree.moment_order),
             p(cos_t), p(sin_t), cos_t.numel(), p(ys), p(out), int(i0), int(i1),

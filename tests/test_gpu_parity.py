@@ -292,3 +292,35 @@ def test_direct_matches_mpmath(dt):
             dd = mpmath.mpf(x) - mpmath.mpf(y)
             acc += mpmath.mpf(q) * dd / mpmath.sqrt(dd * dd + mpmath.mpf(0.05) ** 2)
         assert v == pytest.approx(float(2 * below - tot + acc), rel=1e-13, abs=1e-13)
+
+
+def test_seam_mirror_entry(dt):
+    """dt_tree_phi_sum takes the reference seam's SoA arrays and moments
+    (_kernels.py:164-186) and matches the packed path."""
+    from paper_1710_05781_b200 import _lib
+    from paper_1710_05781_b200.tree import contour_tables, tree_phi_sum
+
+    g = load_case("cfg2s")
+    system = _system(dt, g)
+    kernel = dt.DiscKernel(float(g["r_d"]))
+    cfg = _config(dt, g)
+    tree = dt.build(system, kernel, cfg)
+    ys = torch.from_numpy(g["targets"]).cuda()
+    want = torch.zeros_like(ys)
+    tree_phi_sum(tree, kernel, cfg, ys, want, accumulate=False)
+    got = torch.zeros_like(ys)
+    L = _lib.load()
+    stride = tree.moment_order + 1
+    ws_bytes = L.dt_tree_eval_workspace(len(tree), len(system), stride)
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device="cuda")
+    c, s = contour_tables(ys.device)
+    p = _lib.ptr
+    _lib.check(L.dt_tree_phi_sum(
+        p(tree.center), p(tree.half), p(tree.start), p(tree.end), p(tree.left), p(tree.right),
+        p(tree.moments), stride, len(tree), p(system.xs), p(system.qs), len(system),
+        kernel.r_d ** 2, cfg.theta, cfg.p, 1, cfg.tolerance / (3.0 * tree.depth),
+        tree.moment_order, p(c), p(s), 64, p(ys), p(got), 0, ys.numel(), 0, p(ws), ws_bytes,
+        _lib.stream_handle()), "dt_tree_phi_sum")
+    scale = np.abs(g["qs"]).sum()
+    assert float((got - want).abs().max()) <= 1e-14 * scale
+    assert np.max(np.abs(got.cpu().numpy() - g["phi_tree"])) <= 1e-13 * scale
