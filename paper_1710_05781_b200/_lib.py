@@ -11,7 +11,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libdisctree_b200.so")
+LIB_PATH = os.environ.get("DISCTREE_B200_LIB", os.path.join(_HERE, "libdisctree_b200.so"))
 
 DT_OK = 0
 DT_PSEL_FAST = 0

@@ -35,6 +35,9 @@
 
 namespace {
 
+#ifndef DT_EVAL_MINB
+#define DT_EVAL_MINB 4
+#endif
 constexpr int EVAL_THREADS = 256;
 constexpr int EVAL_WARPS = EVAL_THREADS / 32;
 constexpr int STACK_DEPTH = 64;         // >= max_depth + 2
@@ -235,7 +238,7 @@ __device__ int psel_fast(double big_r, double h, const EvalArgs &a, const float 
         return -1;
     const float ratio = __fdividef(hf, Rf);
     const float sstar = __fdividef(rd2f, Rf * Rf);
-    if (!(sstar > 1e-12f) || !(sstar < 1e30f))
+    if (!(sstar > 1e-12f) || !(sstar < 1e30f) || !(ratio > 1e-30f))
         return -1;
     // bracket: s_t = 4 sin^2(pi t / 64) = s*  ->  t* = (64/pi) asin(sqrt(s*)/2);
     // asin via Abramowitz-Stegun 4.4.45 (|err| < 7e-5 rad), enough to place
@@ -246,14 +249,11 @@ __device__ int psel_fast(double big_r, double h, const EvalArgs &a, const float 
                             1.5707288f);
     const float asz = 1.57079633f - om * rsqrtf(fmaxf(om, 1e-30f)) * poly;
     const int t0 = (int)floorf(asz * 20.371832715762604f);
-    float emin = 3.0e38f;
-#pragma unroll
-    for (int c = -1; c <= 2; ++c) {
-        const int t = min(max(t0 + c, 1), 32);
-        const float u = sstar * isig[t];
-        const float e = (1.0f - u) * (1.0f - u);
-        emin = fminf(emin, e);
-    }
+    // the sampled maximum is at t0 or t0 + 1 (a t* error of ~1e-3 samples
+    // can only swap in the sample sitting on the peak, which then wins)
+    const int ta = min(max(t0, 1), 32), tb = min(t0 + 1, 32);
+    const float ua = sstar * isig[ta], ub = sstar * isig[tb];
+    const float emin = fminf((1.0f - ua) * (1.0f - ua), (1.0f - ub) * (1.0f - ub));
     const float Q = emin + sstar;         // M^-4
     const float rq = rsqrtf(Q);
     const float M = rq * rsqrtf(rq);      // Q^(-1/4): sampled contour maximum of |f|
@@ -328,7 +328,7 @@ __constant__ double c_rcp[128] = {  // 1/k (k >= 1)
 // 16-byte aligned, read two at a time).  5 FP64 instructions per order.
 template <bool WIDE>
 __device__ __forceinline__ double far_field(double d, double rd2, const double2 *__restrict__ M2,
-                                            int pu, int pmax)
+                                            int pu, int pmin, int pmax)
 {
     const double s2 = __fma_rn(d, d, rd2);
     const double r = dt_rsqrt(s2);
@@ -357,43 +357,40 @@ __device__ __forceinline__ double far_field(double d, double rd2, const double2 
     if (pu >= 3)
         acc = __fma_rn(g3, m23.y, acc);
     double gm3 = g1, gm2 = g2, gm1 = g3;
+    int k = 4;
     if (!WIDE) {
+        // orders every far lane of the warp needs (k <= pmin): no masking
 #pragma unroll
-        for (int k = 4; k < 32; k += 2) {
-            if (k > pmax)
+        for (int kk = 4; kk < 32; kk += 2) {
+            if (kk + 1 > pmin)
                 break;
-            const double2 mm = __ldg(M2 + k / 2);
-            double t = __fma_rn(a0, 1.0 / (k - 1), -ci) * gm1;
+            const double2 mm = __ldg(M2 + kk / 2);
+            double t = __fma_rn(a0, 1.0 / (kk - 1), -ci) * gm1;
             t = __fma_rn(-ir3, gm2, t);
             t = __fma_rn(-inv, gm3, t);
-            if (k <= pu)
-                acc = __fma_rn(t, mm.x, acc);
-            gm3 = gm2;
-            gm2 = gm1;
-            gm1 = t;
-            if (k + 1 > pmax)
-                break;
-            double u = __fma_rn(a0, 1.0 / k, -ci) * gm1;
-            u = __fma_rn(-ir3, gm2, u);
-            u = __fma_rn(-inv, gm3, u);
-            if (k + 1 <= pu)
-                acc = __fma_rn(u, mm.y, acc);
-            gm3 = gm2;
-            gm2 = gm1;
+            acc = __fma_rn(t, mm.x, acc);
+            double u = __fma_rn(a0, 1.0 / kk, -ci) * t;
+            u = __fma_rn(-ir3, gm1, u);
+            u = __fma_rn(-inv, gm2, u);
+            acc = __fma_rn(u, mm.y, acc);
+            gm3 = gm1;
+            gm2 = t;
             gm1 = u;
+            k = kk + 2;
         }
-    } else {
-        const double *M = reinterpret_cast<const double *>(M2);
-        for (int k = 4; k <= pmax; ++k) {
-            double t = __fma_rn(a0, c_rcp[k - 1], -ci) * gm1;
-            t = __fma_rn(-ir3, gm2, t);
-            t = __fma_rn(-inv, gm3, t);
-            if (k <= pu)
-                acc = __fma_rn(t, __ldg(M + k), acc);
-            gm3 = gm2;
-            gm2 = gm1;
-            gm1 = t;
-        }
+    }
+    // remaining orders up to the warp maximum, masked per lane
+    const double *M = reinterpret_cast<const double *>(M2);
+#pragma unroll 1
+    for (; k <= pmax; ++k) {
+        double t = __fma_rn(a0, c_rcp[k - 1], -ci) * gm1;
+        t = __fma_rn(-ir3, gm2, t);
+        t = __fma_rn(-inv, gm3, t);
+        if (k <= pu)
+            acc = __fma_rn(t, __ldg(M + k), acc);
+        gm3 = gm2;
+        gm2 = gm1;
+        gm1 = t;
     }
     return acc;
 }
@@ -424,7 +421,7 @@ __device__ __forceinline__ double near_field(const double2 *__restrict__ xq, int
 #define FNV_MUL 1099511628211ULL
 
 template <bool ADAPTIVE, bool STATS, bool WIDE>
-__global__ void __launch_bounds__(EVAL_THREADS) tree_eval_kernel(EvalArgs a)
+__global__ void __launch_bounds__(EVAL_THREADS, DT_EVAL_MINB) tree_eval_kernel(EvalArgs a)
 {
     if (ADAPTIVE)
         a.tol_share = tol_share_of(a);
@@ -511,11 +508,12 @@ __global__ void __launch_bounds__(EVAL_THREADS) tree_eval_kernel(EvalArgs a)
                     }
                 }
                 const int pmax = __reduce_max_sync(DT_FULL, pu);
+                const int pmin = __reduce_min_sync(DT_FULL, far ? pu : 1 << 20);
                 if (far) {
                     acc += far_field<WIDE>(
                         d, a.rd2,
                         reinterpret_cast<const double2 *>(a.moments + (int64_t)node * a.stride),
-                        pu, pmax);
+                        pu, pmin, pmax);
                     if (STATS) {
                         hh = (hh ^ ((uint64_t)node * 256u + (uint64_t)pu)) * FNV_MUL;
                         ++c_far;
