@@ -81,9 +81,13 @@ int dt_prefix_scan(const double *qs, double *prefix, int64_t n, void *workspace,
 
 /* e(y) = 2 * prefix_excl[lower_bound(xs, y)] - total, total = prefix[n-1]
  * (charges.py:183-187 _sign_terms; a source exactly at y counts on the minus
- * side).  Targets in any order.  n == 0 gives e = 0. */
+ * side).  Targets in any order (ascending runs are located through shared
+ * memory when a workspace of dt_sign_terms_workspace() bytes is given; NULL
+ * workspace searches every target in global memory).  n == 0 gives e = 0. */
+size_t dt_sign_terms_workspace(int64_t n_targets);
 int dt_sign_terms(const double *xs, const double *prefix, int64_t n, const double *ys,
-                  double *e_out, int64_t n_targets, void *stream);
+                  double *e_out, int64_t n_targets, void *workspace, size_t workspace_bytes,
+                  void *stream);
 
 /* ---------------------------------------------------------------- (b) */
 
@@ -106,15 +110,18 @@ int dt_build_tree(const double *xs, int64_t n, int64_t leaf_capacity, int64_t ma
 
 /* Node moments m_k = sum_j q_j (x_j - c)^k / k!, k = 0..order, row-major
  * [n_nodes][order + 1] (tree.py:224-238): P2M at every leaf from its sources,
- * then M2M (binomial shift) bottom-up level by level.  Reads the tree
- * produced by dt_build_tree (meta gives n_nodes, depth and level ranges).
+ * then M2M (binomial shift) bottom-up as a dataflow (a node is formed by the
+ * warp that finishes its last child).  Reads the tree produced by
+ * dt_build_tree (meta gives n_nodes); node_capacity bounds the node arrays.
  * moments_eval (optional) receives the traversal layout used by the *_packed
  * and *_device evaluators: M'_0 = m_0, M'_k = (k-1)! m_k, row stride
  * eval_stride (even, >= order + 1; padding zeroed). */
+size_t dt_moments_workspace(int64_t node_capacity);
 int dt_moments(const double *xs, const double *qs, const double *center, const int64_t *start,
                const int64_t *end, const int64_t *left, const int64_t *right,
                const int64_t *meta, int64_t order, double *moments, double *moments_eval,
-               int64_t eval_stride, void *stream);
+               int64_t eval_stride, int64_t node_capacity, void *workspace,
+               size_t workspace_bytes, void *stream);
 
 /* ---------------------------------------------------------------- (d)+(e) */
 

@@ -53,13 +53,17 @@ SIGNATURES = {
     "dt_device_check": (C.c_int, []),
     "dt_prefix_scan_workspace": (_SZ, [_I64]),
     "dt_prefix_scan": (C.c_int, [_P, _P, _I64, _P, _SZ, _P]),
-    "dt_sign_terms": (C.c_int, [_P, _P, _I64, _P, _P, _I64, _P]),
+    "dt_sign_terms_workspace": (_SZ, [_I64]),
+    "dt_sign_terms": (C.c_int, [_P, _P, _I64, _P, _P, _I64, _P, _SZ, _P]),
     "dt_build_workspace": (_SZ, [_I64, _I64]),
     "dt_build_tree": (
         C.c_int,
         [_P, _I64, _I64, _I64, _I64, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P],
     ),
-    "dt_moments": (C.c_int, [_P, _P, _P, _P, _P, _P, _P, _P, _I64, _P, _P, _I64, _P]),
+    "dt_moments_workspace": (_SZ, [_I64]),
+    "dt_moments": (
+        C.c_int, [_P, _P, _P, _P, _P, _P, _P, _P, _I64, _P, _P, _I64, _I64, _P, _SZ, _P],
+    ),
     "dt_pack_sources": (C.c_int, [_P, _P, _I64, _P, _P]),
     "dt_pack_tree": (C.c_int, [_P, _P, _P, _P, _P, _P, _I64, _P, _P]),
     "dt_tree_eval_workspace": (_SZ, [_I64, _I64, _I64]),

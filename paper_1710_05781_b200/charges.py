@@ -120,9 +120,12 @@ def _sign_terms(system: ChargeSystem, targets: torch.Tensor) -> torch.Tensor:
     if T == 0:
         return out
     L = _lib.load()
+    ws_bytes = int(L.dt_sign_terms_workspace(T))
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device=targets.device)
     _lib.check(
         L.dt_sign_terms(_lib.ptr(system.xs), _lib.ptr(system.prefix), len(system),
-                        _lib.ptr(targets), _lib.ptr(out), T, _lib.stream_handle()),
+                        _lib.ptr(targets), _lib.ptr(out), T, _lib.ptr(ws), ws_bytes,
+                        _lib.stream_handle()),
         "dt_sign_terms",
     )
     return out

@@ -37,6 +37,7 @@ struct BuildArgs {
     dt_node *packed;
     int64_t *meta;
     int32_t *scratch_off;    // [capacity] local exclusive offset within the block chunk
+    int32_t *scratch_split;  // [capacity] split index found in phase A
     int64_t *block_total;    // [gridDim]
 };
 
@@ -89,12 +90,12 @@ __device__ __forceinline__ int node_children(const BuildArgs &a, int64_t node, i
     return (split > s) + (e > split);
 }
 
-__device__ void emit_children(const BuildArgs &a, int64_t node, int64_t lev, int64_t first_child)
+__device__ void emit_children(const BuildArgs &a, int64_t node, int64_t lev, int64_t first_child,
+                              int64_t split)
 {
     int64_t s = ld_cg(a.start + node), e = ld_cg(a.end + node);
     double lo = ld_cg(a.lo + node), hi = ld_cg(a.hi + node);
     double mid = mid_of(lo, hi);
-    int64_t split = dt_lower_bound(a.xs, s, e, mid);
     int64_t c = first_child;
     int64_t l_slot = -1, r_slot = -1;
     if (split > s) {  // (lo, mid): child_hi == mid -> left
@@ -168,7 +169,7 @@ __device__ int64_t level_in_block(const BuildArgs &a, int64_t f0, int64_t f1, in
         if (next + tot > a.capacity)
             return -1;
         if (nc)
-            emit_children(a, node, lev, next + excl);
+            emit_children(a, node, lev, next + excl, split);
         next += tot;
     }
     *leaves += leaf_acc;
@@ -262,8 +263,10 @@ __global__ void __launch_bounds__(BUILD_THREADS) build_kernel(BuildArgs a)
                 ++leaves;
             int excl;
             int tot = block_excl_scan(nc, &excl, warp_sums);
-            if (node < b1)
+            if (node < b1) {
                 a.scratch_off[node - f0] = (int32_t)(run + excl);
+                a.scratch_split[node - f0] = (int32_t)split;
+            }
             run += tot;
         }
         if (threadIdx.x == 0)
@@ -305,7 +308,8 @@ __global__ void __launch_bounds__(BUILD_THREADS) build_kernel(BuildArgs a)
             int64_t s = ld_cg(a.start + node), e = ld_cg(a.end + node);
             if (e - s <= a.leaf_capacity || lev >= a.max_depth)
                 continue;
-            emit_children(a, node, lev, f1 + base + __ldcg(a.scratch_off + (node - f0)));
+            emit_children(a, node, lev, f1 + base + __ldcg(a.scratch_off + (node - f0)),
+                          __ldcg(a.scratch_split + (node - f0)));
         }
         if (blockIdx.x == 0 && threadIdx.x == 0) {
             a.meta[DT_META_LEVEL0 + lev + 2] = f1 + total;
@@ -323,7 +327,7 @@ __global__ void __launch_bounds__(BUILD_THREADS) build_kernel(BuildArgs a)
 extern "C" size_t dt_build_workspace(int64_t n, int64_t node_capacity)
 {
     (void)n;
-    return (size_t)node_capacity * sizeof(int32_t) + 4096 * sizeof(int64_t);
+    return (size_t)node_capacity * 2 * sizeof(int32_t) + 4096 * sizeof(int64_t) + 16;
 }
 
 extern "C" int dt_build_tree(const double *xs, int64_t n, int64_t leaf_capacity, int64_t max_depth, int64_t node_capacity,
@@ -362,7 +366,8 @@ extern "C" int dt_build_tree(const double *xs, int64_t n, int64_t leaf_capacity,
     a.packed = (dt_node *)packed;
     a.meta = meta;
     a.scratch_off = (int32_t *)workspace;
-    a.block_total = (int64_t *)((char *)workspace + (size_t)node_capacity * sizeof(int32_t));
+    a.scratch_split = a.scratch_off + node_capacity;
+    a.block_total = (int64_t *)((char *)workspace + (size_t)node_capacity * 2 * sizeof(int32_t));
     // 8-byte align block_total
     a.block_total = (int64_t *)(((uintptr_t)a.block_total + 7) & ~(uintptr_t)7);
 

@@ -8,16 +8,14 @@
 // internal node is the sum of its children shifted to its center:
 //     m_k(parent) = sum_{j<=k} m_j(child) * delta^(k-j) / (k-j)!,
 //     delta = c_child - c_parent,
-// bottom-up, one grid barrier per level (cooperative persistent kernel).
+// bottom-up as a dataflow, with no grid barriers: the warp that finishes a
+// node bumps its parent's arrival counter, and the warp that completes the
+// parent's last child goes on to form the parent (BVH-refit style).
 // The shift is exact algebra; round-off differs from the reference's direct
 // sums at the 1e-16 level of sum|q| r^k / k!.
 // Algorithmic HBM bytes: P2M 16 N + 8 (order+1) leaves; M2M 24 (order+1)
 // per internal node (two child rows read, one row written).
-#include <cooperative_groups.h>
-
 #include "dt_common.cuh"
-
-namespace cg = cooperative_groups;
 
 namespace {
 
@@ -33,6 +31,8 @@ struct MomArgs {
     double *moments;
     double *meval;     // optional traversal copy: M'_0 = m_0, M'_k = (k-1)! m_k
     int64_t estride;   // its row stride (even, >= order + 1; pad entries are 0)
+    int32_t *parent;   // workspace: parent index per node (-1 at the root)
+    int32_t *arrived;  // workspace: finished children per node
 };
 
 __constant__ double c_inv_k[MAX_ORDER1] = {  // 1/k rounded to nearest (k >= 1)
@@ -105,6 +105,41 @@ __constant__ double c_fact_km1[MAX_ORDER1] = {  // (k-1)! rounded (k >= 1)
     0x1.35ece2af0162bp+681, 0x1.2c3d7b998957ap+688, 0x1.25340ab3f01f9p+695, 0x1.209f3a89205f1p+702,
 };
 
+__constant__ double c_inv_fact[MAX_ORDER1] = {  // 1/k! rounded
+    0x1.0000000000000p+0, 0x1.0000000000000p+0, 0x1.0000000000000p-1, 0x1.5555555555555p-3,
+    0x1.5555555555555p-5, 0x1.1111111111111p-7, 0x1.6c16c16c16c17p-10, 0x1.a01a01a01a01ap-13,
+    0x1.a01a01a01a01ap-16, 0x1.71de3a556c734p-19, 0x1.27e4fb7789f5cp-22, 0x1.ae64567f544e4p-26,
+    0x1.1eed8eff8d898p-29, 0x1.6124613a86d09p-33, 0x1.93974a8c07c9dp-37, 0x1.ae7f3e733b81fp-41,
+    0x1.ae7f3e733b81fp-45, 0x1.952c77030ad4ap-49, 0x1.6827863b97d97p-53, 0x1.2f49b46814157p-57,
+    0x1.e542ba4020225p-62, 0x1.71b8ef6dcf572p-66, 0x1.0ce396db7f853p-70, 0x1.761b413163819p-75,
+    0x1.f2cf01972f578p-80, 0x1.3f3ccdd165fa9p-84, 0x1.88e85fc6a4e59p-89, 0x1.d1ab1c2dccea3p-94,
+    0x1.0a18a2635085dp-98, 0x1.259f98b4358aep-103, 0x1.3932c5047d60ep-108, 0x1.434d2e783f5bdp-113,
+    0x1.434d2e783f5bdp-118, 0x1.3981254dd0d52p-123, 0x1.2710231c0fd7ap-128, 0x1.0dc59c716d91fp-133,
+    0x1.df983290c2ca8p-139, 0x1.9ec8d1c94e85bp-144, 0x1.5d4acb9c0c3abp-149, 0x1.1e99449a4bacep-154,
+    0x1.ca8ed42a12ae4p-160, 0x1.65e61c39d0241p-165, 0x1.10af527530de8p-170, 0x1.95db45257e512p-176,
+    0x1.272b1b03fec6ap-181, 0x1.a3cb872220648p-187, 0x1.240804f659510p-192, 0x1.8da8e0a127ebap-198,
+    0x1.091b406b6ff27p-203, 0x1.5a42f0dfeb086p-209, 0x1.bb36f6e12cd79p-215, 0x1.161872bf7b824p-220,
+    0x1.56457989358c9p-226, 0x1.9d4f1058674dfp-232, 0x1.e9d8f6ed83eaap-238, 0x1.1d008faac5c50p-243,
+    0x1.45b77f9e98e12p-249, 0x1.6db793c887b97p-255, 0x1.938cc661b03f6p-261, 0x1.b5bfc17fa97d2p-267,
+    0x1.d2eeac43e7fd0p-273, 0x1.e9e56d649f768p-279, 0x1.f9b3059128bc6p-285, 0x1.00dcf6a320e1cp-290,
+    0x1.00dcf6a320e1cp-296, 0x1.f9d2a2bb5471ap-303, 0x1.ea7ead50ce01ap-309, 0x1.d48849da8f4a3p-315,
+    0x1.b8f8bdfae136cp-321, 0x1.99046602abcafp-327, 0x1.75f56494ba531p-333, 0x1.5116e3adb9fb9p-339,
+    0x1.2ba2917dfaa6cp-345, 0x1.06b1981a48762p-351, 0x1.c6639f500ea2dp-358, 0x1.83bed30a49edep-364,
+    0x1.4685bf3115d5dp-370, 0x1.0f653132c5ae6p-376, 0x1.bd5dda94f5a18p-383, 0x1.68cda75b82f10p-389,
+    0x1.20a485e2cf273p-395, 0x1.c8206e6fe560cp-402, 0x1.64005631debbep-408, 0x1.1281cd42368abp-414,
+    0x1.a24be3711628bp-421, 0x1.3af3de7343e27p-427, 0x1.d4c44522a0927p-434, 0x1.58d700d5cb749p-440,
+    0x1.f595d2ab567b0p-447, 0x1.68b0c583d6a34p-453, 0x1.007db446ff080p-459, 0x1.68c751f8f632ap-466,
+    0x1.f5f3ec7bc5d71p-473, 0x1.596e0e189e2b7p-479, 0x1.d65f64e59b771p-486, 0x1.3ce1f3216b6dep-492,
+    0x1.a6829981e4928p-499, 0x1.16c503a23d142p-505, 0x1.6c1b7275dcd65p-512, 0x1.d6c3cf76c59b9p-519,
+    0x1.2d4a1e607e781p-525, 0x1.7dd50faf84657p-532, 0x1.df297d187dfcdp-539, 0x1.29bb552f8772dp-545,
+    0x1.6e7068d8092aep-552, 0x1.beb4eb15fc8c0p-559, 0x1.0db5afbffdea5p-565, 0x1.42a4b5885d34fp-572,
+    0x1.7e64655f3f0f6p-579, 0x1.c10c3547ec1b7p-586, 0x1.05439cac2c47dp-592, 0x1.2d470c4e9d270p-599,
+    0x1.585132a2fcbeep-606, 0x1.8605e345153bep-613, 0x1.b5eba9d8cb7dap-620, 0x1.e76cb424808bcp-627,
+    0x1.0cec86b309210p-633, 0x1.263516a53c4fep-640, 0x1.3f23e47f2bba7p-647, 0x1.5746e043f2ccep-654,
+    0x1.6e2977bff1eb9p-661, 0x1.83584be68daaep-668, 0x1.9665084a05f25p-675, 0x1.a6ea2e16eb21ap-682,
+    0x1.b48ea3306e964p-689, 0x1.bf08d841fa750p-696, 0x1.c6215db8ddeccp-703, 0x1.c9b4c7476cc65p-710,
+};
+
 __device__ __forceinline__ double inv_k(int k) { return c_inv_k[k]; }
 
 // Store m_k of `node` (and its scaled traversal copy).
@@ -118,50 +153,65 @@ __device__ __forceinline__ void put_moment(const MomArgs &a, int64_t node, int k
     }
 }
 
-// P2M for one leaf, order + 1 <= 32, one warp.
-__device__ void p2m_leaf_reg(const MomArgs &a, int64_t node, double (*tr)[33])
+// Store from the raw power sum S_k = sum_j q_j (x_j - c)^k:
+// m_k = S_k / k!, traversal copy (k-1)! m_k = S_k / k.
+__device__ __forceinline__ void put_raw_sum(const MomArgs &a, int64_t node, int k, double S)
+{
+    a.moments[node * (a.order + 1) + k] = __dmul_rn(S, c_inv_fact[k]);
+    if (a.meval) {
+        a.meval[node * a.estride + k] = k == 0 ? S : __dmul_rn(S, c_inv_k[k]);
+        if (k == a.order && a.estride > a.order + 1)
+            a.meval[node * a.estride + k + 1] = 0.0;
+    }
+}
+
+// P2M for one leaf, order + 1 <= 32, one warp: raw power sums in two
+// halves of 16 orders (2 FP64 ops per source and order), smem transpose-
+// reduce over the 32 lanes.
+__device__ void p2m_leaf_reg(const MomArgs &a, int64_t node, int64_t s, int64_t e, double c,
+                             double (*tr)[33])
 {
     const int lane = dt_lane();
     const int o1 = (int)a.order + 1;
-    const int64_t s = a.start[node], e = a.end[node];
-    const double c = a.center[node];
-    double acc[REG_ORDER];
+    for (int base = 0; base < o1; base += 16) {
+        double acc[16];
 #pragma unroll
-    for (int k = 0; k < REG_ORDER; ++k)
-        acc[k] = 0.0;
-    for (int64_t j = s + lane; j < e; j += 32) {
-        double t = __ldg(a.xs + j) - c;
-        double term = __ldg(a.qs + j);
-        acc[0] += term;
+        for (int k = 0; k < 16; ++k)
+            acc[k] = 0.0;
+        for (int64_t j = s + lane; j < e; j += 32) {
+            const double t = __ldg(a.xs + j) - c;
+            double w = __ldg(a.qs + j);
+            if (base) {
+                const double t2 = t * t, t4 = t2 * t2, t8 = t4 * t4;
+                w *= t8 * t8;
+            }
 #pragma unroll
-        for (int k = 1; k < REG_ORDER; ++k) {
-            if (k < o1) {
-                term *= t * inv_k(k);
-                acc[k] += term;
+            for (int k = 0; k < 16; ++k) {
+                acc[k] += w;
+                w *= t;
             }
         }
-    }
 #pragma unroll
-    for (int k = 0; k < REG_ORDER; ++k)
-        tr[k][lane] = acc[k];
-    __syncwarp();
-    if (lane < o1) {
-        double sum = 0.0;
+        for (int k = 0; k < 16; ++k)
+            tr[k][lane] = acc[k];
+        __syncwarp();
+        if (lane < 16 && base + lane < o1) {
+            double sum = 0.0;
 #pragma unroll 8
-        for (int l = 0; l < 32; ++l)
-            sum += tr[lane][l];
-        put_moment(a, node, lane, sum);
+            for (int l = 0; l < 32; ++l)
+                sum += tr[lane][l];
+            put_raw_sum(a, node, base + lane, sum);
+        }
+        __syncwarp();
     }
-    __syncwarp();
 }
 
 // P2M for one leaf, any order <= 127 (per-order warp reductions).
-__device__ void p2m_leaf_generic(const MomArgs &a, int64_t node, double *row_smem)
+__device__ void p2m_leaf_generic(const MomArgs &a, int64_t node, int64_t s, int64_t e, double c,
+                                 double *row_smem)
 {
     const int lane = dt_lane();
     const int o1 = (int)a.order + 1;
-    const int64_t s = a.start[node], e = a.end[node];
-    const double c = a.center[node];
     for (int k = lane; k < o1; k += 32)
         row_smem[k] = 0.0;
     __syncwarp();
@@ -187,21 +237,21 @@ __device__ void p2m_leaf_generic(const MomArgs &a, int64_t node, double *row_sme
 }
 
 // M2M for one internal node (one warp): sum of shifted child rows.
-__device__ void m2m_node(const MomArgs &a, int64_t node, double *pw, double *mrow)
+__device__ void m2m_node(const MomArgs &a, int64_t node, int64_t left, int64_t right, double c,
+                         double *pw, double *mrow)
 {
     const int lane = dt_lane();
     const int o1 = (int)a.order + 1;
-    const double c = a.center[node];
     double out[MAX_ORDER1 / 32];
 #pragma unroll
     for (int i = 0; i < MAX_ORDER1 / 32; ++i)
         out[i] = 0.0;
-    const int64_t kids[2] = {__ldcg(a.left + node), __ldcg(a.right + node)};
+    const int64_t kids[2] = {left, right};
     for (int ci = 0; ci < 2; ++ci) {
         const int64_t ch = kids[ci];
         if (ch < 0)
             continue;
-        const double delta = a.center[ch] - c;
+        const double delta = __ldg(a.center + ch) - c;
         // pw[i] = delta^i / i!  (multiplicative scan across lanes, chunks of 32)
         double carry = 1.0;
         for (int b = 0; b < o1; b += 32) {
@@ -241,66 +291,113 @@ __device__ void m2m_node(const MomArgs &a, int64_t node, double *pw, double *mro
     }
 }
 
+__global__ void moments_prep_kernel(MomArgs a)
+{
+    const int64_t n = __ldg(a.meta + DT_META_NODES);
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        a.arrived[i] = 0;
+        const int64_t l = __ldg(a.left + i), r = __ldg(a.right + i);
+        if (l >= 0)
+            a.parent[l] = (int32_t)i;
+        if (r >= 0)
+            a.parent[r] = (int32_t)i;
+        if (i == 0)
+            a.parent[0] = -1;
+    }
+}
+
 __global__ void __launch_bounds__(MOM_THREADS) moments_kernel(MomArgs a)
 {
-    cg::grid_group grid = cg::this_grid();
-    __shared__ double tr[MOM_WARPS][32][33];
+    __shared__ double tr[MOM_WARPS][16][33];
     __shared__ double pw_s[MOM_WARPS][MAX_ORDER1];
     __shared__ double row_s[MOM_WARPS][MAX_ORDER1];
-    const volatile int64_t *meta = a.meta;
-    const int warp = threadIdx.x >> 5;
+    const int warp = threadIdx.x >> 5, lane = dt_lane();
     const int64_t gwarp = (int64_t)blockIdx.x * MOM_WARPS + warp;
     const int64_t nwarps = (int64_t)gridDim.x * MOM_WARPS;
-    const int64_t n_nodes = meta[DT_META_NODES];
-    const int64_t depth = meta[DT_META_DEPTH];
+    const int64_t n_nodes = __ldg(a.meta + DT_META_NODES);
     const bool reg_path = a.order + 1 <= REG_ORDER;
 
-    // P2M: every leaf, any level
-    for (int64_t node = gwarp; node < n_nodes; node += nwarps) {
-        if (__ldg(a.left + node) >= 0 || __ldg(a.right + node) >= 0)
-            continue;
-        if (reg_path)
-            p2m_leaf_reg(a, node, tr[warp]);
-        else
-            p2m_leaf_generic(a, node, row_s[warp]);
-    }
-    grid.sync();
-    // M2M bottom-up
-    for (int64_t lev = depth - 1; lev >= 0; --lev) {
-        const int64_t f0 = meta[DT_META_LEVEL0 + lev];
-        const int64_t f1 = meta[DT_META_LEVEL0 + lev + 1];
-        for (int64_t node = f0 + gwarp; node < f1; node += nwarps) {
-            if (__ldg(a.left + node) < 0 && __ldg(a.right + node) < 0)
-                continue;
-            m2m_node(a, node, pw_s[warp], row_s[warp]);
+    // each warp scans 32 consecutive nodes at a time for leaves
+    for (int64_t c0 = gwarp * 32; c0 < n_nodes; c0 += nwarps * 32) {
+        const int64_t mine = c0 + lane;
+        bool leaf = false;
+        int64_t s = 0, e = 0;
+        double ctr = 0.0;
+        if (mine < n_nodes) {
+            leaf = __ldg(a.left + mine) < 0 && __ldg(a.right + mine) < 0;
+            s = __ldg(a.start + mine);
+            e = __ldg(a.end + mine);
+            ctr = __ldg(a.center + mine);
         }
-        grid.sync();
+        unsigned leaves = __ballot_sync(DT_FULL, leaf);
+        while (leaves) {
+            const int i = __ffs(leaves) - 1;
+            leaves &= leaves - 1;
+            int64_t node = c0 + i;
+            const int64_t ns = __shfl_sync(DT_FULL, s, i);
+            const int64_t ne = __shfl_sync(DT_FULL, e, i);
+            const double nc = __shfl_sync(DT_FULL, ctr, i);
+            if (reg_path)
+                p2m_leaf_reg(a, node, ns, ne, nc, tr[warp]);
+            else
+                p2m_leaf_generic(a, node, ns, ne, nc, row_s[warp]);
+            // climb while this warp completes the parent's last child
+            while (true) {
+                __threadfence();
+                __syncwarp();
+                int64_t par = -1;
+                if (lane == 0) {
+                    const int32_t pp = __ldcg(a.parent + node);
+                    if (pp >= 0) {
+                        const int64_t pl = __ldg(a.left + pp), pr = __ldg(a.right + pp);
+                        const int need = (pl >= 0) + (pr >= 0);
+                        const int got = atomicAdd(a.arrived + pp, 1) + 1;
+                        if (got == need)
+                            par = pp;
+                    }
+                }
+                par = __shfl_sync(DT_FULL, par, 0);
+                if (par < 0)
+                    break;
+                __threadfence();
+                m2m_node(a, par, __ldg(a.left + par), __ldg(a.right + par),
+                         __ldg(a.center + par), pw_s[warp], row_s[warp]);
+                node = par;
+            }
+        }
     }
 }
 
 }  // namespace
 
+extern "C" size_t dt_moments_workspace(int64_t node_capacity)
+{
+    return (size_t)node_capacity * 2 * sizeof(int32_t) + 256;
+}
+
 extern "C" int dt_moments(const double *xs, const double *qs, const double *center,
                           const int64_t *start, const int64_t *end, const int64_t *left,
                           const int64_t *right, const int64_t *meta, int64_t order,
                           double *moments, double *moments_eval, int64_t eval_stride,
+                          int64_t node_capacity, void *workspace, size_t workspace_bytes,
                           void *stream)
 {
     DT_CHECK_ARG(!moments_eval || (eval_stride >= order + 1 && eval_stride % 2 == 0),
                  "eval_stride must be even and >= order + 1");
     DT_CHECK_ARG(order >= 0 && order < MAX_ORDER1, "moment order must be in [0, 127]");
+    DT_CHECK_ARG(node_capacity >= 1 && node_capacity < (int64_t)1 << 31, "bad node capacity");
     DT_CHECK_ARG(xs && qs && center && start && end && left && right && meta && moments,
                  "null pointer");
+    if (!workspace || workspace_bytes < dt_moments_workspace(node_capacity))
+        return dt_set_error(DT_ERR_WORKSPACE, "moments workspace too small");
     MomArgs a{xs, qs, center, start, end, left, right, meta, order, moments, moments_eval,
-              eval_stride};
-    int per_sm = 0;
-    DT_CUDA_TRY(
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, moments_kernel, MOM_THREADS, 0));
-    if (per_sm < 1)
-        return dt_set_error(DT_ERR_CUDA, "moments kernel cannot be resident");
-    int grid = dt_num_sms() * (per_sm > 4 ? 4 : per_sm);
-    void *args[] = {&a};
-    DT_CUDA_TRY(cudaLaunchCooperativeKernel((const void *)moments_kernel, grid, MOM_THREADS, args,
-                                            0, (cudaStream_t)stream));
+              eval_stride, (int32_t *)workspace, (int32_t *)workspace + node_capacity};
+    cudaStream_t s = (cudaStream_t)stream;
+    const int sms = dt_num_sms();
+    moments_prep_kernel<<<sms * 8, 256, 0, s>>>(a);
+    DT_CUDA_TRY(cudaGetLastError());
+    moments_kernel<<<sms * 8, MOM_THREADS, 0, s>>>(a);
+    DT_CUDA_TRY(cudaGetLastError());
     return DT_OK;
 }

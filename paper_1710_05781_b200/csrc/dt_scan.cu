@@ -46,17 +46,17 @@ __device__ double block_inclusive_scan(double v, double *warp_tot)
     return v;
 }
 
-// Pass 1: per-tile sums (each thread sums SCAN_ITEMS consecutive values).
+// Pass 1: per-tile sums, coalesced (thread t sums elements t, t+256, ...).
 __global__ void __launch_bounds__(SCAN_THREADS) tile_sums_kernel(const double *__restrict__ q,
                                                                  int64_t n,
                                                                  double *__restrict__ tile_sum)
 {
     __shared__ double wt[SCAN_THREADS / 32];
-    const int64_t base = (int64_t)blockIdx.x * SCAN_TILE + (int64_t)threadIdx.x * SCAN_ITEMS;
+    const int64_t base = (int64_t)blockIdx.x * SCAN_TILE + threadIdx.x;
     double s = 0.0;
 #pragma unroll
     for (int i = 0; i < SCAN_ITEMS; ++i) {
-        int64_t j = base + i;
+        const int64_t j = base + (int64_t)i * SCAN_THREADS;
         if (j < n)
             s += __ldg(q + j);
     }
@@ -98,51 +98,136 @@ __global__ void __launch_bounds__(PARTIAL_THREADS) tile_scan_kernel(double *__re
     }
 }
 
-// Pass 3: scan each tile with its exclusive offset.
+// Pass 3: scan each tile with its exclusive offset.  Warp w owns 512
+// consecutive elements, read/written coalesced in 16 rows of 32; each row is
+// a warp shuffle scan carried across rows, then warps are offset in order.
 __global__ void __launch_bounds__(SCAN_THREADS) tile_apply_kernel(const double *__restrict__ q,
                                                                   int64_t n,
                                                                   const double *__restrict__ tile_off,
                                                                   double *__restrict__ prefix)
 {
     __shared__ double wt[SCAN_THREADS / 32];
-    const int64_t base = (int64_t)blockIdx.x * SCAN_TILE + (int64_t)threadIdx.x * SCAN_ITEMS;
+    const int lane = dt_lane(), warp = threadIdx.x >> 5;
+    const int64_t base = (int64_t)blockIdx.x * SCAN_TILE + (int64_t)warp * (32 * SCAN_ITEMS) + lane;
     double v[SCAN_ITEMS];
-    double s = 0.0;
 #pragma unroll
     for (int i = 0; i < SCAN_ITEMS; ++i) {
-        int64_t j = base + i;
+        const int64_t j = base + 32 * i;
         v[i] = j < n ? __ldg(q + j) : 0.0;
-        s += v[i];
     }
-    double incl = block_inclusive_scan(s, wt);
-    double run = tile_off[blockIdx.x] + (incl - s);
+    double carry = 0.0;
 #pragma unroll
     for (int i = 0; i < SCAN_ITEMS; ++i) {
-        run += v[i];
-        int64_t j = base + i;
+        double x = v[i];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const double t = __shfl_up_sync(DT_FULL, x, o);
+            if (lane >= o)
+                x += t;
+        }
+        x += carry;
+        carry = __shfl_sync(DT_FULL, x, 31);
+        v[i] = x;
+    }
+    if (lane == 31)
+        wt[warp] = carry;
+    __syncthreads();
+    double off = tile_off[blockIdx.x];
+    for (int w = 0; w < warp; ++w)
+        off += wt[w];
+#pragma unroll
+    for (int i = 0; i < SCAN_ITEMS; ++i) {
+        const int64_t j = base + 32 * i;
         if (j < n)
-            prefix[j] = run;
+            prefix[j] = off + v[i];
     }
 }
 
-// e(y) for arbitrary targets; total = prefix[n-1].
-__global__ void sign_terms_kernel(const double *__restrict__ xs,
-                                  const double *__restrict__ prefix, int64_t n,
-                                  const double *__restrict__ ys, double *__restrict__ e,
-                                  int64_t t)
+// e(y) for arbitrary targets; total = prefix[n-1].  A block owns 2048
+// consecutive targets.  When they ascend (the usual case: evaluate_all sorts
+// them) two threads bracket the block's source range with global searches,
+// the range is staged in shared memory and every target is located there;
+// otherwise each target is searched in global memory.
+constexpr int SIGN_THREADS = 256;
+constexpr int SIGN_PER_THREAD = 8;
+constexpr int SIGN_TILE = SIGN_THREADS * SIGN_PER_THREAD;
+constexpr int SIGN_SMEM = 4096;
+
+// bracket[b] = lower_bound(xs, ys[b * SIGN_TILE]) for every tile boundary
+// (and the last target), all searched in parallel.
+__global__ void sign_bracket_kernel(const double *__restrict__ xs, int64_t n,
+                                    const double *__restrict__ ys, int64_t t,
+                                    int64_t *__restrict__ bracket, int64_t nb)
 {
-    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= t)
+    const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (b > nb)
         return;
+    const int64_t i = b < nb ? b * SIGN_TILE : t - 1;
+    bracket[b] = dt_lower_bound(xs, 0, n, __ldg(ys + i));
+}
+
+__global__ void __launch_bounds__(SIGN_THREADS) sign_terms_kernel(
+    const double *__restrict__ xs, const double *__restrict__ prefix, int64_t n,
+    const double *__restrict__ ys, double *__restrict__ e, int64_t t,
+    const int64_t *__restrict__ bracket, int64_t nb)
+{
+    __shared__ double xsm[SIGN_SMEM];
+    const int64_t t0 = (int64_t)blockIdx.x * SIGN_TILE;
+    const int64_t t1 = min(t, t0 + SIGN_TILE);
+    double y[SIGN_PER_THREAD];
+    bool ok = true;
+#pragma unroll
+    for (int k = 0; k < SIGN_PER_THREAD; ++k) {
+        const int64_t i = t0 + (int64_t)k * SIGN_THREADS + threadIdx.x;
+        y[k] = i < t1 ? __ldg(ys + i) : 0.0;
+        if (i + 1 < t1 && !(y[k] <= __ldg(ys + i + 1)))
+            ok = false;
+    }
+    const bool sorted = __syncthreads_and(ok);
     if (n == 0) {
-        e[i] = 0.0;
+#pragma unroll
+        for (int k = 0; k < SIGN_PER_THREAD; ++k) {
+            const int64_t i = t0 + (int64_t)k * SIGN_THREADS + threadIdx.x;
+            if (i < t1)
+                e[i] = 0.0;
+        }
         return;
     }
-    double y = __ldg(ys + i);
-    int64_t idx = dt_lower_bound(xs, 0, n, y);
-    double total = __ldg(prefix + n - 1);
-    double below = idx == 0 ? 0.0 : __ldg(prefix + idx - 1);
-    e[i] = __dsub_rn(__dmul_rn(2.0, below), total);
+    int64_t lo = 0, hi = n;
+    if (sorted && bracket) {
+        // the next tile's first target bounds this tile's last one from above
+        lo = __ldg(bracket + blockIdx.x);
+        hi = min(n, __ldg(bracket + blockIdx.x + 1) + 1);
+    }
+    const bool staged = sorted && bracket && hi - lo <= SIGN_SMEM;
+    if (staged) {
+        for (int64_t j = lo + threadIdx.x; j < hi; j += SIGN_THREADS)
+            xsm[j - lo] = __ldg(xs + j);
+        __syncthreads();
+    }
+    const double total = __ldg(prefix + n - 1);
+#pragma unroll
+    for (int k = 0; k < SIGN_PER_THREAD; ++k) {
+        const int64_t i = t0 + (int64_t)k * SIGN_THREADS + threadIdx.x;
+        if (i >= t1)
+            continue;
+        int64_t idx;
+        if (staged) {
+            int a = 0, b = (int)(hi - lo);
+            while (a < b) {
+                const int m = (a + b) >> 1;
+                if (xsm[m] < y[k])
+                    a = m + 1;
+                else
+                    b = m;
+            }
+            idx = lo + a;
+        } else {
+            idx = dt_lower_bound(xs, lo, hi, y[k]);
+        }
+        const double below = idx == 0 ? 0.0 : __ldg(prefix + idx - 1);
+        e[i] = __dsub_rn(__dmul_rn(2.0, below), total);
+    }
 }
 
 }  // namespace
@@ -172,16 +257,29 @@ extern "C" int dt_prefix_scan(const double *qs, double *prefix, int64_t n, void 
     return DT_OK;
 }
 
+extern "C" size_t dt_sign_terms_workspace(int64_t n_targets)
+{
+    return (size_t)((n_targets + SIGN_TILE - 1) / SIGN_TILE + 2) * sizeof(int64_t);
+}
+
 extern "C" int dt_sign_terms(const double *xs, const double *prefix, int64_t n, const double *ys,
-                             double *e_out, int64_t n_targets, void *stream)
+                             double *e_out, int64_t n_targets, void *workspace,
+                             size_t workspace_bytes, void *stream)
 {
     DT_CHECK_ARG(n >= 0 && n_targets >= 0, "negative size");
     if (n_targets == 0)
         return DT_OK;
     DT_CHECK_ARG(ys && e_out && (n == 0 || (xs && prefix)), "null pointer");
-    const int th = 256;
-    sign_terms_kernel<<<(unsigned)((n_targets + th - 1) / th), th, 0, (cudaStream_t)stream>>>(
-        xs, prefix, n, ys, e_out, n_targets);
+    cudaStream_t s = (cudaStream_t)stream;
+    const int64_t nb = (n_targets + SIGN_TILE - 1) / SIGN_TILE;
+    int64_t *bracket = nullptr;
+    if (workspace && workspace_bytes >= dt_sign_terms_workspace(n_targets) && n > 0) {
+        bracket = (int64_t *)workspace;
+        sign_bracket_kernel<<<(unsigned)((nb + 1 + 127) / 128), 128, 0, s>>>(xs, n, ys, n_targets,
+                                                                         bracket, nb);
+    }
+    sign_terms_kernel<<<(unsigned)nb, SIGN_THREADS, 0, s>>>(xs, prefix, n, ys, e_out, n_targets,
+                                                            bracket, nb);
     DT_CUDA_TRY(cudaGetLastError());
     return DT_OK;
 }

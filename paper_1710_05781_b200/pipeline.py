@@ -32,7 +32,7 @@ from .tree import (
 )
 
 # kernels launched per step (memset of the work counter not counted)
-LAUNCHES_PER_STEP = 3 + 1 + 1 + 1 + 1 + 1  # scan(3) sign build moments pack eval
+LAUNCHES_PER_STEP = 3 + 2 + 1 + 2 + 1 + 1  # scan(3) sign(2) build moments(2) pack eval
 
 
 class TreePipeline:
@@ -53,6 +53,8 @@ class TreePipeline:
         self.scan_ws = torch.empty(self.scan_ws_bytes, dtype=torch.uint8, device=self.dev)
         self.xq = torch.empty(2 * self.n, dtype=torch.float64, device=self.dev)
         self.eval_ws = torch.empty(256, dtype=torch.uint8, device=self.dev)
+        self.sign_ws_bytes = int(L.dt_sign_terms_workspace(self.T))
+        self.sign_ws = torch.empty(self.sign_ws_bytes, dtype=torch.uint8, device=self.dev)
         self.cos_t, self.sin_t = contour_tables(self.dev)
 
     @classmethod
@@ -89,7 +91,8 @@ class TreePipeline:
         ys_part = ys[i0:i1]
         out_part = out[i0:i1]
         _lib.check(L.dt_sign_terms(p(xs), p(self.prefix), self.n, p(ys_part), p(out_part),
-                                   i1 - i0, s), "dt_sign_terms")
+                                   i1 - i0, p(self.sign_ws), self.sign_ws_bytes, s),
+                   "dt_sign_terms")
         self.bufs.launch(xs, cfg.leaf_capacity)
         launch_moments(self.bufs, xs, qs, self.order, self.moments, self.meval)
         pack_sources(xs, qs, self.xq)

@@ -170,6 +170,8 @@ class TreeBuffers:
         L = _lib.load()
         self.ws_bytes = int(L.dt_build_workspace(n, capacity))
         self.ws = torch.empty(self.ws_bytes, dtype=torch.uint8, device=device)
+        self.mws_bytes = int(L.dt_moments_workspace(capacity))
+        self.mws = torch.empty(self.mws_bytes, dtype=torch.uint8, device=device)
 
     def launch(self, xs: torch.Tensor, leaf_capacity: int, max_depth: int = MAX_DEPTH) -> None:
         L = _lib.load()
@@ -197,7 +199,8 @@ def launch_moments(bufs: TreeBuffers, xs, qs, order: int, moments: torch.Tensor,
     _lib.check(
         L.dt_moments(p(xs), p(qs), p(bufs.center), p(bufs.start), p(bufs.end), p(bufs.left),
                      p(bufs.right), p(bufs.meta), int(order), p(moments), p(meval),
-                     eval_stride(order), _lib.stream_handle()),
+                     eval_stride(order), bufs.capacity, p(bufs.mws), bufs.mws_bytes,
+                     _lib.stream_handle()),
         "dt_moments",
     )
 
