@@ -324,3 +324,22 @@ def test_seam_mirror_entry(dt):
     scale = np.abs(g["qs"]).sum()
     assert float((got - want).abs().max()) <= 1e-14 * scale
     assert np.max(np.abs(got.cpu().numpy() - g["phi_tree"])) <= 1e-13 * scale
+
+
+def test_sharded_evaluation_is_partition_invariant(dt):
+    """Contiguous target slices per rank (parallel.shard_bounds) give a
+    bit-identical field for any world size (the GPU analogue of the
+    reference's thread-count invariance, test_tree.py:269-278)."""
+    from paper_1710_05781_b200.parallel import gpu_slice_evaluator, shard_bounds
+
+    g = load_case("cfg2s")
+    system = _system(dt, g)
+    kernel = dt.DiscKernel(float(g["r_d"]))
+    cfg = _config(dt, g)
+    tree = dt.build(system, kernel, cfg)
+    ys = torch.from_numpy(g["targets"]).cuda()
+    base = dt.evaluate_all(tree, kernel, cfg, system, ys).values
+    run = gpu_slice_evaluator(tree, kernel, cfg, system, ys)
+    for world in (2, 3, 8):
+        parts = [run(*shard_bounds(ys.numel(), world, r)) for r in range(world)]
+        assert torch.equal(torch.cat(parts), base)
