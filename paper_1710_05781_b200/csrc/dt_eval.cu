@@ -9,8 +9,8 @@
 // else descends.
 //
 // B200 mapping: one warp owns 32 consecutive (sorted) targets and walks the
-// UNION of their traversals with a per-entry lane mask (stack in shared
-// memory).  Each lane applies the reference's MAC to its own target, so the
+// UNION of their traversals with a per-entry lane mask (the warp-uniform
+// stack lives in the lanes' registers).  Each lane applies the reference's MAC to its own target, so the
 // per-target interaction lists -- and their DFS order -- are exactly the
 // reference's.  Warps pull 32-target chunks from a global counter
 // (persistent grid, 148 x k CTAs).
@@ -38,9 +38,11 @@ namespace {
 #ifndef DT_EVAL_MINB
 #define DT_EVAL_MINB 4
 #endif
-constexpr int EVAL_THREADS = 256;
+#ifndef DT_EVAL_THREADS
+#define DT_EVAL_THREADS 256
+#endif
+constexpr int EVAL_THREADS = DT_EVAL_THREADS;
 constexpr int EVAL_WARPS = EVAL_THREADS / 32;
-constexpr int STACK_DEPTH = 64;         // >= max_depth + 2
 constexpr int MAX_SAMPLES = 256;
 constexpr float PSEL_MARGIN = 1e-4f;    // in units of the order axis
 constexpr double CONTOUR_SAFETY = 1.1;  // kernel.py:27
@@ -227,6 +229,9 @@ __device__ __forceinline__ void split_log2(float x, int *e, float *f)
 // Error budget of the order estimate (in units of p): MUFU logs 2^-22 each
 // (x up to 31 for the ratio term), approximate fp32 divisions/roots (a few
 // ulp of the factors of X) -> below 2e-5; PSEL_MARGIN is 5x that.
+// s* = r_d^2/R^2 >= 4 puts every sample below the peak of |f| (maximum at
+// t = 32, the far side of the contour) and s* <= s_1 puts every sample above
+// it (maximum at t = 1); only in between is the bracket located (asin).
 __device__ int psel_fast(double big_r, double h, const EvalArgs &a, const float *isig,
                          float rd2f, float inv_tol_f)
 {
@@ -236,35 +241,47 @@ __device__ int psel_fast(double big_r, double h, const EvalArgs &a, const float 
     const float hf = (float)h;
     if (!(Rf > 1e-15f && Rf < 1e15f && hf > 1e-30f))
         return -1;
-    const float ratio = __fdividef(hf, Rf);
-    const float sstar = __fdividef(rd2f, Rf * Rf);
+    const float iR = __frcp_rn(Rf);
+    const float ratio = hf * iR;
+    const float sstar = rd2f * iR * iR;
     if (!(sstar > 1e-12f) || !(sstar < 1e30f) || !(ratio > 1e-30f))
         return -1;
-    // bracket: s_t = 4 sin^2(pi t / 64) = s*  ->  t* = (64/pi) asin(sqrt(s*)/2);
-    // asin via Abramowitz-Stegun 4.4.45 (|err| < 7e-5 rad), enough to place
-    // s* within the 4 candidate samples t0-1 .. t0+2.
-    const float z = fminf(1.0f, 0.5f * sstar * rsqrtf(sstar));
-    const float om = 1.0f - z;
-    const float poly = fmaf(fmaf(fmaf(-0.0187293f, z, 0.0742610f), z, -0.2121144f), z,
-                            1.5707288f);
-    const float asz = 1.57079633f - om * rsqrtf(fmaxf(om, 1e-30f)) * poly;
-    const int t0 = (int)floorf(asz * 20.371832715762604f);
-    // the sampled maximum is at t0 or t0 + 1 (a t* error of ~1e-3 samples
-    // can only swap in the sample sitting on the peak, which then wins)
-    const int ta = min(max(t0, 1), 32), tb = min(t0 + 1, 32);
-    const float ua = sstar * isig[ta], ub = sstar * isig[tb];
-    const float emin = fminf((1.0f - ua) * (1.0f - ua), (1.0f - ub) * (1.0f - ub));
-    const float Q = emin + sstar;         // M^-4
-    const float rq = rsqrtf(Q);
-    const float M = rq * rsqrtf(rq);      // Q^(-1/4): sampled contour maximum of |f|
-    const float X = 1.1f * M * __fdividef(ratio, 1.0f - ratio) * inv_tol_f;  // value_0 / tol
+    int t0;
+    float emin;
+    if (sstar >= 4.0f) {
+        t0 = 32;
+        const float u = sstar * 0.25f;
+        emin = (1.0f - u) * (1.0f - u);
+    } else if (sstar <= isig[34]) {
+        t0 = 0;
+        const float u = sstar * isig[1];
+        emin = (1.0f - u) * (1.0f - u);
+    } else {
+        // bracket: s_t = 4 sin^2(pi t / 64) = s*  ->  t* = (64/pi) asin(sqrt(s*)/2);
+        // asin via Abramowitz-Stegun 4.4.45 (|err| < 7e-5 rad).  The sampled
+        // maximum is at t0 or t0 + 1 (a t* error of ~1e-3 samples can only
+        // swap in the sample sitting on the peak, which then wins).
+        const float z = 0.5f * sstar * rsqrtf(sstar);
+        const float om = 1.0f - z;
+        const float poly = fmaf(fmaf(fmaf(-0.0187293f, z, 0.0742610f), z, -0.2121144f), z,
+                                1.5707288f);
+        const float asz = 1.57079633f - om * rsqrtf(fmaxf(om, 1e-30f)) * poly;
+        t0 = (int)(asz * 20.371832715762604f);
+        const int ta = max(t0, 1), tb = min(t0 + 1, 32);
+        const float ua = sstar * isig[ta], ub = sstar * isig[tb];
+        emin = fminf((1.0f - ua) * (1.0f - ua), (1.0f - ub) * (1.0f - ub));
+    }
+    const float rq = rsqrtf(emin + sstar);     // (M^-4)^(-1/2)
+    const float M = rq * rsqrtf(rq);           // sampled contour maximum of |f|
+    // value_0 / tol = 1.1 M (h/R) / (1 - h/R) / tol
+    const float X = 1.1f * M * hf * inv_tol_f * __frcp_rn(Rf - hf);
     if (!(X > 1e-37f && X < 1e37f))
         return -1;
     int ex, er;
     float fx, fr;
     split_log2(X, &ex, &fx);
     split_log2(ratio, &er, &fr);
-    const float L = -((float)er + fr);    // -log2(ratio) > 0
+    const float L = -((float)er + fr);         // -log2(ratio) > 0
     const float iL = __frcp_rn(L);
     const float pstar_approx = ((float)ex + fx) * iL;
     if (pstar_approx < -1.0f)
@@ -274,7 +291,7 @@ __device__ int psel_fast(double big_r, double h, const EvalArgs &a, const float 
     const int n = __float2int_rn(pstar_approx);
     // residual N - n L with the integer parts kept exact
     const float resid = (float)(ex + n * er) + fmaf((float)n, fr, fx);
-    const float dist = resid * iL;        // pstar - n
+    const float dist = resid * iL;             // pstar - n
     if (fabsf(dist) < PSEL_MARGIN && n >= 0 && n <= a.p_cap - 1)
         return -(t0 + 2);
     const int p = max(dist > 0.0f ? n + 1 : n, 0);
@@ -356,7 +373,11 @@ __device__ __forceinline__ double far_field(double d, double rd2, const double2 
     const double g3 = __fma_rn(-ir3, g1, __fma_rn(a0, 0.5, -ci) * g2);
     if (pu >= 3)
         acc = __fma_rn(g3, m23.y, acc);
+    // The g_{k-2}, g_{k-3} part of each step is formed off the critical
+    // path: the recurrence carries one dependent DFMA per order; a second
+    // accumulator halves the accumulation chain.
     double gm3 = g1, gm2 = g2, gm1 = g3;
+    double acc1 = 0.0;
     int k = 4;
     if (!WIDE) {
         // orders every far lane of the warp needs (k <= pmin): no masking
@@ -365,14 +386,12 @@ __device__ __forceinline__ double far_field(double d, double rd2, const double2 
             if (kk + 1 > pmin)
                 break;
             const double2 mm = __ldg(M2 + kk / 2);
-            double t = __fma_rn(a0, 1.0 / (kk - 1), -ci) * gm1;
-            t = __fma_rn(-ir3, gm2, t);
-            t = __fma_rn(-inv, gm3, t);
+            const double pa = __fma_rn(-ir3, gm2, -inv * gm3);
+            const double t = __fma_rn(__fma_rn(a0, c_rcp[kk - 1], -ci), gm1, pa);
             acc = __fma_rn(t, mm.x, acc);
-            double u = __fma_rn(a0, 1.0 / kk, -ci) * t;
-            u = __fma_rn(-ir3, gm1, u);
-            u = __fma_rn(-inv, gm2, u);
-            acc = __fma_rn(u, mm.y, acc);
+            const double pb = __fma_rn(-ir3, gm1, -inv * gm2);
+            const double u = __fma_rn(__fma_rn(a0, c_rcp[kk], -ci), t, pb);
+            acc1 = __fma_rn(u, mm.y, acc1);
             gm3 = gm1;
             gm2 = t;
             gm1 = u;
@@ -383,38 +402,42 @@ __device__ __forceinline__ double far_field(double d, double rd2, const double2 
     const double *M = reinterpret_cast<const double *>(M2);
 #pragma unroll 1
     for (; k <= pmax; ++k) {
-        double t = __fma_rn(a0, c_rcp[k - 1], -ci) * gm1;
-        t = __fma_rn(-ir3, gm2, t);
-        t = __fma_rn(-inv, gm3, t);
+        const double pa = __fma_rn(-ir3, gm2, -inv * gm3);
+        const double t = __fma_rn(__fma_rn(a0, c_rcp[k - 1], -ci), gm1, pa);
         if (k <= pu)
             acc = __fma_rn(t, __ldg(M + k), acc);
         gm3 = gm2;
         gm2 = gm1;
         gm1 = t;
     }
-    return acc;
+    return acc + acc1;
 }
 
+__device__ __forceinline__ double near_term(double2 u, double y, double rd2)
+{
+    const double du = u.x - y;
+    return u.y * du * dt_rsqrt(__fma_rn(du, du, rd2));
+}
+
+// Leaf sources [s, e): four (x, q) broadcast loads in flight per step.
 __device__ __forceinline__ double near_field(const double2 *__restrict__ xq, int s, int e,
                                              double y, double rd2)
 {
-    double a0 = 0.0, a1 = 0.0;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
     int j = s;
-    for (; j + 1 < e; j += 2) {
-        const double2 u = __ldg(xq + j);
-        const double2 v = __ldg(xq + j + 1);
-        const double du = u.x - y, dv = v.x - y;
-        const double ru = dt_rsqrt(__fma_rn(du, du, rd2));
-        const double rv = dt_rsqrt(__fma_rn(dv, dv, rd2));
-        a0 = __fma_rn(u.y * du, ru, a0);
-        a1 = __fma_rn(v.y * dv, rv, a1);
+    for (; j + 3 < e; j += 4) {
+        const double2 u0 = __ldg(xq + j);
+        const double2 u1 = __ldg(xq + j + 1);
+        const double2 u2 = __ldg(xq + j + 2);
+        const double2 u3 = __ldg(xq + j + 3);
+        a0 += near_term(u0, y, rd2);
+        a1 += near_term(u1, y, rd2);
+        a2 += near_term(u2, y, rd2);
+        a3 += near_term(u3, y, rd2);
     }
-    if (j < e) {
-        const double2 u = __ldg(xq + j);
-        const double du = u.x - y;
-        a0 = __fma_rn(u.y * du, dt_rsqrt(__fma_rn(du, du, rd2)), a0);
-    }
-    return a0 + a1;
+    for (; j < e; ++j)
+        a0 += near_term(__ldg(xq + j), y, rd2);
+    return (a0 + a1) + (a2 + a3);
 }
 
 #define FNV_OFF 1469598103934665603ULL
@@ -425,10 +448,9 @@ __global__ void __launch_bounds__(EVAL_THREADS, DT_EVAL_MINB) tree_eval_kernel(E
 {
     if (ADAPTIVE)
         a.tol_share = tol_share_of(a);
-    __shared__ int2 stack_s[EVAL_WARPS][STACK_DEPTH];
-    __shared__ float isig_s[33];
+    __shared__ float isig_s[35];
     __shared__ double cos_s[MAX_SAMPLES], sin_s[MAX_SAMPLES];
-    const int lane = dt_lane(), warp = threadIdx.x >> 5;
+    const int lane = dt_lane();
     const bool tables_in_smem = a.n_samples <= MAX_SAMPLES;
     if (ADAPTIVE) {
         if (tables_in_smem) {
@@ -444,6 +466,8 @@ __global__ void __launch_bounds__(EVAL_THREADS, DT_EVAL_MINB) tree_eval_kernel(E
             double s = a.n_samples == 64 ? a.sin_tab[t] : 0.0;
             double sig = (c - 1.0) * (c - 1.0) + s * s;
             isig_s[t] = sig > 0.0 ? (float)(1.0 / sig) : 3.0e38f;
+            if (t == 1)
+                isig_s[34] = (float)sig;  // s_1: below it the maximum is at t = 1
         }
         __syncthreads();
     }
@@ -452,7 +476,6 @@ __global__ void __launch_bounds__(EVAL_THREADS, DT_EVAL_MINB) tree_eval_kernel(E
     const bool fast_ok = a.n_samples == 64 && a.psel_mode == DT_PSEL_FAST;
     const float rd2f = (float)a.rd2;
     const float inv_tol_f = (float)(1.0 / a.tol_share);
-    int2 *stack = stack_s[warp];
 
     while (true) {
         unsigned long long base = 0;
@@ -469,17 +492,17 @@ __global__ void __launch_bounds__(EVAL_THREADS, DT_EVAL_MINB) tree_eval_kernel(E
         uint64_t hh = FNV_OFF;
         int64_t c_near = 0, c_far = 0, c_sump = 0, c_p0 = 0, c_exact = 0;
 
+        // warp-uniform DFS stack distributed over the lanes' registers:
+        // entry k lives in lane k % 32 (sn0/sm0 for k < 32, sn1/sm1 above)
         int top = 0;
         const unsigned vmask = __ballot_sync(DT_FULL, valid);
-        if (lane == 0)
-            stack[0] = make_int2(0, (int)vmask);
-        __syncwarp();
+        int sn0 = 0, sn1 = 0;
+        unsigned sm0 = lane == 0 ? vmask : 0u, sm1 = 0u;
         while (top >= 0) {
-            const int2 ent = stack[top];
+            const bool low = top < 32;
+            const int node = __shfl_sync(DT_FULL, low ? sn0 : sn1, top & 31);
+            const unsigned mask = __shfl_sync(DT_FULL, low ? sm0 : sm1, top & 31);
             --top;
-            __syncwarp();
-            const int node = ent.x;
-            const unsigned mask = (unsigned)ent.y;
             const double4 raw0 = *reinterpret_cast<const double4 *>(a.nodes + node);
             const double center = raw0.x, half = raw0.y;
             const int2 lr = make_int2(__double2loint(raw0.z), __double2hiint(raw0.z));
@@ -533,15 +556,18 @@ __global__ void __launch_bounds__(EVAL_THREADS, DT_EVAL_MINB) tree_eval_kernel(E
                         }
                     }
                 } else {
-                    if (lane == 0) {
-                        if (lr.y >= 0)
-                            stack[++top] = make_int2(lr.y, (int)rest);
-                        if (lr.x >= 0)
-                            stack[++top] = make_int2(lr.x, (int)rest);
-                    } else {
-                        top += (lr.y >= 0) + (lr.x >= 0);
+                    if (lr.y >= 0) {
+                        ++top;
+                        if (lane == (top & 31)) {
+                            if (top < 32) { sn0 = lr.y; sm0 = rest; } else { sn1 = lr.y; sm1 = rest; }
+                        }
                     }
-                    __syncwarp();
+                    if (lr.x >= 0) {
+                        ++top;
+                        if (lane == (top & 31)) {
+                            if (top < 32) { sn0 = lr.x; sm0 = rest; } else { sn1 = lr.x; sm1 = rest; }
+                        }
+                    }
                 }
             }
         }
@@ -617,13 +643,15 @@ __global__ void choose_p_kernel(const double *__restrict__ R, const double *__re
                                 int64_t n, EvalArgs a, int64_t *__restrict__ p_out,
                                 int32_t *__restrict__ tier_out)
 {
-    __shared__ float isig_s[33];
+    __shared__ float isig_s[35];
     if (threadIdx.x <= 32) {
         int t = threadIdx.x;
         double c = a.n_samples == 64 ? a.cos_tab[t] : 1.0;
         double s = a.n_samples == 64 ? a.sin_tab[t] : 0.0;
         double sig = (c - 1.0) * (c - 1.0) + s * s;
         isig_s[t] = sig > 0.0 ? (float)(1.0 / sig) : 3.0e38f;
+        if (t == 1)
+            isig_s[34] = (float)sig;  // s_1: below it the maximum is at t = 1
     }
     __syncthreads();
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
