@@ -126,7 +126,7 @@ int dt_moments(const double *xs, const double *qs, const double *center, const i
 /* ---------------------------------------------------------------- (d)+(e) */
 
 typedef struct dt_eval_stats {
-    uint64_t *hash;      /* FNV-1a over interaction events in DFS order         */
+    uint64_t *hash;      /* sum of splitmix64(event code) over interaction events */
     int64_t *near_pairs; /* near-field (source, target) pairs                    */
     int64_t *n_far;      /* accepted far nodes                                   */
     int64_t *sum_p;      /* sum of truncation orders over accepted far nodes     */
@@ -141,7 +141,13 @@ int dt_pack_tree(const double *centers, const double *halves, const int64_t *sta
                  const int64_t *ends, const int64_t *lefts, const int64_t *rights,
                  int64_t n_nodes, void *packed, void *stream);
 
+/* Workspace of dt_tree_phi_sum (packed copies + counter).  Any entry's
+ * workspace may be enlarged by dt_tree_eval_items_workspace(i1 - i0) bytes
+ * (appended) to enable the two-phase path: a walk kernel that sums the near
+ * field and lists far interactions, then a far kernel that evaluates two list
+ * items at a time; without it a single fused traversal kernel runs. */
 size_t dt_tree_eval_workspace(int64_t n_nodes, int64_t n_src, int64_t moment_stride);
+size_t dt_tree_eval_items_workspace(int64_t n_targets);
 
 /* Mirror of the numba seam _kernels.tree_phi_sum (_kernels.py:163-266):
  * far-field/near-field traversal for targets ys[i0:i1]; writes out[i0:i1]

@@ -343,19 +343,23 @@ void or_phi_derivatives(double d, double rd2, int64_t p, double *deriv)
     }
 }
 
-#define OR_FNV_OFF 1469598103934665603ULL
-#define OR_FNV_MUL 1099511628211ULL
-
-static inline uint64_t fnv_step(uint64_t h, uint64_t v)
+/* Interaction-set hash: sum over events of splitmix64(code), code =
+ * node*256 + p_use (far) or node*256 + 255 (near).  Order-independent, so a
+ * GPU path that evaluates far and near interactions in separate passes can
+ * be compared event set for event set. */
+static inline uint64_t mix64(uint64_t z)
 {
-    return (h ^ v) * OR_FNV_MUL;
+    z += 0x9e3779b97f4a7c15ULL;
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    return z ^ (z >> 31);
 }
 
 /*
  * _kernels.py:163-266 (tree_phi_sum) for targets [i0, i1).  Optional
  * instrumentation (any pointer may be NULL):
- *   hash[i]      FNV-1a fold over the target's interaction events in DFS
- *                order: far node -> node*256 + p_use, near leaf -> node*256+255
+ *   hash[i]      sum of mix64(code) over the target's interaction events:
+ *                far node -> node*256 + p_use, near leaf -> node*256 + 255
  *   near[i]      number of near-field (source, target) pairs
  *   nfar[i]      number of accepted far nodes
  *   sump[i]      sum of p_use over accepted far nodes
@@ -378,7 +382,7 @@ void or_tree_phi_sum(const double *centers, const double *halves, const int64_t 
         for (int64_t i = i0; i < i1; ++i) {
             double y = ys[i];
             double acc = 0.0;
-            uint64_t hh = OR_FNV_OFF;
+            uint64_t hh = 0;
             int64_t c_near = 0, c_far = 0, c_sump = 0, c_p0 = 0;
             int top = 0;
             stack[0] = 0;
@@ -397,7 +401,7 @@ void or_tree_phi_sum(const double *centers, const double *halves, const int64_t 
                     const double *mrow = moments + node * moment_stride;
                     for (int64_t k = 0; k <= p_use; ++k)
                         acc += deriv[k] * mrow[k];
-                    hh = fnv_step(hh, (uint64_t)node * 256u + (uint64_t)p_use);
+                    hh += mix64((uint64_t)node * 256u + (uint64_t)p_use);
                     ++c_far;
                     c_sump += p_use;
                     if (p_use == 0)
@@ -407,7 +411,7 @@ void or_tree_phi_sum(const double *centers, const double *halves, const int64_t 
                         double dd = xs[j] - y;
                         acc += qs[j] * dd / sqrt(dd * dd + rd2);
                     }
-                    hh = fnv_step(hh, (uint64_t)node * 256u + 255u);
+                    hh += mix64((uint64_t)node * 256u + 255u);
                     c_near += ends[node] - starts[node];
                 } else {
                     if (rights[node] >= 0)

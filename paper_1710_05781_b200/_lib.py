@@ -67,6 +67,7 @@ SIGNATURES = {
     "dt_pack_sources": (C.c_int, [_P, _P, _I64, _P, _P]),
     "dt_pack_tree": (C.c_int, [_P, _P, _P, _P, _P, _P, _I64, _P, _P]),
     "dt_tree_eval_workspace": (_SZ, [_I64, _I64, _I64]),
+    "dt_tree_eval_items_workspace": (_SZ, [_I64]),
     "dt_tree_phi_sum": (
         C.c_int,
         [_P, _P, _P, _P, _P, _P, _P, _I64, _I64, _P, _P, _I64, _D, _D, _I64, C.c_int, _D,

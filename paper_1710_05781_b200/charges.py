@@ -31,6 +31,15 @@ def _to_device(a, dtype=torch.float64) -> torch.Tensor:
     return torch.from_numpy(arr).to(dev).to(dtype).contiguous()
 
 
+def _to_host(v: torch.Tensor) -> torch.Tensor:
+    """Device -> page-locked host copy (a pageable destination runs the DMA
+    at a few GB/s; numpy views of the pinned buffer keep it alive)."""
+    out = torch.empty(v.shape, dtype=v.dtype, pin_memory=True)
+    out.copy_(v, non_blocking=True)
+    torch.cuda.current_stream(v.device).synchronize()
+    return out
+
+
 def prefix_sum(qs: torch.Tensor) -> torch.Tensor:
     """Inclusive scan of q on the device (replaces np.cumsum, charges.py:130)."""
     n = qs.numel()
@@ -148,13 +157,13 @@ def as_targets(targets, check_finite: bool = True):
     if isinstance(targets, torch.Tensor):
         if targets.ndim != 1:
             raise ValueError(f"targets must be one-dimensional, got shape {tuple(targets.shape)}")
-        back = (lambda v: v) if targets.is_cuda else (lambda v: v.cpu())  # noqa: E731
+        back = (lambda v: v) if targets.is_cuda else _to_host  # noqa: E731
         t = _to_device(targets)
     else:
         arr = np.asarray(targets, dtype=np.float64)
         if arr.ndim != 1:
             raise ValueError(f"targets must be one-dimensional, got shape {arr.shape}")
-        back = lambda v: v.cpu().numpy()  # noqa: E731
+        back = lambda v: _to_host(v).numpy()  # noqa: E731
         t = _to_device(arr)
     if check_finite and t.numel() and not bool(torch.isfinite(t).all()):
         raise ValueError("targets must all be finite")
