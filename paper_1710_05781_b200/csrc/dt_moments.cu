@@ -15,7 +15,11 @@
 // sums at the 1e-16 level of sum|q| r^k / k!.
 // Algorithmic HBM bytes: P2M 16 N + 8 (order+1) leaves; M2M 24 (order+1)
 // per internal node (two child rows read, one row written).
+#include <cooperative_groups.h>
+
 #include "dt_common.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace {
 
@@ -369,6 +373,135 @@ __global__ void __launch_bounds__(MOM_THREADS) moments_kernel(MomArgs a)
     }
 }
 
+// ---- order + 1 <= 32: thread-per-leaf P2M + level-synchronous M2M ----
+
+// P2M with one thread per leaf: raw power sums S_k = sum q (x - c)^k in
+// registers, two sources in flight (independent multiply chains), no
+// shuffles or shared memory.
+__global__ void __launch_bounds__(128) p2m_thread_kernel(MomArgs a)
+{
+    const int64_t n = __ldg(a.meta + DT_META_NODES);
+    const int o1 = (int)a.order + 1;
+    for (int64_t node = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; node < n;
+         node += (int64_t)gridDim.x * blockDim.x) {
+        if (__ldg(a.left + node) >= 0 || __ldg(a.right + node) >= 0)
+            continue;
+        const int64_t s = __ldg(a.start + node), e = __ldg(a.end + node);
+        const double c = __ldg(a.center + node);
+        double acc[REG_ORDER];
+#pragma unroll
+        for (int k = 0; k < REG_ORDER; ++k)
+            acc[k] = 0.0;
+        int64_t j = s;
+        for (; j + 3 < e; j += 4) {
+            const double t0 = __ldg(a.xs + j) - c, t1 = __ldg(a.xs + j + 1) - c;
+            const double t2 = __ldg(a.xs + j + 2) - c, t3 = __ldg(a.xs + j + 3) - c;
+            double w0 = __ldg(a.qs + j), w1 = __ldg(a.qs + j + 1);
+            double w2 = __ldg(a.qs + j + 2), w3 = __ldg(a.qs + j + 3);
+#pragma unroll
+            for (int k = 0; k < REG_ORDER; ++k) {
+                if (k < o1) {
+                    acc[k] += (w0 + w1) + (w2 + w3);
+                    w0 *= t0;
+                    w1 *= t1;
+                    w2 *= t2;
+                    w3 *= t3;
+                }
+            }
+        }
+        for (; j + 1 < e; j += 2) {
+            const double t0 = __ldg(a.xs + j) - c, t1 = __ldg(a.xs + j + 1) - c;
+            double w0 = __ldg(a.qs + j), w1 = __ldg(a.qs + j + 1);
+#pragma unroll
+            for (int k = 0; k < REG_ORDER; ++k) {
+                if (k < o1) {
+                    acc[k] += w0 + w1;
+                    w0 *= t0;
+                    w1 *= t1;
+                }
+            }
+        }
+        if (j < e) {
+            const double t0 = __ldg(a.xs + j) - c;
+            double w0 = __ldg(a.qs + j);
+#pragma unroll
+            for (int k = 0; k < REG_ORDER; ++k) {
+                if (k < o1) {
+                    acc[k] += w0;
+                    w0 *= t0;
+                }
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < REG_ORDER; ++k)
+            if (k < o1)
+                put_raw_sum(a, node, k, acc[k]);
+    }
+}
+
+// M2M of one level, one warp per internal node, lane k -> order k:
+// m_k(parent) = sum_children sum_{j<=k} m_j(child) pw_{k-j},
+// pw_i = delta^i / i! from a multiplicative warp scan; the child row and pw
+// are staged in shared memory (row reads broadcast, pw reads conflict-free).
+__device__ __forceinline__ void m2m_level_warps(const MomArgs &a, int64_t f0, int64_t f1,
+                                                int64_t gwarp, int64_t nwarps,
+                                                const double *inv_s, double *pw_s, double *m_s)
+{
+    const int lane = dt_lane();
+    const int o1 = (int)a.order + 1;
+    for (int64_t node = f0 + gwarp; node < f1; node += nwarps) {
+        const int64_t l = __ldg(a.left + node), r = __ldg(a.right + node);
+        if (l < 0 && r < 0)
+            continue;
+        const double c = __ldg(a.center + node);
+        double out = 0.0;
+#pragma unroll
+        for (int ci = 0; ci < 2; ++ci) {
+            const int64_t ch = ci == 0 ? l : r;
+            if (ch < 0)
+                continue;
+            const double delta = __ldg(a.center + ch) - c;
+            double v = lane == 0 ? 1.0 : delta * inv_s[lane];
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const double t = __shfl_up_sync(DT_FULL, v, o);
+                if (lane >= o)
+                    v *= t;
+            }
+            pw_s[lane] = v;
+            m_s[lane] = lane < o1 ? __ldcg(a.moments + ch * o1 + lane) : 0.0;
+            __syncwarp();
+            double acc = 0.0;
+            for (int j = 0; j <= lane && j < o1; ++j)
+                acc = __fma_rn(m_s[j], pw_s[lane - j], acc);
+            out += acc;
+            __syncwarp();
+        }
+        if (lane < o1)
+            put_moment(a, node, lane, out);
+    }
+}
+
+__global__ void __launch_bounds__(256) m2m_levels_kernel(MomArgs a)
+{
+    cg::grid_group grid = cg::this_grid();
+    __shared__ double inv_s[32];
+    __shared__ double pw_s[8][32], m_s[8][32];
+    if (threadIdx.x < 32)
+        inv_s[threadIdx.x] = c_inv_k[threadIdx.x];
+    __syncthreads();
+    const volatile int64_t *meta = a.meta;
+    const int64_t depth = meta[DT_META_DEPTH];
+    const int warp = threadIdx.x >> 5;
+    const int64_t gwarp = (int64_t)blockIdx.x * 8 + warp;
+    const int64_t nwarps = (int64_t)gridDim.x * 8;
+    for (int64_t lev = depth - 1; lev >= 0; --lev) {
+        m2m_level_warps(a, meta[DT_META_LEVEL0 + lev], meta[DT_META_LEVEL0 + lev + 1], gwarp,
+                        nwarps, inv_s, pw_s[warp], m_s[warp]);
+        grid.sync();
+    }
+}
+
 }  // namespace
 
 extern "C" size_t dt_moments_workspace(int64_t node_capacity)
@@ -395,6 +528,20 @@ extern "C" int dt_moments(const double *xs, const double *qs, const double *cent
               eval_stride, (int32_t *)workspace, (int32_t *)workspace + node_capacity};
     cudaStream_t s = (cudaStream_t)stream;
     const int sms = dt_num_sms();
+    if (order + 1 <= REG_ORDER) {
+        p2m_thread_kernel<<<sms * 16, 128, 0, s>>>(a);
+        DT_CUDA_TRY(cudaGetLastError());
+        int per_sm = 0;
+        DT_CUDA_TRY(
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, m2m_levels_kernel, 256, 0));
+        if (per_sm < 1)
+            return dt_set_error(DT_ERR_CUDA, "m2m kernel cannot be resident");
+        const int grid = sms * (per_sm > 4 ? 4 : per_sm);
+        void *args[] = {&a};
+        DT_CUDA_TRY(cudaLaunchCooperativeKernel((const void *)m2m_levels_kernel, grid, 256, args,
+                                                0, s));
+        return DT_OK;
+    }
     moments_prep_kernel<<<sms * 8, 256, 0, s>>>(a);
     DT_CUDA_TRY(cudaGetLastError());
     moments_kernel<<<sms * 8, MOM_THREADS, 0, s>>>(a);
