@@ -42,6 +42,9 @@ namespace {
 #ifndef DT_EVAL_MINB
 #define DT_EVAL_MINB 4
 #endif
+#ifndef DT_EVAL_OVERLAP
+#define DT_EVAL_OVERLAP 0
+#endif
 #ifndef DT_EVAL_THREADS
 #define DT_EVAL_THREADS 256
 #endif
@@ -312,6 +315,53 @@ __device__ int psel_fast(double big_r, double h, const EvalArgs &a, const float 
     return min(p, a.p_cap);
 }
 
+
+// Branch-free form of psel_fast (same return codes): every regime is
+// evaluated and selected, so the compiler can interleave this fp32 chain
+// with the independent FP64 far-field setup of the same pair.
+__device__ __forceinline__ int psel_fast_bf(double big_r, double h, const EvalArgs &a,
+                                            const float *isig, float rd2f, float inv_tol_f)
+{
+    const float Rf = (float)big_r;
+    const float hf = (float)h;
+    const float iR = fast_rcp(Rf);
+    const float ratio = hf * iR;
+    const float sstar = rd2f * iR * iR;
+    const bool bad0 =
+        !(Rf > 1e-15f && Rf < 1e15f && ratio > 1e-30f && sstar > 1e-12f && sstar < 1e30f);
+    const float z = fminf(1.0f, 0.5f * sstar * rsqrtf(sstar));
+    const float om = 1.0f - z;
+    const float poly = fmaf(fmaf(fmaf(-0.0187293f, z, 0.0742610f), z, -0.2121144f), z,
+                            1.5707288f);
+    const float asz = 1.57079633f - om * rsqrtf(fmaxf(om, 1e-30f)) * poly;
+    const int tb0 = min(max((int)(asz * 20.371832715762604f), 0), 32);
+    const int t0 = sstar >= 4.0f ? 32 : (sstar <= isig[34] ? 0 : tb0);
+    const int ta = max(t0, 1), tb = min(t0 + 1, 32);
+    const float ua = sstar * isig[ta], ub = sstar * isig[tb];
+    const float emin = fminf((1.0f - ua) * (1.0f - ua), (1.0f - ub) * (1.0f - ub));
+    const float rq = rsqrtf(emin + sstar);
+    const float M = rq * rsqrtf(rq);
+    const float X = 1.1f * M * hf * inv_tol_f * fast_rcp(Rf - hf);
+    const bool bad = bad0 || !(X > 1e-37f && X < 1e37f);
+    int ex, er;
+    float fx, fr;
+    split_log2(X, &ex, &fx);
+    split_log2(ratio, &er, &fr);
+    const float L = -((float)er + fr);
+    const float iL = fast_rcp(L);
+    const float pstar_approx = ((float)ex + fx) * iL;
+    const int n = __float2int_rn(fminf(fmaxf(pstar_approx, -2.0f), 1e4f));
+    const float resid = (float)(ex + n * er) + fmaf((float)n, fr, fx);
+    const float dist = resid * iL;
+    const bool amb = fabsf(dist) < PSEL_MARGIN && n >= 0 && n <= a.p_cap - 1;
+    const int p = min(max(dist > 0.0f ? n + 1 : n, 0), a.p_cap);
+    int r = amb ? -(t0 + 2) : p;
+    r = pstar_approx < -1.0f ? 0 : r;
+    r = pstar_approx > (float)a.p_cap + 1.0f ? a.p_cap : r;
+    r = bad ? -1 : r;
+    return h == 0.0 ? 0 : r;
+}
+
 // ------------------------------------------------------------------ far / near
 
 __constant__ double c_rcp[128] = {  // 1/k (k >= 1)
@@ -357,34 +407,50 @@ __constant__ double c_rcp[128] = {  // 1/k (k >= 1)
 // with g_2, g_3 from the same formula without the vanishing terms.  The
 // matching moments M'_k = (k-1)! m_k come from dt_moments (row stride even,
 // 16-byte aligned, read two at a time).  5 FP64 instructions per order.
-template <bool WIDE>
-__device__ __forceinline__ double far_field(double d, double rd2, const double2 *__restrict__ M2,
-                                            int pu, int pmin, int pmax)
+struct FarPre {
+    double g0, g1, g2, g3, a0, ci, ir3, inv;
+};
+
+__device__ __forceinline__ FarPre far_setup(double d, double rd2)
 {
+    FarPre f;
     const double s2 = __fma_rn(d, d, rd2);
     const double r = dt_rsqrt(s2);
-    const double g0 = d * r;
+    const double ir2 = r * r;
+    f.g0 = d * r;
+    f.g1 = rd2 * r * ir2;
+    f.inv = ir2 * dt_rcp(d);
+    f.a0 = rd2 * f.inv;
+    f.ci = __fma_rn(3.0 * d, d, rd2) * f.inv;
+    f.ir3 = 3.0 * ir2;
+    f.g2 = (f.a0 - f.ci) * f.g1;
+    f.g3 = __fma_rn(-f.ir3, f.g1, __fma_rn(f.a0, 0.5, -f.ci) * f.g2);
+    return f;
+}
+
+template <bool WIDE>
+__device__ __forceinline__ double far_field(double d, double rd2, const double2 *__restrict__ M2,
+                                            int pu, int pmin, int pmax);
+
+template <bool WIDE>
+__device__ __forceinline__ double far_sum(const FarPre &f, const double2 *__restrict__ M2,
+                                          int pu, int pmin, int pmax)
+{
+    const double a0 = f.a0, ci = f.ci, ir3 = f.ir3, inv = f.inv;
+    const double g1 = f.g1, g2 = f.g2, g3 = f.g3;
     const double2 m01 = __ldg(M2);
-    double acc = g0 * m01.x;
+    double acc = f.g0 * m01.x;
     if (pmax < 1)
         return acc;
-    const double ir2 = r * r;
-    const double g1 = rd2 * r * ir2;
     if (pu >= 1)
         acc = __fma_rn(g1, m01.y, acc);
     if (pmax < 2)
         return acc;
-    const double inv = ir2 * dt_rcp(d);
-    const double a0 = rd2 * inv;
-    const double ci = __fma_rn(3.0 * d, d, rd2) * inv;
-    const double ir3 = 3.0 * ir2;
     const double2 m23 = __ldg(M2 + 1);
-    const double g2 = (a0 - ci) * g1;
     if (pu >= 2)
         acc = __fma_rn(g2, m23.x, acc);
     if (pmax < 3)
         return acc;
-    const double g3 = __fma_rn(-ir3, g1, __fma_rn(a0, 0.5, -ci) * g2);
     if (pu >= 3)
         acc = __fma_rn(g3, m23.y, acc);
     // The g_{k-2}, g_{k-3} part of each step is formed off the critical
@@ -431,6 +497,13 @@ __device__ __forceinline__ double far_field(double d, double rd2, const double2 
         gm1 = t;
     }
     return acc + acc1;
+}
+
+template <bool WIDE>
+__device__ __forceinline__ double far_field(double d, double rd2, const double2 *__restrict__ M2,
+                                            int pu, int pmin, int pmax)
+{
+    return far_sum<WIDE>(far_setup(d, rd2), M2, pu, pmin, pmax);
 }
 
 __device__ __forceinline__ double near_term(double2 u, double y, double rd2)
@@ -548,6 +621,44 @@ __global__ void __launch_bounds__(EVAL_THREADS, DT_EVAL_MINB) tree_eval_kernel(E
             const double big_r = fabs(d);
             const bool far = act && big_r > 0.0 && half <= __dmul_rn(a.theta, big_r);
             const unsigned fm = __ballot_sync(DT_FULL, far);
+#if DT_EVAL_OVERLAP
+            if (fm) {
+                int pu = -1;
+                FarPre fpre;
+                if (far) {
+                    fpre = far_setup(d, a.rd2);
+                    if (ADAPTIVE) {
+                        int r = fast_ok ? psel_fast_bf(big_r, half, a, isig_s, rd2f, inv_tol_f)
+                                        : -1;
+                        if (r < 0) {
+                            if (r <= -2 && fast_ok)
+                                r = psel_exact_bracket(big_r, half, -r - 2, a, cs, sn);
+                            else
+                                r = psel_exact_all(big_r, half, a, cs, sn);
+                            if (STATS)
+                                ++c_exact;
+                        }
+                        pu = r;
+                    } else {
+                        pu = a.p;
+                    }
+                }
+                const int pmax = __reduce_max_sync(DT_FULL, pu);
+                const int pmin = __reduce_min_sync(DT_FULL, far ? pu : 1 << 20);
+                if (far) {
+                    acc += far_sum<WIDE>(
+                        fpre,
+                        reinterpret_cast<const double2 *>(a.moments + (int64_t)node * a.stride),
+                        pu, pmin, pmax);
+                    if (STATS) {
+                        hh += mix64((uint64_t)node * 256u + (uint64_t)pu);
+                        ++c_far;
+                        c_sump += pu;
+                        c_p0 += pu == 0;
+                    }
+                }
+            }
+#else
             if (fm) {
                 int pu = -1;
                 if (far) {
@@ -581,6 +692,7 @@ __global__ void __launch_bounds__(EVAL_THREADS, DT_EVAL_MINB) tree_eval_kernel(E
                     }
                 }
             }
+#endif
             const unsigned rest = mask & ~fm;
             if (rest) {
                 if (lr.x < 0 && lr.y < 0) {
