@@ -110,8 +110,8 @@ int dt_build_tree(const double *xs, int64_t n, int64_t leaf_capacity, int64_t ma
 
 /* Node moments m_k = sum_j q_j (x_j - c)^k / k!, k = 0..order, row-major
  * [n_nodes][order + 1] (tree.py:224-238): P2M at every leaf from its sources,
- * then M2M (binomial shift) bottom-up as a dataflow (a node is formed by the
- * warp that finishes its last child).  Reads the tree produced by
+ * then M2M (binomial shift) bottom-up, one level at a time (order <= 31;
+ * higher orders use a barrier-free dataflow).  Reads the tree produced by
  * dt_build_tree (meta gives n_nodes); node_capacity bounds the node arrays.
  * moments_eval (optional) receives the traversal layout used by the *_packed
  * and *_device evaluators: M'_0 = m_0, M'_k = (k-1)! m_k, row stride
@@ -122,6 +122,63 @@ int dt_moments(const double *xs, const double *qs, const double *center, const i
                const int64_t *meta, int64_t order, double *moments, double *moments_eval,
                int64_t eval_stride, int64_t node_capacity, void *workspace,
                size_t workspace_bytes, void *stream);
+
+/* ---------------------------------------------------------------- (c) sharded */
+
+/* Multi-GPU upward pass (the reference's run_chunked,
+ * _kernels.py:269-289, shards targets only).  Every rank holds the full tree
+ * and sources; rank r evaluates a contiguous slice of the sorted targets.
+ * The moments are split at a cut level l: rank r forms (P2M + M2M) only the
+ * subtrees under the level-l nodes it owns or its targets can open, the
+ * level-l rows of the owners are all-gathered (one NCCL all-gather of
+ * dt_shard_rows_bytes() per rank), and every rank forms levels < l
+ * redundantly.  Each row is produced by the same arithmetic as dt_moments,
+ * so every row a rank's traversal reads is bit-identical to the
+ * single-GPU row and the field is bit-identical for any world size.
+ *
+ * Plan block: int64[DT_PLAN_WORDS] in device memory, written by
+ * dt_shard_plan without host round trips. */
+#define DT_MAX_WORLD 64
+#define DT_PLAN_CUT 0         /* cut level l = min(requested, depth)               */
+#define DT_PLAN_LEVEL_BEGIN 1 /* level-l nodes are [begin, end)                     */
+#define DT_PLAN_LEVEL_END 2
+#define DT_PLAN_SRC_LO 3      /* this rank forms the subtrees under level l whose   */
+#define DT_PLAN_SRC_HI 4      /* source ranges lie in [src_lo, src_hi)              */
+#define DT_PLAN_NEED_LO 5     /* level-l nodes its targets may open: [lo, hi)       */
+#define DT_PLAN_NEED_HI 6
+#define DT_PLAN_OWNER0 8      /* rank r owns level-l nodes [plan[8 + r], plan[9 + r]) */
+#define DT_PLAN_WORDS (DT_PLAN_OWNER0 + DT_MAX_WORLD + 1)
+
+/* Plan for `rank` of `world`: owners split the level-l nodes into contiguous
+ * runs of ~n_src / world sources; the opened set holds every level-l node
+ * with half * (1 + 2^-40) > theta * dist(center, [min ys, max ys]) -- a
+ * superset of the nodes the MAC (R > 0 && h <= theta R, _kernels.py:211)
+ * can reject for any of this rank's targets ys[0..n_targets).
+ * targets_sorted != 0 reads the extremes from the ends of ys. */
+int dt_shard_plan(const double *center, const double *half, const int64_t *start,
+                  const int64_t *end, const int64_t *meta, int64_t n_src, const double *ys,
+                  int64_t n_targets, int targets_sorted, double theta, int64_t cut_level,
+                  int world, int rank, int64_t *plan, void *stream);
+/* Per-rank slot of the gather buffer: 2^cut_level rows of (order + 1) moments
+ * followed by eval_stride traversal moments. */
+size_t dt_shard_rows_bytes(int64_t cut_level, int64_t order, int64_t eval_stride);
+/* dt_moments restricted to the plan: leaves above level l, and every node at
+ * levels >= l whose sources lie in [src_lo, src_hi).  order <= 31. */
+int dt_moments_partial(const double *xs, const double *qs, const double *center,
+                       const int64_t *start, const int64_t *end, const int64_t *left,
+                       const int64_t *right, const int64_t *meta, const int64_t *plan,
+                       int64_t order, double *moments, double *moments_eval,
+                       int64_t eval_stride, void *stream);
+/* Copy this rank's owned level-l rows into its gather slot `send`. */
+int dt_shard_pack(const int64_t *plan, int rank, int64_t cut_level, int64_t order,
+                  const double *moments, const double *moments_eval, int64_t eval_stride,
+                  double *send, void *stream);
+/* After the all-gather (recv = world slots, rank order): write every owner's
+ * level-l rows, then form levels < l (M2M), in one kernel. */
+int dt_shard_finish(const int64_t *plan, int world, int64_t cut_level, const double *recv,
+                    const double *center, const int64_t *left, const int64_t *right,
+                    const int64_t *meta, int64_t order, double *moments, double *moments_eval,
+                    int64_t eval_stride, void *stream);
 
 /* ---------------------------------------------------------------- (d)+(e) */
 

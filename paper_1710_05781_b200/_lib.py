@@ -26,6 +26,16 @@ DT_META_LEAVES = 2
 DT_META_OVERFLOW = 3
 DT_META_LEVEL0 = 8
 DT_META_WORDS = 72
+DT_MAX_WORLD = 64
+DT_PLAN_CUT = 0
+DT_PLAN_LEVEL_BEGIN = 1
+DT_PLAN_LEVEL_END = 2
+DT_PLAN_SRC_LO = 3
+DT_PLAN_SRC_HI = 4
+DT_PLAN_NEED_LO = 5
+DT_PLAN_NEED_HI = 6
+DT_PLAN_OWNER0 = 8
+DT_PLAN_WORDS = DT_PLAN_OWNER0 + DT_MAX_WORLD + 1
 
 _P = C.c_void_p
 _I64 = C.c_int64
@@ -63,6 +73,18 @@ SIGNATURES = {
     "dt_moments_workspace": (_SZ, [_I64]),
     "dt_moments": (
         C.c_int, [_P, _P, _P, _P, _P, _P, _P, _P, _I64, _P, _P, _I64, _I64, _P, _SZ, _P],
+    ),
+    "dt_shard_plan": (
+        C.c_int,
+        [_P, _P, _P, _P, _P, _I64, _P, _I64, C.c_int, _D, _I64, C.c_int, C.c_int, _P, _P],
+    ),
+    "dt_shard_rows_bytes": (_SZ, [_I64, _I64, _I64]),
+    "dt_moments_partial": (
+        C.c_int, [_P, _P, _P, _P, _P, _P, _P, _P, _P, _I64, _P, _P, _I64, _P],
+    ),
+    "dt_shard_pack": (C.c_int, [_P, C.c_int, _I64, _I64, _P, _P, _I64, _P, _P]),
+    "dt_shard_finish": (
+        C.c_int, [_P, C.c_int, _I64, _P, _P, _P, _P, _P, _I64, _P, _P, _I64, _P],
     ),
     "dt_pack_sources": (C.c_int, [_P, _P, _I64, _P, _P]),
     "dt_pack_tree": (C.c_int, [_P, _P, _P, _P, _P, _P, _I64, _P, _P]),

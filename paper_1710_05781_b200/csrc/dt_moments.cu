@@ -37,6 +37,7 @@ struct MomArgs {
     int64_t estride;   // its row stride (even, >= order + 1; pad entries are 0)
     int32_t *parent;   // workspace: parent index per node (-1 at the root)
     int32_t *arrived;  // workspace: finished children per node
+    const int64_t *plan;  // optional shard plan (DT_PLAN_*): restrict to this rank's subtrees
 };
 
 __constant__ double c_inv_k[MAX_ORDER1] = {  // 1/k rounded to nearest (k >= 1)
@@ -382,11 +383,20 @@ __global__ void __launch_bounds__(128) p2m_thread_kernel(MomArgs a)
 {
     const int64_t n = __ldg(a.meta + DT_META_NODES);
     const int o1 = (int)a.order + 1;
+    // shard plan: leaves above the cut always, below it only inside [lo, hi)
+    int64_t cut_begin = INT64_MAX, lo = 0, hi = 0;
+    if (a.plan) {
+        cut_begin = __ldg(a.plan + DT_PLAN_LEVEL_BEGIN);
+        lo = __ldg(a.plan + DT_PLAN_SRC_LO);
+        hi = __ldg(a.plan + DT_PLAN_SRC_HI);
+    }
     for (int64_t node = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; node < n;
          node += (int64_t)gridDim.x * blockDim.x) {
         if (__ldg(a.left + node) >= 0 || __ldg(a.right + node) >= 0)
             continue;
         const int64_t s = __ldg(a.start + node), e = __ldg(a.end + node);
+        if (node >= cut_begin && (s < lo || e > hi))
+            continue;
         const double c = __ldg(a.center + node);
         double acc[REG_ORDER];
 #pragma unroll
@@ -445,13 +455,17 @@ __global__ void __launch_bounds__(128) p2m_thread_kernel(MomArgs a)
 // are staged in shared memory (row reads broadcast, pw reads conflict-free).
 __device__ __forceinline__ void m2m_level_warps(const MomArgs &a, int64_t f0, int64_t f1,
                                                 int64_t gwarp, int64_t nwarps,
-                                                const double *inv_s, double *pw_s, double *m_s)
+                                                const double *inv_s, double *pw_s, double *m_s,
+                                                bool filter = false, int64_t src_lo = 0,
+                                                int64_t src_hi = 0)
 {
     const int lane = dt_lane();
     const int o1 = (int)a.order + 1;
     for (int64_t node = f0 + gwarp; node < f1; node += nwarps) {
         const int64_t l = __ldg(a.left + node), r = __ldg(a.right + node);
         if (l < 0 && r < 0)
+            continue;
+        if (filter && (__ldg(a.start + node) < src_lo || __ldg(a.end + node) > src_hi))
             continue;
         const double c = __ldg(a.center + node);
         double out = 0.0;
@@ -495,11 +509,188 @@ __global__ void __launch_bounds__(256) m2m_levels_kernel(MomArgs a)
     const int warp = threadIdx.x >> 5;
     const int64_t gwarp = (int64_t)blockIdx.x * 8 + warp;
     const int64_t nwarps = (int64_t)gridDim.x * 8;
-    for (int64_t lev = depth - 1; lev >= 0; --lev) {
+    int64_t stop = 0, lo = 0, hi = 0;
+    if (a.plan) {  // levels >= cut, this rank's subtrees only
+        stop = __ldg(a.plan + DT_PLAN_CUT);
+        lo = __ldg(a.plan + DT_PLAN_SRC_LO);
+        hi = __ldg(a.plan + DT_PLAN_SRC_HI);
+    }
+    for (int64_t lev = depth - 1; lev >= stop; --lev) {
         m2m_level_warps(a, meta[DT_META_LEVEL0 + lev], meta[DT_META_LEVEL0 + lev + 1], gwarp,
-                        nwarps, inv_s, pw_s[warp], m_s[warp]);
+                        nwarps, inv_s, pw_s[warp], m_s[warp], a.plan != nullptr, lo, hi);
         grid.sync();
     }
+}
+
+// ---- multi-GPU sharding (include/disctree_b200.h "(c) sharded") ----
+
+constexpr int PLAN_THREADS = 256;
+
+__global__ void __launch_bounds__(PLAN_THREADS)
+    shard_plan_kernel(const double *center, const double *half, const int64_t *start,
+                      const int64_t *end, const int64_t *meta, int64_t n_src, const double *ys,
+                      int64_t n_targets, int sorted, double theta, int64_t cut_req, int world,
+                      int rank, int64_t *plan)
+{
+    __shared__ double s_lo[PLAN_THREADS / 32], s_hi[PLAN_THREADS / 32];
+    __shared__ unsigned long long s_need_lo, s_need_hi;
+    const int tid = threadIdx.x, lane = dt_lane(), warp = tid >> 5;
+    const int64_t depth = __ldg(meta + DT_META_DEPTH);
+    const int64_t cut = cut_req < depth ? cut_req : depth;
+    const int64_t b = __ldg(meta + DT_META_LEVEL0 + cut), e = __ldg(meta + DT_META_LEVEL0 + cut + 1);
+    // target extremes
+    double ylo = INFINITY, yhi = -INFINITY;
+    if (n_targets > 0) {
+        if (sorted) {
+            ylo = __ldg(ys);
+            yhi = __ldg(ys + n_targets - 1);
+        } else {
+            for (int64_t i = tid; i < n_targets; i += PLAN_THREADS) {
+                const double y = __ldg(ys + i);
+                ylo = fmin(ylo, y);
+                yhi = fmax(yhi, y);
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                ylo = fmin(ylo, __shfl_xor_sync(DT_FULL, ylo, o));
+                yhi = fmax(yhi, __shfl_xor_sync(DT_FULL, yhi, o));
+            }
+            if (lane == 0) {
+                s_lo[warp] = ylo;
+                s_hi[warp] = yhi;
+            }
+            __syncthreads();
+            ylo = s_lo[0];
+            yhi = s_hi[0];
+            for (int w = 1; w < PLAN_THREADS / 32; ++w) {
+                ylo = fmin(ylo, s_lo[w]);
+                yhi = fmax(yhi, s_hi[w]);
+            }
+        }
+    }
+    if (tid == 0) {
+        s_need_lo = (unsigned long long)e;
+        s_need_hi = (unsigned long long)b;
+    }
+    __syncthreads();
+    // level-l nodes some target may open: not (h <= theta R) for some y
+    if (n_targets > 0) {
+        for (int64_t i = b + tid; i < e; i += PLAN_THREADS) {
+            const double c = __ldg(center + i), h = __ldg(half + i);
+            const double dist = c < ylo ? ylo - c : (c > yhi ? c - yhi : 0.0);
+            if (h * (1.0 + 0x1p-40) > theta * dist) {
+                atomicMin(&s_need_lo, (unsigned long long)i);
+                atomicMax(&s_need_hi, (unsigned long long)(i + 1));
+            }
+        }
+    }
+    // owners: rank r starts at the first level-l node with start >= floor(r n / world)
+    for (int r = tid; r <= world; r += PLAN_THREADS) {
+        int64_t at;
+        if (r == 0) {
+            at = b;
+        } else if (r == world) {
+            at = e;
+        } else {
+            const int64_t want = (int64_t)(((__int128)r * n_src) / world);
+            int64_t lo = b, hi = e;
+            while (lo < hi) {
+                const int64_t mid = lo + ((hi - lo) >> 1);
+                if (__ldg(start + mid) < want)
+                    lo = mid + 1;
+                else
+                    hi = mid;
+            }
+            at = lo;
+        }
+        plan[DT_PLAN_OWNER0 + r] = at;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        const int64_t nlo = (int64_t)s_need_lo, nhi = (int64_t)s_need_hi;
+        int64_t ulo = plan[DT_PLAN_OWNER0 + rank], uhi = plan[DT_PLAN_OWNER0 + rank + 1];
+        if (nlo < nhi) {
+            if (ulo >= uhi) {
+                ulo = nlo;
+                uhi = nhi;
+            } else {
+                ulo = nlo < ulo ? nlo : ulo;
+                uhi = nhi > uhi ? nhi : uhi;
+            }
+        }
+        plan[DT_PLAN_CUT] = cut;
+        plan[DT_PLAN_LEVEL_BEGIN] = b;
+        plan[DT_PLAN_LEVEL_END] = e;
+        plan[DT_PLAN_SRC_LO] = ulo < uhi ? __ldg(start + ulo) : 0;
+        plan[DT_PLAN_SRC_HI] = ulo < uhi ? __ldg(end + uhi - 1) : 0;
+        plan[DT_PLAN_NEED_LO] = nlo < nhi ? nlo : b;
+        plan[DT_PLAN_NEED_HI] = nlo < nhi ? nhi : b;
+        for (int r = world + 1; r <= DT_MAX_WORLD; ++r)
+            plan[DT_PLAN_OWNER0 + r] = e;
+    }
+}
+
+__global__ void shard_pack_kernel(const int64_t *plan, int rank, int64_t o1, const double *moments,
+                                  const double *meval, int64_t es, double *send)
+{
+    const int64_t a0 = __ldg(plan + DT_PLAN_OWNER0 + rank);
+    const int64_t rows = __ldg(plan + DT_PLAN_OWNER0 + rank + 1) - a0;
+    const int64_t w = o1 + es;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < rows * w;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t row = i / w, k = i - row * w;
+        send[i] = k < o1 ? __ldg(moments + (a0 + row) * o1 + k)
+                         : __ldg(meval + (a0 + row) * es + (k - o1));
+    }
+}
+
+// One block: scatter every owner's level-l rows, then M2M levels cut-1 .. 0.
+__global__ void __launch_bounds__(256) shard_finish_kernel(MomArgs a, int world, int64_t slot_rows,
+                                                           const double *recv)
+{
+    __shared__ double inv_s[32];
+    __shared__ double pw_s[8][32], m_s[8][32];
+    if (threadIdx.x < 32)
+        inv_s[threadIdx.x] = c_inv_k[threadIdx.x];
+    const int64_t o1 = a.order + 1, es = a.meval ? a.estride : 0, w = o1 + es;
+    for (int r = 0; r < world; ++r) {
+        const int64_t a0 = __ldg(a.plan + DT_PLAN_OWNER0 + r);
+        const int64_t rows = __ldg(a.plan + DT_PLAN_OWNER0 + r + 1) - a0;
+        const double *slot = recv + (int64_t)r * slot_rows * w;
+        for (int64_t i = threadIdx.x; i < rows * w; i += blockDim.x) {
+            const int64_t row = i / w, k = i - row * w;
+            if (k < o1)
+                a.moments[(a0 + row) * o1 + k] = slot[i];
+            else
+                a.meval[(a0 + row) * es + (k - o1)] = slot[i];
+        }
+    }
+    __syncthreads();
+    const int64_t cut = __ldg(a.plan + DT_PLAN_CUT);
+    const int warp = threadIdx.x >> 5;
+    for (int64_t lev = cut - 1; lev >= 0; --lev) {
+        m2m_level_warps(a, __ldg(a.meta + DT_META_LEVEL0 + lev),
+                        __ldg(a.meta + DT_META_LEVEL0 + lev + 1), warp, 8, inv_s, pw_s[warp],
+                        m_s[warp]);
+        __syncthreads();
+    }
+}
+
+// P2M (thread per leaf) + cooperative level M2M, honouring a.plan.
+int launch_level_moments(MomArgs &a, cudaStream_t s)
+{
+    const int sms = dt_num_sms();
+    p2m_thread_kernel<<<sms * 16, 128, 0, s>>>(a);
+    DT_CUDA_TRY(cudaGetLastError());
+    int per_sm = 0;
+    DT_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, m2m_levels_kernel, 256, 0));
+    if (per_sm < 1)
+        return dt_set_error(DT_ERR_CUDA, "m2m kernel cannot be resident");
+    const int grid = sms * (per_sm > 4 ? 4 : per_sm);
+    void *args[] = {&a};
+    DT_CUDA_TRY(
+        cudaLaunchCooperativeKernel((const void *)m2m_levels_kernel, grid, 256, args, 0, s));
+    return DT_OK;
 }
 
 }  // namespace
@@ -525,26 +716,96 @@ extern "C" int dt_moments(const double *xs, const double *qs, const double *cent
     if (!workspace || workspace_bytes < dt_moments_workspace(node_capacity))
         return dt_set_error(DT_ERR_WORKSPACE, "moments workspace too small");
     MomArgs a{xs, qs, center, start, end, left, right, meta, order, moments, moments_eval,
-              eval_stride, (int32_t *)workspace, (int32_t *)workspace + node_capacity};
+              eval_stride, (int32_t *)workspace, (int32_t *)workspace + node_capacity, nullptr};
     cudaStream_t s = (cudaStream_t)stream;
     const int sms = dt_num_sms();
-    if (order + 1 <= REG_ORDER) {
-        p2m_thread_kernel<<<sms * 16, 128, 0, s>>>(a);
-        DT_CUDA_TRY(cudaGetLastError());
-        int per_sm = 0;
-        DT_CUDA_TRY(
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, m2m_levels_kernel, 256, 0));
-        if (per_sm < 1)
-            return dt_set_error(DT_ERR_CUDA, "m2m kernel cannot be resident");
-        const int grid = sms * (per_sm > 4 ? 4 : per_sm);
-        void *args[] = {&a};
-        DT_CUDA_TRY(cudaLaunchCooperativeKernel((const void *)m2m_levels_kernel, grid, 256, args,
-                                                0, s));
-        return DT_OK;
-    }
+    if (order + 1 <= REG_ORDER)
+        return launch_level_moments(a, s);
     moments_prep_kernel<<<sms * 8, 256, 0, s>>>(a);
     DT_CUDA_TRY(cudaGetLastError());
     moments_kernel<<<sms * 8, MOM_THREADS, 0, s>>>(a);
+    DT_CUDA_TRY(cudaGetLastError());
+    return DT_OK;
+}
+
+extern "C" int dt_shard_plan(const double *center, const double *half, const int64_t *start,
+                             const int64_t *end, const int64_t *meta, int64_t n_src,
+                             const double *ys, int64_t n_targets, int targets_sorted,
+                             double theta, int64_t cut_level, int world, int rank, int64_t *plan,
+                             void *stream)
+{
+    DT_CHECK_ARG(center && half && start && end && meta && plan, "null pointer");
+    DT_CHECK_ARG(n_targets == 0 || ys, "null targets");
+    DT_CHECK_ARG(world >= 1 && world <= DT_MAX_WORLD && rank >= 0 && rank < world,
+                 "bad world size / rank");
+    DT_CHECK_ARG(cut_level >= 0 && cut_level <= 24, "cut_level must be in [0, 24]");
+    DT_CHECK_ARG(theta > 0.0, "theta must be > 0");
+    shard_plan_kernel<<<1, PLAN_THREADS, 0, (cudaStream_t)stream>>>(
+        center, half, start, end, meta, n_src, ys, n_targets, targets_sorted, theta, cut_level,
+        world, rank, plan);
+    DT_CUDA_TRY(cudaGetLastError());
+    return DT_OK;
+}
+
+extern "C" size_t dt_shard_rows_bytes(int64_t cut_level, int64_t order, int64_t eval_stride)
+{
+    if (cut_level < 0 || cut_level > 24 || order < 0 || eval_stride < 0)
+        return 0;
+    return ((size_t)1 << cut_level) * (size_t)(order + 1 + eval_stride) * sizeof(double);
+}
+
+extern "C" int dt_moments_partial(const double *xs, const double *qs, const double *center,
+                                  const int64_t *start, const int64_t *end, const int64_t *left,
+                                  const int64_t *right, const int64_t *meta, const int64_t *plan,
+                                  int64_t order, double *moments, double *moments_eval,
+                                  int64_t eval_stride, void *stream)
+{
+    DT_CHECK_ARG(order >= 0 && order + 1 <= REG_ORDER, "sharded moments need order <= 31");
+    DT_CHECK_ARG(!moments_eval || (eval_stride >= order + 1 && eval_stride % 2 == 0),
+                 "eval_stride must be even and >= order + 1");
+    DT_CHECK_ARG(xs && qs && center && start && end && left && right && meta && plan && moments,
+                 "null pointer");
+    MomArgs a{xs, qs, center, start, end, left, right, meta, order, moments, moments_eval,
+              eval_stride, nullptr, nullptr, plan};
+    return launch_level_moments(a, (cudaStream_t)stream);
+}
+
+extern "C" int dt_shard_pack(const int64_t *plan, int rank, int64_t cut_level, int64_t order,
+                             const double *moments, const double *moments_eval,
+                             int64_t eval_stride, double *send, void *stream)
+{
+    DT_CHECK_ARG(plan && moments && send, "null pointer");
+    DT_CHECK_ARG(rank >= 0 && rank < DT_MAX_WORLD, "bad rank");
+    DT_CHECK_ARG(cut_level >= 0 && cut_level <= 24 && order >= 0, "bad cut level / order");
+    const int64_t es = moments_eval ? eval_stride : 0;
+    DT_CHECK_ARG(!moments_eval || (eval_stride >= order + 1 && eval_stride % 2 == 0),
+                 "eval_stride must be even and >= order + 1");
+    const int64_t cells = ((int64_t)1 << cut_level) * (order + 1 + es);
+    int blocks = (int)((cells + 255) / 256);
+    blocks = blocks < 1 ? 1 : (blocks > 4 * dt_num_sms() ? 4 * dt_num_sms() : blocks);
+    shard_pack_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(plan, rank, order + 1, moments,
+                                                               moments_eval, es, send);
+    DT_CUDA_TRY(cudaGetLastError());
+    return DT_OK;
+}
+
+extern "C" int dt_shard_finish(const int64_t *plan, int world, int64_t cut_level,
+                               const double *recv, const double *center, const int64_t *left,
+                               const int64_t *right, const int64_t *meta, int64_t order,
+                               double *moments, double *moments_eval, int64_t eval_stride,
+                               void *stream)
+{
+    DT_CHECK_ARG(plan && recv && center && left && right && meta && moments, "null pointer");
+    DT_CHECK_ARG(world >= 1 && world <= DT_MAX_WORLD, "bad world size");
+    DT_CHECK_ARG(cut_level >= 0 && cut_level <= 24, "bad cut level");
+    DT_CHECK_ARG(order >= 0 && order + 1 <= REG_ORDER, "sharded moments need order <= 31");
+    DT_CHECK_ARG(!moments_eval || (eval_stride >= order + 1 && eval_stride % 2 == 0),
+                 "eval_stride must be even and >= order + 1");
+    // start/end are only read by the range filter, which is open here
+    MomArgs a{nullptr, nullptr, center, nullptr, nullptr, left, right, meta, order, moments,
+              moments_eval, eval_stride, nullptr, nullptr, plan};
+    shard_finish_kernel<<<1, 256, 0, (cudaStream_t)stream>>>(a, world, (int64_t)1 << cut_level,
+                                                             recv);
     DT_CUDA_TRY(cudaGetLastError());
     return DT_OK;
 }

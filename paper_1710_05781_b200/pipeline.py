@@ -11,7 +11,8 @@ ranges, tol_share) from device memory, so the step can be timed back to back
 or captured in a CUDA graph.  Buffers are sized once (node capacity from a
 planning build); a step whose tree overflows the capacity is detected by
 ``check()``.  Used by bench.py and by the multi-GPU driver (contiguous target
-slices [i0, i1) per rank, sources replicated).
+slices [i0, i1) per rank, sources replicated, world > 1: sharded upward
+pass with one all-gather of the cut-level moment rows).
 """
 
 from __future__ import annotations
@@ -39,7 +40,8 @@ LAUNCHES_PER_STEP = 3 + 2 + 1 + 2 + 1 + 1  # scan(3) sign(2) build moments(2) pa
 
 class TreePipeline:
     def __init__(self, n: int, n_targets: int, kernel: DiscKernel, config: EvalConfig,
-                 node_capacity: int | None = None, device=None):
+                 node_capacity: int | None = None, device=None, world: int = 1, rank: int = 0,
+                 group=None, cut_level: int | None = None):
         self.dev = device or _lib.require_device()
         self.n, self.T = int(n), int(n_targets)
         self.kernel, self.config = kernel, config
@@ -61,10 +63,20 @@ class TreePipeline:
         self.sign_ws_bytes = int(L.dt_sign_terms_workspace(self.T))
         self.sign_ws = torch.empty(self.sign_ws_bytes, dtype=torch.uint8, device=self.dev)
         self.cos_t, self.sin_t = contour_tables(self.dev)
+        # world > 1: sharded upward pass (one all-gather of cut-level rows)
+        self.shard = None
+        if world > 1:
+            from .parallel import ShardedMoments
+
+            self.shard = ShardedMoments(self.bufs, self.order, self.moments, self.meval,
+                                        self.estride, config.theta, world, rank, group,
+                                        cut_level)
+        self.launches_per_step = LAUNCHES_PER_STEP + (
+            self.shard.LAUNCHES - 2 if self.shard else 0)
 
     @classmethod
     def planned(cls, xs: torch.Tensor, n_targets: int, kernel: DiscKernel,
-                config: EvalConfig, slack: float = 1.25) -> "TreePipeline":
+                config: EvalConfig, slack: float = 1.25, **kw) -> "TreePipeline":
         """Size the node capacity from one synchronous build of these sources."""
         n = xs.numel()
         cap = initial_node_capacity(n, config.leaf_capacity)
@@ -77,7 +89,7 @@ class TreePipeline:
             cap *= 4
         need = int(meta[_lib.DT_META_NODES] * slack) + 64
         del probe
-        return cls(n, n_targets, kernel, config, node_capacity=need)
+        return cls(n, n_targets, kernel, config, node_capacity=need, **kw)
 
     def step(self, xs: torch.Tensor, qs: torch.Tensor, ys: torch.Tensor, out: torch.Tensor,
              i0: int = 0, i1: int | None = None, eval_events=None) -> None:
@@ -99,7 +111,10 @@ class TreePipeline:
                                    i1 - i0, p(self.sign_ws), self.sign_ws_bytes, s),
                    "dt_sign_terms")
         self.bufs.launch(xs, cfg.leaf_capacity)
-        launch_moments(self.bufs, xs, qs, self.order, self.moments, self.meval)
+        if self.shard is None:
+            launch_moments(self.bufs, xs, qs, self.order, self.moments, self.meval)
+        else:  # this rank's subtrees + all-gather of the cut-level rows
+            self.shard.launch(xs, qs, ys_part, targets_sorted=True)
         pack_sources(xs, qs, self.xq)
         if eval_events is not None:
             eval_events[0].record()

@@ -227,6 +227,12 @@ def build(system: ChargeSystem, kernel: DiscKernel, config: EvalConfig) -> Tree:
     """
     if len(system) == 0:
         raise ValueError("cannot build a tree over an empty charge system")
+    return _build(system, config, None)
+
+
+def _build(system: ChargeSystem, config: EvalConfig, upward) -> Tree:
+    """Structure + moments; ``upward(bufs, order, moments, meval)`` replaces
+    the full upward pass when given (parallel.build_sharded)."""
     dev = _lib.require_device()
     torch.cuda.synchronize(dev)
     t0 = time.perf_counter()
@@ -243,7 +249,10 @@ def build(system: ChargeSystem, kernel: DiscKernel, config: EvalConfig) -> Tree:
     order = moment_order_for(config)
     moments = torch.empty((n_nodes, order + 1), dtype=torch.float64, device=dev)
     meval = torch.empty((n_nodes, eval_stride(order)), dtype=torch.float64, device=dev)
-    launch_moments(bufs, system.xs, system.qs, order, moments, meval)
+    if upward is None:
+        launch_moments(bufs, system.xs, system.qs, order, moments, meval)
+    else:
+        upward(bufs, order, moments, meval)
     xq = pack_sources(system.xs, system.qs)
     torch.cuda.synchronize(dev)
     elapsed = time.perf_counter() - t0

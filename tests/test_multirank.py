@@ -76,3 +76,91 @@ def test_gloo_world2_matches_single_rank(tmp_path, case):
     np.testing.assert_array_equal(got, want)  # bit-identical for any world size
     scale = np.abs(g["qs"]).sum()
     assert np.max(np.abs(got - g["E_tree"])) <= 1e-13 * scale
+
+
+# ---------------------------------------------------------------- sharded moments
+# The sharded upward pass (parallel.ShardedMoments): each rank forms the rows
+# of its own subtrees below the cut, all-gathers the owners' cut-level rows
+# and forms the levels above.  Here the oracle's moments stand in for the
+# device P2M/M2M (rows a rank would not form are NaN), the gather is the real
+# parallel.gather_rows over gloo, and the check is that each rank's traversal
+# of its targets never touches a NaN row and is bit-identical to the
+# single-rank result.
+
+
+def _shard_worker(rank, world, port, case, cut_req, unsorted, out_path):
+    import shard_ref as S
+    from oracle import oracle as O
+    from paper_1710_05781_b200.parallel import gather_rows
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        g = load_case(case)
+        xs, qs = g["xs"], g["qs"]
+        ot = O.build(xs, qs, int(g["p"]), int(g["leaf_capacity"]), bool(g["adaptive"]))
+        tree = {f: getattr(ot, f) for f in O.NODE_FIELDS}
+        ys = g["targets"]
+        if unsorted:  # ragged, unsorted slices
+            ys = np.random.default_rng(7).permutation(ys)
+        i0, i1 = shard_bounds(len(ys), world, rank)
+        mine = ys[i0:i1]
+        plan = S.shard_plan(tree, len(xs), mine, float(g["theta"]), cut_req, world, rank)
+        o1 = ot.moment_order + 1
+        m = np.full_like(ot.moments, np.nan)
+        loc = S.local_rows(tree, plan)
+        m[loc] = ot.moments[loc]
+        rows = 1 << cut_req
+        a, b = plan["owners"][rank], plan["owners"][rank + 1]
+        send = torch.zeros(rows * o1, dtype=torch.float64)
+        send[: (b - a) * o1] = torch.from_numpy(m[a:b].reshape(-1))
+        assert not torch.isnan(send).any(), "an owner must form its own cut-level rows"
+        recv = torch.empty(world * rows * o1, dtype=torch.float64)
+        gather_rows(send, recv, world)
+        slots = recv.numpy().reshape(world, rows, o1)
+        for r in range(world):
+            ra, rb = plan["owners"][r], plan["owners"][r + 1]
+            m[ra:rb] = slots[r, : rb - ra]
+        upper = np.arange(len(m)) < plan["level"][0]  # levels above the cut (M2M stand-in)
+        m[upper] = ot.moments[upper]
+        formed = ~np.isnan(m).any(axis=1)
+        np.testing.assert_array_equal(formed, S.formed_rows(tree, plan))
+        ot_r = O.OracleTree(**tree, depth=ot.depth, leaf_count=ot.leaf_count, moments=m,
+                            moment_order=ot.moment_order)
+        args = (xs, qs, float(g["r_d"]) ** 2, float(g["theta"]), int(g["p"]),
+                bool(g["adaptive"]), O.tol_share(float(g["tolerance"]), ot.depth))
+        got = O.tree_phi_sum(ot_r, *args, mine)
+        want = O.tree_phi_sum(ot, *args, mine)
+        assert np.isfinite(got).all(), "a rank read a moment row it does not hold"
+        np.testing.assert_array_equal(got, want)
+        frac = torch.tensor([formed.mean()], dtype=torch.float64)
+        dist.all_reduce(frac)
+        if rank == 0:
+            np.save(out_path, frac.numpy())
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("case,cut_req,unsorted", [
+    ("cfg1s", 5, False), ("cfg2s", 5, False), ("rand_adaptive", 3, True), ("cfg0", 20, False),
+])
+def test_gloo_world2_sharded_moments(tmp_path, case, cut_req, unsorted):
+    out = str(tmp_path / "frac.npy")
+    mp.start_processes(_shard_worker, args=(2, _free_port(), case, cut_req, unsorted, out),
+                       nprocs=2, join=True, start_method="spawn")
+    frac = float(np.load(out)[0])
+    # sorted slices: each rank forms well under all rows (unsorted slices span
+    # the whole domain, so every rank forms everything)
+    assert frac <= 2.0 and (unsorted or cut_req > 10 or frac < 1.5)
+
+
+def test_default_cut_level_and_gather_single_rank():
+    from paper_1710_05781_b200.parallel import default_cut_level, gather_rows
+
+    assert [default_cut_level(w) for w in (1, 2, 3, 4, 8)] == [4, 5, 6, 6, 7]
+    send = torch.arange(6, dtype=torch.float64)
+    recv = torch.empty(6, dtype=torch.float64)
+    assert torch.equal(gather_rows(send, recv, 1), send)
+    with pytest.raises(ValueError):
+        gather_rows(send, torch.empty(5, dtype=torch.float64), 1)
