@@ -160,7 +160,8 @@ int dt_shard_plan(const double *center, const double *half, const int64_t *start
                   int64_t n_targets, int targets_sorted, double theta, int64_t cut_level,
                   int world, int rank, int64_t *plan, void *stream);
 /* Per-rank slot of the gather buffer: 2^cut_level rows of (order + 1) moments
- * followed by eval_stride traversal moments. */
+ * followed by eval_stride traversal moments (cut_level <= 20; 0 on bad
+ * arguments). */
 size_t dt_shard_rows_bytes(int64_t cut_level, int64_t order, int64_t eval_stride);
 /* dt_moments restricted to the plan: leaves above level l, and every node at
  * levels >= l whose sources lie in [src_lo, src_hi).  order <= 31. */

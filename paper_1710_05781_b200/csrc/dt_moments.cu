@@ -738,7 +738,7 @@ extern "C" int dt_shard_plan(const double *center, const double *half, const int
     DT_CHECK_ARG(n_targets == 0 || ys, "null targets");
     DT_CHECK_ARG(world >= 1 && world <= DT_MAX_WORLD && rank >= 0 && rank < world,
                  "bad world size / rank");
-    DT_CHECK_ARG(cut_level >= 0 && cut_level <= 24, "cut_level must be in [0, 24]");
+    DT_CHECK_ARG(cut_level >= 0 && cut_level <= 20, "cut_level must be in [0, 20]");
     DT_CHECK_ARG(theta > 0.0, "theta must be > 0");
     shard_plan_kernel<<<1, PLAN_THREADS, 0, (cudaStream_t)stream>>>(
         center, half, start, end, meta, n_src, ys, n_targets, targets_sorted, theta, cut_level,
@@ -749,7 +749,7 @@ extern "C" int dt_shard_plan(const double *center, const double *half, const int
 
 extern "C" size_t dt_shard_rows_bytes(int64_t cut_level, int64_t order, int64_t eval_stride)
 {
-    if (cut_level < 0 || cut_level > 24 || order < 0 || eval_stride < 0)
+    if (cut_level < 0 || cut_level > 20 || order < 0 || eval_stride < 0)
         return 0;
     return ((size_t)1 << cut_level) * (size_t)(order + 1 + eval_stride) * sizeof(double);
 }
@@ -776,7 +776,7 @@ extern "C" int dt_shard_pack(const int64_t *plan, int rank, int64_t cut_level, i
 {
     DT_CHECK_ARG(plan && moments && send, "null pointer");
     DT_CHECK_ARG(rank >= 0 && rank < DT_MAX_WORLD, "bad rank");
-    DT_CHECK_ARG(cut_level >= 0 && cut_level <= 24 && order >= 0, "bad cut level / order");
+    DT_CHECK_ARG(cut_level >= 0 && cut_level <= 20 && order >= 0, "bad cut level / order");
     const int64_t es = moments_eval ? eval_stride : 0;
     DT_CHECK_ARG(!moments_eval || (eval_stride >= order + 1 && eval_stride % 2 == 0),
                  "eval_stride must be even and >= order + 1");
@@ -797,7 +797,7 @@ extern "C" int dt_shard_finish(const int64_t *plan, int world, int64_t cut_level
 {
     DT_CHECK_ARG(plan && recv && center && left && right && meta && moments, "null pointer");
     DT_CHECK_ARG(world >= 1 && world <= DT_MAX_WORLD, "bad world size");
-    DT_CHECK_ARG(cut_level >= 0 && cut_level <= 24, "bad cut level");
+    DT_CHECK_ARG(cut_level >= 0 && cut_level <= 20, "bad cut level");
     DT_CHECK_ARG(order >= 0 && order + 1 <= REG_ORDER, "sharded moments need order <= 31");
     DT_CHECK_ARG(!moments_eval || (eval_stride >= order + 1 && eval_stride % 2 == 0),
                  "eval_stride must be even and >= order + 1");

@@ -100,7 +100,7 @@ def test_sharded_moments_golden_cases(dt, case, world):
     _simulate(dt, system, kernel, cfg, ys, world)
 
 
-@pytest.mark.parametrize("cut", [0, 1, 3, 9, 24])
+@pytest.mark.parametrize("cut", [0, 1, 3, 9, 20])
 def test_sharded_moments_cut_levels(dt, cut):
     g = load_case("cfg2s")
     system = dt.from_particles(np.column_stack([g["xs"], g["qs"]]))
