@@ -42,11 +42,20 @@ namespace {
 #ifndef DT_EVAL_MINB
 #define DT_EVAL_MINB 4
 #endif
-#ifndef DT_EVAL_OVERLAP
-#define DT_EVAL_OVERLAP 0
-#endif
 #ifndef DT_EVAL_THREADS
 #define DT_EVAL_THREADS 256
+#endif
+#ifndef DT_PSEL_BF
+#define DT_PSEL_BF 0  // branch-free order estimate (psel_fast_bf)
+#endif
+#ifndef DT_EVAL_UTIL
+#define DT_EVAL_UTIL 0  // development: lane-utilisation counters (variant builds only)
+#endif
+#if DT_EVAL_UTIL
+__device__ unsigned long long g_util[16];
+#define UTIL_ADD(k, v) u_[k] += (unsigned long long)(v)
+#else
+#define UTIL_ADD(k, v) ((void)0)
 #endif
 constexpr int EVAL_THREADS = DT_EVAL_THREADS;
 constexpr int EVAL_WARPS = EVAL_THREADS / 32;
@@ -226,6 +235,14 @@ __device__ int psel_exact_bracket(double big_r, double h, int t0, const EvalArgs
 
 // MUFU reciprocal (rcp.approx.ftz.f32, ~1 ulp): the order estimate's error
 // budget absorbs it; IEEE division would cost a Newton step and a fixup.
+// double -> float, round to nearest, subnormal results flushed (no fixup code)
+__device__ __forceinline__ float f32_of(double x)
+{
+    float r;
+    asm("cvt.rn.ftz.f32.f64 %0, %1;" : "=f"(r) : "d"(x));
+    return r;
+}
+
 __device__ __forceinline__ float fast_rcp(float x)
 {
     float r;
@@ -255,8 +272,8 @@ __device__ int psel_fast(double big_r, double h, const EvalArgs &a, const float 
 {
     if (h == 0.0)
         return 0;  // value == 0 <= tol at cand 0
-    const float Rf = (float)big_r;
-    const float hf = (float)h;
+    const float Rf = f32_of(big_r);
+    const float hf = f32_of(h);
     const float iR = fast_rcp(Rf);
     const float ratio = hf * iR;
     const float sstar = rd2f * iR * iR;
@@ -322,8 +339,8 @@ __device__ int psel_fast(double big_r, double h, const EvalArgs &a, const float 
 __device__ __forceinline__ int psel_fast_bf(double big_r, double h, const EvalArgs &a,
                                             const float *isig, float rd2f, float inv_tol_f)
 {
-    const float Rf = (float)big_r;
-    const float hf = (float)h;
+    const float Rf = f32_of(big_r);
+    const float hf = f32_of(h);
     const float iR = fast_rcp(Rf);
     const float ratio = hf * iR;
     const float sstar = rd2f * iR * iR;
@@ -460,23 +477,32 @@ __device__ __forceinline__ double far_sum(const FarPre &f, const double2 *__rest
     double acc1 = 0.0;
     int k = 4;
     if (!WIDE) {
-        // orders every far lane of the warp needs (k <= pmin): no masking
+        // orders every far lane of the warp needs (k <= pmin): no masking.
+        // Exits every three orders, so each recurrence value is live at one
+        // exit only and needs no register moves.
+#define DT_FAR_STEP(KK, G3, G2, G1, OUT)                                          \
+    const double OUT = __fma_rn(__fma_rn(a0, c_rcp[(KK) - 1], -ci), G1,           \
+                                __fma_rn(-ir3, G2, -inv * G3));                   \
+    {                                                                             \
+        const double2 mm_ = __ldg(M2 + (KK) / 2);                                 \
+        if ((KK) & 1)                                                             \
+            acc1 = __fma_rn(OUT, mm_.y, acc1);                                    \
+        else                                                                      \
+            acc = __fma_rn(OUT, mm_.x, acc);                                      \
+    }
 #pragma unroll
-        for (int kk = 4; kk < 32; kk += 2) {
-            if (kk + 1 > pmin)
+        for (int kk = 4; kk + 2 <= 31; kk += 3) {
+            if (kk + 2 > pmin)
                 break;
-            const double2 mm = __ldg(M2 + kk / 2);
-            const double pa = __fma_rn(-ir3, gm2, -inv * gm3);
-            const double t = __fma_rn(__fma_rn(a0, c_rcp[kk - 1], -ci), gm1, pa);
-            acc = __fma_rn(t, mm.x, acc);
-            const double pb = __fma_rn(-ir3, gm1, -inv * gm2);
-            const double u = __fma_rn(__fma_rn(a0, c_rcp[kk], -ci), t, pb);
-            acc1 = __fma_rn(u, mm.y, acc1);
-            gm3 = gm1;
-            gm2 = t;
-            gm1 = u;
-            k = kk + 2;
+            DT_FAR_STEP(kk, gm3, gm2, gm1, v0)
+            DT_FAR_STEP(kk + 1, gm2, gm1, v0, v1)
+            DT_FAR_STEP(kk + 2, gm1, v0, v1, v2)
+            gm3 = v0;
+            gm2 = v1;
+            gm1 = v2;
+            k = kk + 3;
         }
+#undef DT_FAR_STEP
     }
     // remaining orders up to the warp maximum, masked per lane; even orders
     // go to acc and odd ones to acc1 on both paths, so a target's result does
@@ -506,11 +532,23 @@ __device__ __forceinline__ double far_field(double d, double rd2, const double2 
     return far_sum<WIDE>(far_setup(d, rd2), M2, pu, pmin, pmax);
 }
 
-__device__ __forceinline__ double near_term(double2 u, double y, double rd2)
+#ifndef DT_NEAR_FMA
+#define DT_NEAR_FMA 0
+#endif
+#if DT_NEAR_FMA
+// acc + q (x - y) / sqrt((x - y)^2 + r_d^2): 9 FP64 instructions + MUFU
+__device__ __forceinline__ double near_term(double2 u, double y, double rd2, double acc)
 {
     const double du = u.x - y;
-    return u.y * du * dt_rsqrt(__fma_rn(du, du, rd2));
+    return __fma_rn(u.y * du, dt_rsqrt(__fma_rn(du, du, rd2)), acc);
 }
+#else
+__device__ __forceinline__ double near_term(double2 u, double y, double rd2, double acc)
+{
+    const double du = u.x - y;
+    return acc + u.y * du * dt_rsqrt(__fma_rn(du, du, rd2));
+}
+#endif
 
 // Leaf sources [s, e): four (x, q) broadcast loads in flight per step.
 __device__ __forceinline__ double near_field(const double2 *__restrict__ xq, int s, int e,
@@ -523,13 +561,13 @@ __device__ __forceinline__ double near_field(const double2 *__restrict__ xq, int
         const double2 u1 = __ldg(xq + j + 1);
         const double2 u2 = __ldg(xq + j + 2);
         const double2 u3 = __ldg(xq + j + 3);
-        a0 += near_term(u0, y, rd2);
-        a1 += near_term(u1, y, rd2);
-        a2 += near_term(u2, y, rd2);
-        a3 += near_term(u3, y, rd2);
+        a0 = near_term(u0, y, rd2, a0);
+        a1 = near_term(u1, y, rd2, a1);
+        a2 = near_term(u2, y, rd2, a2);
+        a3 = near_term(u3, y, rd2, a3);
     }
     for (; j < e; ++j)
-        a0 += near_term(__ldg(xq + j), y, rd2);
+        a0 = near_term(__ldg(xq + j), y, rd2, a0);
     return (a0 + a1) + (a2 + a3);
 }
 
@@ -573,8 +611,12 @@ __global__ void __launch_bounds__(EVAL_THREADS, DT_EVAL_MINB) tree_eval_kernel(E
     const double *cs = tables_in_smem ? cos_s : a.cos_tab;
     const double *sn = tables_in_smem ? sin_s : a.sin_tab;
     const bool fast_ok = a.n_samples == 64 && a.psel_mode == DT_PSEL_FAST;
-    const float rd2f = (float)a.rd2;
-    const float inv_tol_f = (float)(1.0 / a.tol_share);
+    __shared__ float fconst_s[2];
+    if (threadIdx.x == 0) {
+        fconst_s[0] = f32_of(a.rd2);
+        fconst_s[1] = f32_of(1.0 / a.tol_share);
+    }
+    __syncthreads();
 
     while (true) {
         unsigned long long base = 0;
@@ -601,17 +643,21 @@ __global__ void __launch_bounds__(EVAL_THREADS, DT_EVAL_MINB) tree_eval_kernel(E
         uint64_t hh = 0;
         int64_t c_near = 0, c_far = 0, c_sump = 0, c_p0 = 0, c_exact = 0;
 
-        // warp-uniform DFS stack distributed over the lanes' registers:
-        // entry k lives in lane k % 32 (sn0/sm0 for k < 32, sn1/sm1 above)
-        int top = 0;
-        const unsigned vmask = __ballot_sync(DT_FULL, valid);
+        // Warp-uniform DFS (left subtree first, _kernels.py:199-264) over the
+        // union of the 32 targets' traversals, one lane mask per entry.  An
+        // opened node continues directly into its first child; only the
+        // pending right siblings go on the stack, which is distributed over
+        // the lanes' registers: entry k lives in lane k % 32 (sn0/sm0 for
+        // k < 32, sn1/sm1 above; depth <= 60).
+        int top = -1;
+#if DT_EVAL_UTIL
+        unsigned long long u_[12] = {0};
+#endif
         int sn0 = 0, sn1 = 0;
-        unsigned sm0 = lane == 0 ? vmask : 0u, sm1 = 0u;
-        while (top >= 0) {
-            const bool low = top < 32;
-            const int node = __shfl_sync(DT_FULL, low ? sn0 : sn1, top & 31);
-            const unsigned mask = __shfl_sync(DT_FULL, low ? sm0 : sm1, top & 31);
-            --top;
+        unsigned sm0 = 0u, sm1 = 0u;
+        int node = 0;
+        unsigned mask = __ballot_sync(DT_FULL, valid);
+        while (true) {
             const double4 raw0 = *reinterpret_cast<const double4 *>(a.nodes + node);
             const double center = raw0.x, half = raw0.y;
             const int2 lr = make_int2(__double2loint(raw0.z), __double2hiint(raw0.z));
@@ -621,49 +667,20 @@ __global__ void __launch_bounds__(EVAL_THREADS, DT_EVAL_MINB) tree_eval_kernel(E
             const double big_r = fabs(d);
             const bool far = act && big_r > 0.0 && half <= __dmul_rn(a.theta, big_r);
             const unsigned fm = __ballot_sync(DT_FULL, far);
-#if DT_EVAL_OVERLAP
+            UTIL_ADD(0, 1);
             if (fm) {
                 int pu = -1;
-                FarPre fpre;
                 if (far) {
-                    fpre = far_setup(d, a.rd2);
                     if (ADAPTIVE) {
-                        int r = fast_ok ? psel_fast_bf(big_r, half, a, isig_s, rd2f, inv_tol_f)
+#if DT_PSEL_BF
+                        int r = fast_ok ? psel_fast_bf(big_r, half, a, isig_s, fconst_s[0],
+                                                       fconst_s[1])
                                         : -1;
-                        if (r < 0) {
-                            if (r <= -2 && fast_ok)
-                                r = psel_exact_bracket(big_r, half, -r - 2, a, cs, sn);
-                            else
-                                r = psel_exact_all(big_r, half, a, cs, sn);
-                            if (STATS)
-                                ++c_exact;
-                        }
-                        pu = r;
-                    } else {
-                        pu = a.p;
-                    }
-                }
-                const int pmax = __reduce_max_sync(DT_FULL, pu);
-                const int pmin = __reduce_min_sync(DT_FULL, far ? pu : 1 << 20);
-                if (far) {
-                    acc += far_sum<WIDE>(
-                        fpre,
-                        reinterpret_cast<const double2 *>(a.moments + (int64_t)node * a.stride),
-                        pu, pmin, pmax);
-                    if (STATS) {
-                        hh += mix64((uint64_t)node * 256u + (uint64_t)pu);
-                        ++c_far;
-                        c_sump += pu;
-                        c_p0 += pu == 0;
-                    }
-                }
-            }
 #else
-            if (fm) {
-                int pu = -1;
-                if (far) {
-                    if (ADAPTIVE) {
-                        int r = fast_ok ? psel_fast(big_r, half, a, isig_s, rd2f, inv_tol_f) : -1;
+                        int r = fast_ok ? psel_fast(big_r, half, a, isig_s, fconst_s[0],
+                                                    fconst_s[1])
+                                        : -1;
+#endif
                         if (r < 0) {
                             if (r <= -2 && fast_ok)
                                 r = psel_exact_bracket(big_r, half, -r - 2, a, cs, sn);
@@ -679,6 +696,11 @@ __global__ void __launch_bounds__(EVAL_THREADS, DT_EVAL_MINB) tree_eval_kernel(E
                 }
                 const int pmax = __reduce_max_sync(DT_FULL, pu);
                 const int pmin = __reduce_min_sync(DT_FULL, far ? pu : 1 << 20);
+                UTIL_ADD(1, 1);
+                UTIL_ADD(2, __popc(fm));
+                UTIL_ADD(3, pmax);
+                UTIL_ADD(4, __reduce_add_sync(DT_FULL, far ? pu : 0));
+                UTIL_ADD(5, pmin);
                 if (far) {
                     acc += far_field<WIDE>(
                         d, a.rd2,
@@ -692,10 +714,12 @@ __global__ void __launch_bounds__(EVAL_THREADS, DT_EVAL_MINB) tree_eval_kernel(E
                     }
                 }
             }
-#endif
             const unsigned rest = mask & ~fm;
             if (rest) {
                 if (lr.x < 0 && lr.y < 0) {
+                    UTIL_ADD(6, 1);
+                    UTIL_ADD(7, __popc(rest));
+                    UTIL_ADD(8, se.y - se.x);
                     if ((rest >> lane) & 1u) {
                         acc += near_field(a.xq, se.x, se.y, y, a.rd2);
                         if (STATS) {
@@ -704,21 +728,30 @@ __global__ void __launch_bounds__(EVAL_THREADS, DT_EVAL_MINB) tree_eval_kernel(E
                         }
                     }
                 } else {
-                    if (lr.y >= 0) {
+                    if (lr.x >= 0 && lr.y >= 0) {  // right sibling waits on the stack
                         ++top;
                         if (lane == (top & 31)) {
                             if (top < 32) { sn0 = lr.y; sm0 = rest; } else { sn1 = lr.y; sm1 = rest; }
                         }
                     }
-                    if (lr.x >= 0) {
-                        ++top;
-                        if (lane == (top & 31)) {
-                            if (top < 32) { sn0 = lr.x; sm0 = rest; } else { sn1 = lr.x; sm1 = rest; }
-                        }
-                    }
+                    node = lr.x >= 0 ? lr.x : lr.y;
+                    mask = rest;
+                    continue;
                 }
             }
+            if (top < 0)
+                break;
+            const bool low = top < 32;
+            node = __shfl_sync(DT_FULL, low ? sn0 : sn1, top & 31);
+            mask = __shfl_sync(DT_FULL, low ? sm0 : sm1, top & 31);
+            --top;
         }
+#if DT_EVAL_UTIL
+        UTIL_ADD(9, 1);
+        if (lane == 0)
+            for (int k = 0; k < 12; ++k)
+                atomicAdd(g_util + k, u_[k]);
+#endif
         if (valid) {
             a.out[i] = a.accumulate ? a.out[i] + acc : acc;
             if (STATS) {
@@ -1237,6 +1270,19 @@ int launch_eval(EvalArgs &a, bool adaptive, bool stats, cudaStream_t s, void *ws
 }
 
 }  // namespace
+
+#if DT_EVAL_UTIL
+extern "C" int dt_eval_util(unsigned long long *host16, int reset)
+{
+    DT_CUDA_TRY(cudaDeviceSynchronize());
+    DT_CUDA_TRY(cudaMemcpyFromSymbol(host16, g_util, sizeof(g_util)));
+    if (reset) {
+        unsigned long long z[16] = {0};
+        DT_CUDA_TRY(cudaMemcpyToSymbol(g_util, z, sizeof(z)));
+    }
+    return DT_OK;
+}
+#endif
 
 extern "C" int dt_pack_sources(const double *xs, const double *qs, int64_t n, double *xq,
                                void *stream)
