@@ -45,6 +45,9 @@ namespace {
 #ifndef DT_EVAL_THREADS
 #define DT_EVAL_THREADS 256
 #endif
+#ifndef DT_FAR_MASKED_CHUNKS
+#define DT_FAR_MASKED_CHUNKS 0
+#endif
 #ifndef DT_PSEL_BF
 #define DT_PSEL_BF 0  // branch-free order estimate (psel_fast_bf)
 #endif
@@ -235,11 +238,12 @@ __device__ int psel_exact_bracket(double big_r, double h, int t0, const EvalArgs
 
 // MUFU reciprocal (rcp.approx.ftz.f32, ~1 ulp): the order estimate's error
 // budget absorbs it; IEEE division would cost a Newton step and a fixup.
-// double -> float, round to nearest, subnormal results flushed (no fixup code)
+// double -> float, round to nearest (one F2F; a subnormal result is kept and
+// the ftz arithmetic that follows reads it as 0, which the range guards catch)
 __device__ __forceinline__ float f32_of(double x)
 {
     float r;
-    asm("cvt.rn.ftz.f32.f64 %0, %1;" : "=f"(r) : "d"(x));
+    asm("cvt.rn.f32.f64 %0, %1;" : "=f"(r) : "d"(x));
     return r;
 }
 
@@ -490,6 +494,33 @@ __device__ __forceinline__ double far_sum(const FarPre &f, const double2 *__rest
         else                                                                      \
             acc = __fma_rn(OUT, mm_.x, acc);                                      \
     }
+#if DT_FAR_MASKED_CHUNKS
+        // one loop to the warp maximum: orders above a lane's own pu are
+        // computed but not accumulated (predicated FMA)
+#define DT_FAR_MSTEP(KK, G3, G2, G1, OUT)                                         \
+    const double OUT = __fma_rn(__fma_rn(a0, c_rcp[(KK) - 1], -ci), G1,           \
+                                __fma_rn(-ir3, G2, -inv * G3));                   \
+    if ((KK) <= pu) {                                                             \
+        const double2 mm_ = __ldg(M2 + (KK) / 2);                                 \
+        if ((KK) & 1)                                                             \
+            acc1 = __fma_rn(OUT, mm_.y, acc1);                                    \
+        else                                                                      \
+            acc = __fma_rn(OUT, mm_.x, acc);                                      \
+    }
+#pragma unroll
+        for (int kk = 4; kk + 2 <= 31; kk += 3) {
+            if (kk > pmax)
+                break;
+            DT_FAR_MSTEP(kk, gm3, gm2, gm1, v0)
+            DT_FAR_MSTEP(kk + 1, gm2, gm1, v0, v1)
+            DT_FAR_MSTEP(kk + 2, gm1, v0, v1, v2)
+            gm3 = v0;
+            gm2 = v1;
+            gm1 = v2;
+            k = kk + 3;
+        }
+#undef DT_FAR_MSTEP
+#else
 #pragma unroll
         for (int kk = 4; kk + 2 <= 31; kk += 3) {
             if (kk + 2 > pmin)
@@ -502,6 +533,7 @@ __device__ __forceinline__ double far_sum(const FarPre &f, const double2 *__rest
             gm1 = v2;
             k = kk + 3;
         }
+#endif
 #undef DT_FAR_STEP
     }
     // remaining orders up to the warp maximum, masked per lane; even orders
@@ -587,6 +619,7 @@ __global__ void __launch_bounds__(EVAL_THREADS, DT_EVAL_MINB) tree_eval_kernel(E
         a.tol_share = tol_share_of(a);
     __shared__ float isig_s[35];
     __shared__ double cos_s[MAX_SAMPLES], sin_s[MAX_SAMPLES];
+    __shared__ uint2 stack_s[EVAL_WARPS][DT_MAX_DEPTH + 4];
     const int lane = dt_lane();
     const bool tables_in_smem = a.n_samples <= MAX_SAMPLES;
     if (ADAPTIVE) {
@@ -646,15 +679,14 @@ __global__ void __launch_bounds__(EVAL_THREADS, DT_EVAL_MINB) tree_eval_kernel(E
         // Warp-uniform DFS (left subtree first, _kernels.py:199-264) over the
         // union of the 32 targets' traversals, one lane mask per entry.  An
         // opened node continues directly into its first child; only the
-        // pending right siblings go on the stack, which is distributed over
-        // the lanes' registers: entry k lives in lane k % 32 (sn0/sm0 for
-        // k < 32, sn1/sm1 above; depth <= 60).
+        // pending right siblings go on the warp's stack in shared memory
+        // (depth <= 60).  Every lane stores the same entry and reads back
+        // its own store, so no warp barrier is needed.
         int top = -1;
 #if DT_EVAL_UTIL
         unsigned long long u_[12] = {0};
 #endif
-        int sn0 = 0, sn1 = 0;
-        unsigned sm0 = 0u, sm1 = 0u;
+        uint2 *const stk = stack_s[threadIdx.x >> 5];
         int node = 0;
         unsigned mask = __ballot_sync(DT_FULL, valid);
         while (true) {
@@ -728,12 +760,8 @@ __global__ void __launch_bounds__(EVAL_THREADS, DT_EVAL_MINB) tree_eval_kernel(E
                         }
                     }
                 } else {
-                    if (lr.x >= 0 && lr.y >= 0) {  // right sibling waits on the stack
-                        ++top;
-                        if (lane == (top & 31)) {
-                            if (top < 32) { sn0 = lr.y; sm0 = rest; } else { sn1 = lr.y; sm1 = rest; }
-                        }
-                    }
+                    if (lr.x >= 0 && lr.y >= 0)  // right sibling waits on the stack
+                        stk[++top] = make_uint2((unsigned)lr.y, rest);
                     node = lr.x >= 0 ? lr.x : lr.y;
                     mask = rest;
                     continue;
@@ -741,10 +769,9 @@ __global__ void __launch_bounds__(EVAL_THREADS, DT_EVAL_MINB) tree_eval_kernel(E
             }
             if (top < 0)
                 break;
-            const bool low = top < 32;
-            node = __shfl_sync(DT_FULL, low ? sn0 : sn1, top & 31);
-            mask = __shfl_sync(DT_FULL, low ? sm0 : sm1, top & 31);
-            --top;
+            const uint2 e = stk[top--];
+            node = (int)e.x;
+            mask = e.y;
         }
 #if DT_EVAL_UTIL
         UTIL_ADD(9, 1);
