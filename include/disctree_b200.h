@@ -199,13 +199,14 @@ int dt_pack_tree(const double *centers, const double *halves, const int64_t *sta
                  const int64_t *ends, const int64_t *lefts, const int64_t *rights,
                  int64_t n_nodes, void *packed, void *stream);
 
-/* Workspace of dt_tree_phi_sum (packed copies + counter).  Any entry's
- * workspace may be enlarged by dt_tree_eval_items_workspace(i1 - i0) bytes
- * (appended) to enable the two-phase path: a walk kernel that sums the near
- * field and lists far interactions, then a far kernel that evaluates two list
- * items at a time; without it a single fused traversal kernel runs. */
+/* Task-counter slot of the traversal (the workspace of the *_packed and
+ * *_device evaluators must hold at least this many bytes; zeroed by the
+ * call, stream-ordered).  Warps take 32-target tasks from per-SM segments
+ * of the target range, so neighbouring targets run on the same SM. */
+#define DT_EVAL_COUNTER_BYTES 1024
+
+/* Workspace of dt_tree_phi_sum (packed copies + the counter slot). */
 size_t dt_tree_eval_workspace(int64_t n_nodes, int64_t n_src, int64_t moment_stride);
-size_t dt_tree_eval_items_workspace(int64_t n_targets);
 
 /* Mirror of the numba seam _kernels.tree_phi_sum (_kernels.py:163-266):
  * far-field/near-field traversal for targets ys[i0:i1]; writes out[i0:i1]

@@ -26,6 +26,7 @@ DT_META_LEAVES = 2
 DT_META_OVERFLOW = 3
 DT_META_LEVEL0 = 8
 DT_META_WORDS = 72
+DT_EVAL_COUNTER_BYTES = 1024
 DT_MAX_WORLD = 64
 DT_PLAN_CUT = 0
 DT_PLAN_LEVEL_BEGIN = 1
@@ -89,7 +90,6 @@ SIGNATURES = {
     "dt_pack_sources": (C.c_int, [_P, _P, _I64, _P, _P]),
     "dt_pack_tree": (C.c_int, [_P, _P, _P, _P, _P, _P, _I64, _P, _P]),
     "dt_tree_eval_workspace": (_SZ, [_I64, _I64, _I64]),
-    "dt_tree_eval_items_workspace": (_SZ, [_I64]),
     "dt_tree_phi_sum": (
         C.c_int,
         [_P, _P, _P, _P, _P, _P, _P, _I64, _I64, _P, _P, _I64, _D, _D, _I64, C.c_int, _D,

@@ -68,6 +68,13 @@ __device__ __forceinline__ double dt_rcp(double x)
 
 __device__ __forceinline__ int dt_lane() { return threadIdx.x & (DT_WARP - 1); }
 
+__device__ __forceinline__ unsigned dt_smid()
+{
+    unsigned r;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+    return r;
+}
+
 __device__ __forceinline__ double dt_shfl(double v, int src)
 {
     return __shfl_sync(DT_FULL, v, src);

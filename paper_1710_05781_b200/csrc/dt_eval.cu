@@ -45,6 +45,10 @@ namespace {
 #ifndef DT_EVAL_THREADS
 #define DT_EVAL_THREADS 256
 #endif
+#ifndef DT_EVAL_SEGMENTS
+#define DT_EVAL_SEGMENTS 148  // per-SM task segments (0: one global counter)
+#endif
+static_assert(DT_EVAL_SEGMENTS * 4 <= DT_EVAL_COUNTER_BYTES, "counter slot too small");
 #ifndef DT_FAR_MASKED_CHUNKS
 #define DT_FAR_MASKED_CHUNKS 0
 #endif
@@ -87,8 +91,6 @@ struct EvalArgs {
     unsigned long long *counter;
     const int64_t *meta;  // if set: tol_share = tolerance / (3 max(depth, 1)) on device
     double tolerance;
-    const int32_t *task_list;                  // fused kernel: only these 32-target tasks
-    const unsigned long long *task_count;      // (device count of task_list)
 };
 
 // tree.py:268-270 _tol_share, evaluated from the device-side tree depth.
@@ -651,20 +653,38 @@ __global__ void __launch_bounds__(EVAL_THREADS, DT_EVAL_MINB) tree_eval_kernel(E
     }
     __syncthreads();
 
+#if DT_EVAL_SEGMENTS
+    // Locality-aware scheduling: the 32-target tasks are split into
+    // DT_EVAL_SEGMENTS contiguous segments; an SM's warps drain the segment
+    // of their SM id first (neighbouring targets share nodes and moment rows
+    // in L1), then move on to the following segments.
+    const int64_t n_tasks = (a.i1 - a.i0 + 31) / 32;
+    unsigned *const seg_ctr = reinterpret_cast<unsigned *>(a.counter);
+    int seg = (int)(dt_smid() % DT_EVAL_SEGMENTS);
+    int seg_left = DT_EVAL_SEGMENTS;
+#endif
     while (true) {
         unsigned long long base = 0;
-        if (a.task_list) {
-            long long k = 0;
+        {
+#if DT_EVAL_SEGMENTS
+            const int64_t s0 = n_tasks * seg / DT_EVAL_SEGMENTS;
+            const int64_t s1 = n_tasks * (seg + 1) / DT_EVAL_SEGMENTS;
+            unsigned t = 0;
             if (lane == 0)
-                k = (long long)atomicAdd(a.counter, 1ull);
-            k = __shfl_sync(DT_FULL, k, 0);
-            if (k >= (long long)*a.task_count)
-                break;
-            base = (unsigned long long)a.task_list[k] * 32ull;
-        } else {
+                t = atomicAdd(seg_ctr + seg, 1u);
+            t = __shfl_sync(DT_FULL, t, 0);
+            if ((int64_t)t >= s1 - s0) {
+                if (--seg_left == 0)
+                    break;
+                seg = seg + 1 == DT_EVAL_SEGMENTS ? 0 : seg + 1;
+                continue;
+            }
+            base = (unsigned long long)(s0 + t) * 32ull;
+#else
             if (lane == 0)
                 base = atomicAdd(a.counter, 32ull);
             base = __shfl_sync(DT_FULL, base, 0);
+#endif
         }
         const int64_t i_first = a.i0 + (int64_t)base;
         if (i_first >= a.i1)
@@ -799,334 +819,7 @@ __global__ void __launch_bounds__(EVAL_THREADS, DT_EVAL_MINB) tree_eval_kernel(E
     }
 }
 
-// ------------------------------------------------------------------ two-phase path
-//
-// Phase 1 (walk): the warp-coherent DFS of the fused kernel with the MAC
-// only.  Near leaves are summed on the spot; every accepted (far) node is
-// appended to the warp's item list as (node, lane mask) in DFS order.
-// Phase 2 (far): a warp re-takes its 32 targets, reads the item list and,
-// two items at a time (two independent FP64 chains per lane), selects each
-// far lane's order and evaluates the expansion.  The walk carries no far
-// code and the far pass no traversal, so each kernel keeps its registers
-// for its own latency hiding.  Items per 32-target task are capped
-// (ITEM_CAP); a task over the cap is re-evaluated by the fused kernel.
-
-constexpr int ITEM_CAP = 192;
-
-struct PhaseWs {
-    unsigned long long *ctr;  // [0] walk tasks, [1] far tasks, [2] overflow count, [3] fixup
-    int32_t *count;           // items per task (-1: overflow)
-    int32_t *ovf;             // overflowed task ids
-    int2 *items;              // [task][ITEM_CAP] (node, lane mask)
-};
-
-__device__ __forceinline__ PhaseWs phase_ws(void *ws, int64_t tasks)
-{
-    PhaseWs w;
-    char *p = (char *)ws;
-    w.ctr = (unsigned long long *)p;
-    w.count = (int32_t *)(p + 256);
-    w.ovf = w.count + tasks;
-    const size_t off = (256 + (size_t)tasks * 8 + 15) & ~(size_t)15;
-    w.items = (int2 *)(p + off);
-    return w;
-}
-
-static size_t phase_ws_bytes(int64_t tasks)
-{
-    return ((256 + (size_t)tasks * 8 + 15) & ~(size_t)15) + (size_t)tasks * ITEM_CAP * sizeof(int2);
-}
-
-template <bool STATS>
-__global__ void __launch_bounds__(256, 4) tree_walk_kernel(EvalArgs a, void *wsp, int64_t tasks)
-{
-    const PhaseWs w = phase_ws(wsp, tasks);
-    const int lane = dt_lane();
-    while (true) {
-        unsigned long long base = 0;
-        if (lane == 0)
-            base = atomicAdd(w.ctr + 0, 32ull);
-        base = __shfl_sync(DT_FULL, base, 0);
-        const int64_t i_first = a.i0 + (int64_t)base;
-        if (i_first >= a.i1)
-            break;
-        const int64_t task = (int64_t)base / 32;
-        int2 *items = w.items + task * ITEM_CAP;
-        const int64_t i = i_first + lane;
-        const bool valid = i < a.i1;
-        const double y = valid ? __ldg(a.ys + i) : 0.0;
-        double acc = 0.0;
-        uint64_t hh = 0;
-        int64_t c_near = 0;
-        int cnt = 0;
-        int top = 0;
-        const unsigned vmask = __ballot_sync(DT_FULL, valid);
-        int sn0 = 0, sn1 = 0;
-        unsigned sm0 = lane == 0 ? vmask : 0u, sm1 = 0u;
-        while (top >= 0) {
-            const bool low = top < 32;
-            const int node = __shfl_sync(DT_FULL, low ? sn0 : sn1, top & 31);
-            const unsigned mask = __shfl_sync(DT_FULL, low ? sm0 : sm1, top & 31);
-            --top;
-            const double4 raw0 = *reinterpret_cast<const double4 *>(a.nodes + node);
-            const double center = raw0.x, half = raw0.y;
-            const int2 lr = make_int2(__double2loint(raw0.z), __double2hiint(raw0.z));
-            const int2 se = make_int2(__double2loint(raw0.w), __double2hiint(raw0.w));
-            const double big_r = fabs(center - y);
-            const bool far =
-                ((mask >> lane) & 1u) && big_r > 0.0 && half <= __dmul_rn(a.theta, big_r);
-            const unsigned fm = __ballot_sync(DT_FULL, far);
-            if (fm) {
-                if (lane == 0 && cnt < ITEM_CAP)
-                    items[cnt] = make_int2(node, (int)fm);
-                ++cnt;
-            }
-            const unsigned rest = mask & ~fm;
-            if (rest) {
-                if (lr.x < 0 && lr.y < 0) {
-                    if ((rest >> lane) & 1u) {
-                        acc += near_field(a.xq, se.x, se.y, y, a.rd2);
-                        if (STATS) {
-                            hh += mix64((uint64_t)node * 256u + 255u);
-                            c_near += se.y - se.x;
-                        }
-                    }
-                } else {
-                    if (lr.y >= 0) {
-                        ++top;
-                        if (lane == (top & 31)) {
-                            if (top < 32) { sn0 = lr.y; sm0 = rest; } else { sn1 = lr.y; sm1 = rest; }
-                        }
-                    }
-                    if (lr.x >= 0) {
-                        ++top;
-                        if (lane == (top & 31)) {
-                            if (top < 32) { sn0 = lr.x; sm0 = rest; } else { sn1 = lr.x; sm1 = rest; }
-                        }
-                    }
-                }
-            }
-        }
-        if (cnt > ITEM_CAP) {
-            // the fused kernel redoes this task from scratch
-            if (lane == 0) {
-                w.count[task] = -1;
-                const unsigned long long k = atomicAdd(w.ctr + 2, 1ull);
-                w.ovf[k] = (int32_t)task;
-            }
-            continue;
-        }
-        if (lane == 0)
-            w.count[task] = cnt;
-        if (valid) {
-            a.out[i] = a.accumulate ? a.out[i] + acc : acc;
-            if (STATS) {
-                if (a.stats.hash)
-                    a.stats.hash[i] = hh;
-                if (a.stats.near_pairs)
-                    a.stats.near_pairs[i] = c_near;
-                if (a.stats.n_far)
-                    a.stats.n_far[i] = 0;
-                if (a.stats.sum_p)
-                    a.stats.sum_p[i] = 0;
-                if (a.stats.n_p0)
-                    a.stats.n_p0[i] = 0;
-                if (a.stats.n_exact)
-                    a.stats.n_exact[i] = 0;
-            }
-        }
-    }
-}
-
-// Two far items of one target lane, interleaved (independent chains).
-__device__ __forceinline__ void far_pair(double dA, double dB, double rd2,
-                                         const double2 *__restrict__ MA,
-                                         const double2 *__restrict__ MB, int puA, int puB,
-                                         int pminA, int pmaxA, int pminB, int pmaxB,
-                                         double &outA, double &outB)
-{
-    const double s2A = __fma_rn(dA, dA, rd2), s2B = __fma_rn(dB, dB, rd2);
-    const double rA = dt_rsqrt(s2A), rB = dt_rsqrt(s2B);
-    const double ir2A = rA * rA, ir2B = rB * rB;
-    const double g0A = dA * rA, g0B = dB * rB;
-    const double g1A = rd2 * rA * ir2A, g1B = rd2 * rB * ir2B;
-    const double invA = ir2A * dt_rcp(dA), invB = ir2B * dt_rcp(dB);
-    const double a0A = rd2 * invA, a0B = rd2 * invB;
-    const double ciA = __fma_rn(3.0 * dA, dA, rd2) * invA, ciB = __fma_rn(3.0 * dB, dB, rd2) * invB;
-    const double ir3A = 3.0 * ir2A, ir3B = 3.0 * ir2B;
-    const double g2A = (a0A - ciA) * g1A, g2B = (a0B - ciB) * g1B;
-    const double g3A = __fma_rn(-ir3A, g1A, __fma_rn(a0A, 0.5, -ciA) * g2A);
-    const double g3B = __fma_rn(-ir3B, g1B, __fma_rn(a0B, 0.5, -ciB) * g2B);
-    const double2 mA01 = __ldg(MA), mA23 = __ldg(MA + 1);
-    const double2 mB01 = __ldg(MB), mB23 = __ldg(MB + 1);
-    double accA = g0A * mA01.x, accB = g0B * mB01.x;
-    if (puA >= 1) accA = __fma_rn(g1A, mA01.y, accA);
-    if (puA >= 2) accA = __fma_rn(g2A, mA23.x, accA);
-    if (puA >= 3) accA = __fma_rn(g3A, mA23.y, accA);
-    if (puB >= 1) accB = __fma_rn(g1B, mB01.y, accB);
-    if (puB >= 2) accB = __fma_rn(g2B, mB23.x, accB);
-    if (puB >= 3) accB = __fma_rn(g3B, mB23.y, accB);
-    double pA3 = g1A, pA2 = g2A, pA1 = g3A;
-    double pB3 = g1B, pB2 = g2B, pB1 = g3B;
-    const double *A = reinterpret_cast<const double *>(MA);
-    const double *B = reinterpret_cast<const double *>(MB);
-    // One fully unrolled pass to the larger warp maximum; each lane keeps
-    // order k of a chain only while k <= its own p (select).  Every exit
-    // leaves the loop for the return, so no state is copied between
-    // unrolled steps (pmin is not needed here).
-    (void)pminA;
-    (void)pminB;
-    const int pm = max(pmaxA, pmaxB);
-#pragma unroll
-    for (int kk = 4; kk < 32; ++kk) {
-        if (kk > pm)
-            break;
-        const double mAk = __ldg(A + kk), mBk = __ldg(B + kk);
-        const double tA = __fma_rn(__fma_rn(a0A, c_rcp[kk - 1], -ciA), pA1,
-                                   __fma_rn(-ir3A, pA2, -invA * pA3));
-        const double tB = __fma_rn(__fma_rn(a0B, c_rcp[kk - 1], -ciB), pB1,
-                                   __fma_rn(-ir3B, pB2, -invB * pB3));
-        const double nA = __fma_rn(tA, mAk, accA), nB = __fma_rn(tB, mBk, accB);
-        accA = kk <= puA ? nA : accA;
-        accB = kk <= puB ? nB : accB;
-        pA3 = pA2; pA2 = pA1; pA1 = tA;
-        pB3 = pB2; pB2 = pB1; pB1 = tB;
-    }
-    outA = accA;
-    outB = accB;
-}
-
-template <bool ADAPTIVE, bool STATS>
-__global__ void __launch_bounds__(256, 3) tree_far_kernel(EvalArgs a, void *wsp, int64_t tasks)
-{
-    if (ADAPTIVE)
-        a.tol_share = tol_share_of(a);
-    __shared__ float isig_s[35];
-    __shared__ double cos_s[MAX_SAMPLES], sin_s[MAX_SAMPLES];
-    const PhaseWs w = phase_ws(wsp, tasks);
-    const int lane = dt_lane();
-    const bool tables_in_smem = a.n_samples <= MAX_SAMPLES;
-    if (ADAPTIVE) {
-        if (tables_in_smem) {
-            for (int t = threadIdx.x; t < a.n_samples; t += blockDim.x) {
-                cos_s[t] = a.cos_tab[t];
-                sin_s[t] = a.sin_tab[t];
-            }
-        }
-        if (threadIdx.x <= 32) {
-            int t = threadIdx.x;
-            double c = a.n_samples == 64 ? a.cos_tab[t] : 1.0;
-            double s = a.n_samples == 64 ? a.sin_tab[t] : 0.0;
-            double sig = (c - 1.0) * (c - 1.0) + s * s;
-            isig_s[t] = sig > 0.0 ? (float)(1.0 / sig) : 3.0e38f;
-            if (t == 1)
-                isig_s[34] = (float)sig;
-        }
-        __syncthreads();
-    }
-    const double *cs = tables_in_smem ? cos_s : a.cos_tab;
-    const double *sn = tables_in_smem ? sin_s : a.sin_tab;
-    const bool fast_ok = a.n_samples == 64 && a.psel_mode == DT_PSEL_FAST;
-    const float rd2f = (float)a.rd2;
-    const float inv_tol_f = (float)(1.0 / a.tol_share);
-    while (true) {
-        unsigned long long base = 0;
-        if (lane == 0)
-            base = atomicAdd(w.ctr + 1, 32ull);
-        base = __shfl_sync(DT_FULL, base, 0);
-        const int64_t i_first = a.i0 + (int64_t)base;
-        if (i_first >= a.i1)
-            break;
-        const int64_t task = (int64_t)base / 32;
-        const int cnt = __ldg(w.count + task);
-        if (cnt <= 0)
-            continue;  // nothing far, or overflow (the fused fixup owns it)
-        const int2 *items = w.items + task * ITEM_CAP;
-        const int64_t i = i_first + lane;
-        const bool valid = i < a.i1;
-        const double y = valid ? __ldg(a.ys + i) : 0.0;
-        double acc = 0.0;
-        uint64_t hh = 0;
-        int64_t c_far = 0, c_sump = 0, c_p0 = 0, c_exact = 0;
-        for (int it = 0; it < cnt; it += 2) {
-            const int2 iA = __ldg(items + it);
-            const bool hasB = it + 1 < cnt;
-            const int2 iB = hasB ? __ldg(items + it + 1) : make_int2(iA.x, 0);
-            const double2 chA = __ldg(reinterpret_cast<const double2 *>(a.nodes + iA.x));
-            const double2 chB = __ldg(reinterpret_cast<const double2 *>(a.nodes + iB.x));
-            const bool fA = ((unsigned)iA.y >> lane) & 1u, fB = ((unsigned)iB.y >> lane) & 1u;
-            const double dA = chA.x - y, dB = chB.x - y;
-            int pA = -1, pB = -1;
-            if (ADAPTIVE) {
-                if (fA) {
-                    int r = fast_ok ? psel_fast(fabs(dA), chA.y, a, isig_s, rd2f, inv_tol_f) : -1;
-                    if (r < 0) {
-                        r = (r <= -2 && fast_ok)
-                                ? psel_exact_bracket(fabs(dA), chA.y, -r - 2, a, cs, sn)
-                                : psel_exact_all(fabs(dA), chA.y, a, cs, sn);
-                        ++c_exact;
-                    }
-                    pA = r;
-                }
-                if (fB) {
-                    int r = fast_ok ? psel_fast(fabs(dB), chB.y, a, isig_s, rd2f, inv_tol_f) : -1;
-                    if (r < 0) {
-                        r = (r <= -2 && fast_ok)
-                                ? psel_exact_bracket(fabs(dB), chB.y, -r - 2, a, cs, sn)
-                                : psel_exact_all(fabs(dB), chB.y, a, cs, sn);
-                        ++c_exact;
-                    }
-                    pB = r;
-                }
-            } else {
-                pA = fA ? a.p : -1;
-                pB = fB ? a.p : -1;
-            }
-            const int pmaxA = __reduce_max_sync(DT_FULL, pA);
-            const int pminA = __reduce_min_sync(DT_FULL, fA ? pA : 1 << 20);
-            const int pmaxB = __reduce_max_sync(DT_FULL, pB);
-            const int pminB = __reduce_min_sync(DT_FULL, fB ? pB : 1 << 20);
-            double oA, oB;
-            far_pair(dA, fB ? dB : dA, a.rd2,
-                     reinterpret_cast<const double2 *>(a.moments + (int64_t)iA.x * a.stride),
-                     reinterpret_cast<const double2 *>(a.moments + (int64_t)iB.x * a.stride),
-                     pA, pB, pminA, pmaxA, pminB, pmaxB, oA, oB);
-            if (fA)
-                acc += oA;
-            if (fB)
-                acc += oB;
-            if (STATS) {
-                if (fA) {
-                    hh += mix64((uint64_t)iA.x * 256u + (uint64_t)pA);
-                    ++c_far;
-                    c_sump += pA;
-                    c_p0 += pA == 0;
-                }
-                if (fB) {
-                    hh += mix64((uint64_t)iB.x * 256u + (uint64_t)pB);
-                    ++c_far;
-                    c_sump += pB;
-                    c_p0 += pB == 0;
-                }
-            }
-        }
-        if (valid) {
-            a.out[i] += acc;
-            if (STATS) {
-                if (a.stats.hash)
-                    a.stats.hash[i] += hh;
-                if (a.stats.n_far)
-                    a.stats.n_far[i] = c_far;
-                if (a.stats.sum_p)
-                    a.stats.sum_p[i] = c_sump;
-                if (a.stats.n_p0)
-                    a.stats.n_p0[i] = c_p0;
-                if (a.stats.n_exact)
-                    a.stats.n_exact[i] = c_exact;
-            }
-        }
-    }
-}
+// ------------------------------------------------------------------ packing, tests
 
 __global__ void pack_tree_kernel(const double *__restrict__ c, const double *__restrict__ h,
                                  const int64_t *__restrict__ s, const int64_t *__restrict__ e,
@@ -1244,55 +937,11 @@ int launch_fused(EvalArgs &a, bool adaptive, bool stats, cudaStream_t s, int64_t
     return DT_OK;
 }
 
-// The two-phase path is correct and tested but slower than the fused kernel
-// on B200 in round 1 (18.3 vs 17.0 ms at configs[2]); opt in with
-// DISCTREE_EVAL_TWOPHASE=1.
-static bool two_phase_enabled()
+// a.counter: the DT_EVAL_COUNTER_BYTES task-counter slot at the start of the
+// caller's workspace (zeroed here, stream-ordered).
+int launch_eval(EvalArgs &a, bool adaptive, bool stats, cudaStream_t s)
 {
-    static int v = -1;
-    if (v < 0) {
-        const char *e = getenv("DISCTREE_EVAL_TWOPHASE");
-        v = (e && e[0] == '1') ? 1 : 0;
-    }
-    return v == 1;
-}
-
-// ws/ws_bytes: the caller's workspace; the two-phase path runs when it holds
-// the item lists (dt_tree_eval_items_workspace), the fused kernel otherwise.
-int launch_eval(EvalArgs &a, bool adaptive, bool stats, cudaStream_t s, void *ws = nullptr,
-                size_t ws_bytes = 0)
-{
-    const int64_t tasks = (a.i1 - a.i0 + 31) / 32;
-    if (a.stride <= 32 && ws && ws_bytes >= phase_ws_bytes(tasks) && two_phase_enabled()) {
-        DT_CUDA_TRY(cudaMemsetAsync(ws, 0, 64, s));
-        const int sms = dt_num_sms();
-        void *args[] = {&a, &ws, (void *)&tasks};
-        const void *walk = stats ? (const void *)tree_walk_kernel<true>
-                                 : (const void *)tree_walk_kernel<false>;
-        int per_sm = 0;
-        DT_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, walk, 256, 0));
-        int64_t grid = (int64_t)sms * (per_sm > 0 ? per_sm : 1);
-        grid = std::min<int64_t>(grid, (tasks + 7) / 8);
-        DT_CUDA_TRY(cudaLaunchKernel(walk, dim3((unsigned)std::max<int64_t>(grid, 1)), dim3(256),
-                                     args, 0, s));
-        const void *far = adaptive ? (stats ? (const void *)tree_far_kernel<true, true>
-                                            : (const void *)tree_far_kernel<true, false>)
-                                   : (stats ? (const void *)tree_far_kernel<false, true>
-                                            : (const void *)tree_far_kernel<false, false>);
-        DT_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, far, 256, 0));
-        grid = (int64_t)sms * (per_sm > 0 ? per_sm : 1);
-        grid = std::min<int64_t>(grid, (tasks + 7) / 8);
-        DT_CUDA_TRY(cudaLaunchKernel(far, dim3((unsigned)std::max<int64_t>(grid, 1)), dim3(256),
-                                     args, 0, s));
-        // tasks whose item list overflowed: fused kernel over that list
-        char *p = (char *)ws;
-        EvalArgs f = a;
-        f.counter = (unsigned long long *)p + 3;
-        f.task_count = (const unsigned long long *)p + 2;
-        f.task_list = (const int32_t *)(p + 256) + tasks;
-        return launch_fused(f, adaptive, stats, s, dt_num_sms());
-    }
-    DT_CUDA_TRY(cudaMemsetAsync(a.counter, 0, sizeof(unsigned long long), s));
+    DT_CUDA_TRY(cudaMemsetAsync(a.counter, 0, DT_EVAL_COUNTER_BYTES, s));
     return launch_fused(a, adaptive, stats, s, 0);
 }
 
@@ -1340,23 +989,17 @@ extern "C" int dt_pack_tree(const double *centers, const double *halves, const i
 
 static inline int64_t even_stride(int64_t stride) { return (stride + 1) & ~(int64_t)1; }
 
-extern "C" size_t dt_tree_eval_items_workspace(int64_t n_targets)
-{
-    return 256 + phase_ws_bytes((n_targets + 31) / 32);
-}
-
 static size_t mirror_prefix_bytes(int64_t n_nodes, int64_t n_src, int64_t moment_stride)
 {
     size_t b = 256 + (size_t)n_nodes * sizeof(dt_node) + (size_t)n_src * 2 * sizeof(double) +
                (size_t)n_nodes * even_stride(moment_stride) * sizeof(double);
-    return ((b + 255) & ~(size_t)255) + 256;  // + the eval counter slot
+    return (b + 255) & ~(size_t)255;
 }
 
 extern "C" size_t dt_tree_eval_workspace(int64_t n_nodes, int64_t n_src, int64_t moment_stride)
 {
-    // packed copies for the seam mirror; item lists (two-phase path) are
-    // optional extra bytes: dt_tree_eval_items_workspace(n_targets)
-    return mirror_prefix_bytes(n_nodes, n_src, moment_stride);
+    // packed copies for the seam mirror, then the task-counter slot
+    return mirror_prefix_bytes(n_nodes, n_src, moment_stride) + DT_EVAL_COUNTER_BYTES;
 }
 
 static int check_eval_args(int64_t n_nodes, int64_t n_src, int64_t p, int adaptive,
@@ -1395,7 +1038,7 @@ extern "C" int dt_tree_phi_sum_packed(const void *packed_nodes, int64_t n_nodes,
         return DT_OK;
     DT_CHECK_ARG(packed_nodes && moments && ys && out && (n_src == 0 || xq), "null pointer");
     DT_CHECK_ARG(!adaptive || (cos_tab && sin_tab), "null contour tables");
-    if (!workspace || workspace_bytes < 64)
+    if (!workspace || workspace_bytes < DT_EVAL_COUNTER_BYTES)
         return dt_set_error(DT_ERR_WORKSPACE, "eval workspace too small");
     EvalArgs a{};
     a.nodes = (const dt_node *)packed_nodes;
@@ -1422,9 +1065,7 @@ extern "C" int dt_tree_phi_sum_packed(const void *packed_nodes, int64_t n_nodes,
     else
         a.stats = dt_eval_stats{nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
     a.counter = (unsigned long long *)workspace;
-    return launch_eval(a, adaptive != 0, stats != nullptr, (cudaStream_t)stream,
-                       workspace_bytes >= 512 ? (char *)workspace + 256 : nullptr,
-                       workspace_bytes >= 512 ? workspace_bytes - 256 : 0);
+    return launch_eval(a, adaptive != 0, stats != nullptr, (cudaStream_t)stream);
 }
 
 extern "C" int dt_tree_eval_device(const void *packed_nodes, const int64_t *meta,
@@ -1445,7 +1086,7 @@ extern "C" int dt_tree_eval_device(const void *packed_nodes, const int64_t *meta
         return DT_OK;
     DT_CHECK_ARG(packed_nodes && moments && ys && out && (n_src == 0 || xq), "null pointer");
     DT_CHECK_ARG(!adaptive || (cos_tab && sin_tab), "null contour tables");
-    if (!workspace || workspace_bytes < 64)
+    if (!workspace || workspace_bytes < DT_EVAL_COUNTER_BYTES)
         return dt_set_error(DT_ERR_WORKSPACE, "eval workspace too small");
     EvalArgs a{};
     a.nodes = (const dt_node *)packed_nodes;
@@ -1471,9 +1112,7 @@ extern "C" int dt_tree_eval_device(const void *packed_nodes, const int64_t *meta
     a.psel_mode = DT_PSEL_FAST;
     a.stats = dt_eval_stats{nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
     a.counter = (unsigned long long *)workspace;
-    return launch_eval(a, adaptive != 0, false, (cudaStream_t)stream,
-                       workspace_bytes >= 512 ? (char *)workspace + 256 : nullptr,
-                       workspace_bytes >= 512 ? workspace_bytes - 256 : 0);
+    return launch_eval(a, adaptive != 0, false, (cudaStream_t)stream);
 }
 
 extern "C" int dt_tree_phi_sum(const double *centers, const double *halves, const int64_t *starts,
@@ -1510,11 +1149,10 @@ extern "C" int dt_tree_phi_sum(const double *centers, const double *halves, cons
         moments, moment_stride, n_nodes, meval, estride);
     DT_CUDA_TRY(cudaGetLastError());
     const size_t pre = mirror_prefix_bytes(n_nodes, n_src, moment_stride);
-    char *eval_ws = ws + pre - 256;  // counter slot + optional item lists after the copies
     return dt_tree_phi_sum_packed(packed, n_nodes, meval, estride, xq, n_src, rd2, theta, p,
                                   adaptive, tol_share, p_cap, cos_tab, sin_tab, n_samples, ys,
-                                  out, i0, i1, accumulate, DT_PSEL_FAST, nullptr, eval_ws,
-                                  workspace_bytes - (pre - 256), stream);
+                                  out, i0, i1, accumulate, DT_PSEL_FAST, nullptr, ws + pre,
+                                  workspace_bytes - pre, stream);
 }
 
 extern "C" int dt_choose_p_batch(const double *big_r, const double *h, int64_t n, double rd2,

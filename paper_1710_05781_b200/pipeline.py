@@ -17,7 +17,6 @@ pass with one all-gather of the cut-level moment rows).
 
 from __future__ import annotations
 
-import os
 
 import torch
 
@@ -56,10 +55,8 @@ class TreePipeline:
         self.scan_ws_bytes = int(L.dt_prefix_scan_workspace(self.n))
         self.scan_ws = torch.empty(self.scan_ws_bytes, dtype=torch.uint8, device=self.dev)
         self.xq = torch.empty(2 * self.n, dtype=torch.float64, device=self.dev)
-        nbytes = 256
-        if os.environ.get("DISCTREE_EVAL_TWOPHASE") == "1":
-            nbytes = int(L.dt_tree_eval_items_workspace(self.T))
-        self.eval_ws = torch.empty(nbytes, dtype=torch.uint8, device=self.dev)
+        self.eval_ws = torch.empty(_lib.DT_EVAL_COUNTER_BYTES, dtype=torch.uint8,
+                                   device=self.dev)
         self.sign_ws_bytes = int(L.dt_sign_terms_workspace(self.T))
         self.sign_ws = torch.empty(self.sign_ws_bytes, dtype=torch.uint8, device=self.dev)
         self.cos_t, self.sin_t = contour_tables(self.dev)

@@ -11,7 +11,6 @@ in the reference's breadth-first layout and are bit-identical to it.
 from __future__ import annotations
 
 import ctypes as C
-import os
 import time
 from dataclasses import dataclass, field
 
@@ -308,10 +307,7 @@ def tree_phi_sum(tree: Tree, kernel: DiscKernel, config: EvalConfig, ys: torch.T
         return
     cos_t, sin_t = contour_tables(ys.device)
     if workspace is None:
-        nbytes = 256
-        if os.environ.get("DISCTREE_EVAL_TWOPHASE") == "1":
-            nbytes = int(_lib.load().dt_tree_eval_items_workspace(i1 - i0))
-        workspace = torch.empty(nbytes, dtype=torch.uint8, device=ys.device)
+        workspace = torch.empty(_lib.DT_EVAL_COUNTER_BYTES, dtype=torch.uint8, device=ys.device)
     p = _lib.ptr
     _lib.check(
         _lib.load().dt_tree_phi_sum_packed(
