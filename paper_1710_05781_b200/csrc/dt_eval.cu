@@ -24,9 +24,9 @@
 // complex arithmetic.  On the contour |f|^4 = 1 / ((1 - s*/s_t)^2 + s*) with
 // s_t = |e^{i theta_t} - 1|^2 and s* = r_d^2 / R^2, unimodal in t, so the
 // sampled maximum sits at the samples bracketing s_t = s*.  Tier 1 evaluates
-// that closed form in fp32 and solves the bound scan for p directly (two
-// logarithms); when the result lies within DT_PSEL_MARGIN of an integer
-// decision boundary, tier 2 re-runs the reference's exact double-precision
+// that closed form in fp32 and solves the bound scan for p directly in
+// log2 space; when log2(value_p / tol) lies within PSEL_MARGIN_LOG2 of 0 at
+// the candidate order, tier 2 re-runs the reference's exact double-precision
 // operation sequence (numpy csqrt, CPython complex quotient, glibc's
 // hypot, the fused forms LLVM emitted) on the bracketing samples and their
 // mirrors, and tier 3 (tiny s*, out-of-range inputs or DT_PSEL_EXACT) on all
@@ -52,9 +52,6 @@ static_assert(DT_EVAL_SEGMENTS * 4 <= DT_EVAL_COUNTER_BYTES, "counter slot too s
 #ifndef DT_FAR_MASKED_CHUNKS
 #define DT_FAR_MASKED_CHUNKS 0
 #endif
-#ifndef DT_PSEL_BF
-#define DT_PSEL_BF 0  // branch-free order estimate (psel_fast_bf)
-#endif
 #ifndef DT_EVAL_UTIL
 #define DT_EVAL_UTIL 0  // development: lane-utilisation counters (variant builds only)
 #endif
@@ -67,7 +64,7 @@ __device__ unsigned long long g_util[16];
 constexpr int EVAL_THREADS = DT_EVAL_THREADS;
 constexpr int EVAL_WARPS = EVAL_THREADS / 32;
 constexpr int MAX_SAMPLES = 256;
-constexpr float PSEL_MARGIN = 1e-4f;    // in units of the order axis
+constexpr float PSEL_MARGIN_LOG2 = 2e-4f;  // ambiguity band of log2(value_n / tol)
 constexpr double CONTOUR_SAFETY = 1.1;  // kernel.py:27
 
 struct EvalArgs {
@@ -267,14 +264,17 @@ __device__ __forceinline__ void split_log2(float x, int *e, float *f)
 
 // Returns p >= 0 on a confident decision, or -(t0 + 2) (<= -2) when the
 // decision is within the margin (tier 2 with bracket t0), or -1 for tier 3.
-// Error budget of the order estimate (in units of p): MUFU logs 2^-22 each
-// (x up to 31 for the ratio term), approximate fp32 divisions/roots (a few
-// ulp of the factors of X) -> below 2e-5; PSEL_MARGIN is 5x that.
+// The decision is the sign of resid = log2(value_n / tol) at the candidate
+// n; its absolute error (log2 units) is below 5e-5: MUFU.LG2 (2 ulp of a
+// result below 128, /4 for the contour term; 2^-22 for the mantissa of
+// ratio), fp32 rounding of the few sums of magnitude < 128, (n + 1) <= 32
+// times the log2 error of the fp32 ratio (~3e-7).  PSEL_MARGIN_LOG2 = 2e-4
+// is 4x that; inside it the exact replica decides.
 // s* = r_d^2/R^2 >= 4 puts every sample below the peak of |f| (maximum at
 // t = 32, the far side of the contour) and s* <= s_1 puts every sample above
 // it (maximum at t = 1); only in between is the bracket located (asin).
 __device__ int psel_fast(double big_r, double h, const EvalArgs &a, const float *isig,
-                         float rd2f, float inv_tol_f)
+                         float rd2f, float log_c)
 {
     if (h == 0.0)
         return 0;  // value == 0 <= tol at cand 0
@@ -311,78 +311,28 @@ __device__ int psel_fast(double big_r, double h, const EvalArgs &a, const float 
         const float ua = sstar * isig[ta], ub = sstar * isig[tb];
         emin = fminf((1.0f - ua) * (1.0f - ua), (1.0f - ub) * (1.0f - ub));
     }
-    const float rq = rsqrtf(emin + sstar);     // (M^-4)^(-1/2)
-    const float M = rq * rsqrtf(rq);           // sampled contour maximum of |f|
-    // value_0 / tol = 1.1 M (h/R) / (1 - h/R) / tol
-    const float X = 1.1f * M * hf * inv_tol_f * fast_rcp(Rf - hf);
-    if (!(X > 1e-37f && X < 1e37f))
-        return -1;
-    int ex, er;
-    float fx, fr;
-    split_log2(X, &ex, &fx);
+    // log2(value_0 / tol) = log2(1.1 / tol) + log2 M + log2 ratio - log2(1 - ratio),
+    // log2 M = -log2(emin + s*) / 4 (the sampled contour maximum of |f|).
+    // log2 ratio = er + fr keeps its integer part exact: it is multiplied by
+    // the candidate order below.
+    int er;
+    float fr;
     split_log2(ratio, &er, &fr);
+    const float lx = (fmaf(-0.25f, __log2f(emin + sstar), log_c) - __log2f(1.0f - ratio)) + fr;
     const float L = -((float)er + fr);         // -log2(ratio) > 0
     const float iL = fast_rcp(L);
-    const float pstar_approx = ((float)ex + fx) * iL;
+    const float pstar_approx = (lx + (float)er) * iL;
     if (pstar_approx < -1.0f)
         return 0;
     if (pstar_approx > (float)a.p_cap + 1.0f)
         return a.p_cap;
     const int n = __float2int_rn(pstar_approx);
-    // residual N - n L with the integer parts kept exact
-    const float resid = (float)(ex + n * er) + fmaf((float)n, fr, fx);
-    const float dist = resid * iL;             // pstar - n
-    if (fabsf(dist) < PSEL_MARGIN && n >= 0 && n <= a.p_cap - 1)
+    // residual log2(value_n / tol) = lx + (n + 1) er + n fr, integer part exact
+    const float resid = fmaf((float)n, fr, lx) + (float)((n + 1) * er);
+    if (fabsf(resid) < PSEL_MARGIN_LOG2 && n >= 0 && n <= a.p_cap - 1)
         return -(t0 + 2);
-    const int p = max(dist > 0.0f ? n + 1 : n, 0);
+    const int p = max(resid > 0.0f ? n + 1 : n, 0);  // value_n > tol: one more order
     return min(p, a.p_cap);
-}
-
-
-// Branch-free form of psel_fast (same return codes): every regime is
-// evaluated and selected, so the compiler can interleave this fp32 chain
-// with the independent FP64 far-field setup of the same pair.
-__device__ __forceinline__ int psel_fast_bf(double big_r, double h, const EvalArgs &a,
-                                            const float *isig, float rd2f, float inv_tol_f)
-{
-    const float Rf = f32_of(big_r);
-    const float hf = f32_of(h);
-    const float iR = fast_rcp(Rf);
-    const float ratio = hf * iR;
-    const float sstar = rd2f * iR * iR;
-    const bool bad0 =
-        !(Rf > 1e-15f && Rf < 1e15f && ratio > 1e-30f && sstar > 1e-12f && sstar < 1e30f);
-    const float z = fminf(1.0f, 0.5f * sstar * rsqrtf(sstar));
-    const float om = 1.0f - z;
-    const float poly = fmaf(fmaf(fmaf(-0.0187293f, z, 0.0742610f), z, -0.2121144f), z,
-                            1.5707288f);
-    const float asz = 1.57079633f - om * rsqrtf(fmaxf(om, 1e-30f)) * poly;
-    const int tb0 = min(max((int)(asz * 20.371832715762604f), 0), 32);
-    const int t0 = sstar >= 4.0f ? 32 : (sstar <= isig[34] ? 0 : tb0);
-    const int ta = max(t0, 1), tb = min(t0 + 1, 32);
-    const float ua = sstar * isig[ta], ub = sstar * isig[tb];
-    const float emin = fminf((1.0f - ua) * (1.0f - ua), (1.0f - ub) * (1.0f - ub));
-    const float rq = rsqrtf(emin + sstar);
-    const float M = rq * rsqrtf(rq);
-    const float X = 1.1f * M * hf * inv_tol_f * fast_rcp(Rf - hf);
-    const bool bad = bad0 || !(X > 1e-37f && X < 1e37f);
-    int ex, er;
-    float fx, fr;
-    split_log2(X, &ex, &fx);
-    split_log2(ratio, &er, &fr);
-    const float L = -((float)er + fr);
-    const float iL = fast_rcp(L);
-    const float pstar_approx = ((float)ex + fx) * iL;
-    const int n = __float2int_rn(fminf(fmaxf(pstar_approx, -2.0f), 1e4f));
-    const float resid = (float)(ex + n * er) + fmaf((float)n, fr, fx);
-    const float dist = resid * iL;
-    const bool amb = fabsf(dist) < PSEL_MARGIN && n >= 0 && n <= a.p_cap - 1;
-    const int p = min(max(dist > 0.0f ? n + 1 : n, 0), a.p_cap);
-    int r = amb ? -(t0 + 2) : p;
-    r = pstar_approx < -1.0f ? 0 : r;
-    r = pstar_approx > (float)a.p_cap + 1.0f ? a.p_cap : r;
-    r = bad ? -1 : r;
-    return h == 0.0 ? 0 : r;
 }
 
 // ------------------------------------------------------------------ far / near
@@ -649,7 +599,7 @@ __global__ void __launch_bounds__(EVAL_THREADS, DT_EVAL_MINB) tree_eval_kernel(E
     __shared__ float fconst_s[2];
     if (threadIdx.x == 0) {
         fconst_s[0] = f32_of(a.rd2);
-        fconst_s[1] = f32_of(1.0 / a.tol_share);
+        fconst_s[1] = f32_of(log2(CONTOUR_SAFETY / a.tol_share));
     }
     __syncthreads();
 
@@ -724,15 +674,9 @@ __global__ void __launch_bounds__(EVAL_THREADS, DT_EVAL_MINB) tree_eval_kernel(E
                 int pu = -1;
                 if (far) {
                     if (ADAPTIVE) {
-#if DT_PSEL_BF
-                        int r = fast_ok ? psel_fast_bf(big_r, half, a, isig_s, fconst_s[0],
-                                                       fconst_s[1])
-                                        : -1;
-#else
                         int r = fast_ok ? psel_fast(big_r, half, a, isig_s, fconst_s[0],
                                                     fconst_s[1])
                                         : -1;
-#endif
                         if (r < 0) {
                             if (r <= -2 && fast_ok)
                                 r = psel_exact_bracket(big_r, half, -r - 2, a, cs, sn);
@@ -888,7 +832,8 @@ __global__ void choose_p_kernel(const double *__restrict__ R, const double *__re
     if (i >= n)
         return;
     const bool fast_ok = a.n_samples == 64 && a.psel_mode == DT_PSEL_FAST;
-    int r = fast_ok ? psel_fast(R[i], H[i], a, isig_s, (float)a.rd2, (float)(1.0 / a.tol_share))
+    int r = fast_ok ? psel_fast(R[i], H[i], a, isig_s, f32_of(a.rd2),
+                                f32_of(log2(CONTOUR_SAFETY / a.tol_share)))
                     : -1;
     int tier = 0;
     if (r < 0) {
