@@ -9,11 +9,13 @@
 // else descends.
 //
 // B200 mapping: one warp owns 32 consecutive (sorted) targets and walks the
-// UNION of their traversals with a per-entry lane mask (the warp-uniform
-// stack lives in the lanes' registers).  Each lane applies the reference's MAC to its own target, so the
-// per-target interaction lists -- and their DFS order -- are exactly the
-// reference's.  Warps pull 32-target chunks from a global counter
-// (persistent grid, 148 x k CTAs).
+// UNION of their traversals with a per-entry lane mask (an opened node
+// continues into its first child; pending right siblings sit on a per-warp
+// stack in shared memory).  Each lane applies the reference's MAC to its own
+// target, so the per-target interaction lists -- and their DFS order -- are
+// exactly the reference's.  Warps pull 32-target tasks from per-SM segments
+// of the target range (persistent grid, 148 x 4 CTAs), so the warps of an SM
+// share node records and moment rows in L1.
 //   far   accepting lanes evaluate the recurrence together up to the warp's
 //         largest order; the moment row is a broadcast load.
 //   near  lanes that reach an unaccepted leaf sum its (x, q) pairs, read as
