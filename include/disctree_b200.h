@@ -110,8 +110,9 @@ int dt_build_tree(const double *xs, int64_t n, int64_t leaf_capacity, int64_t ma
 
 /* Node moments m_k = sum_j q_j (x_j - c)^k / k!, k = 0..order, row-major
  * [n_nodes][order + 1] (tree.py:224-238): P2M at every leaf from its sources,
- * then M2M (binomial shift) bottom-up, one level at a time (order <= 31;
- * higher orders use a barrier-free dataflow).  Reads the tree produced by
+ * then M2M (binomial shift) bottom-up as a dataflow without grid barriers
+ * (the warp completing a node's last child forms the node).  Reads the tree
+ * produced by
  * dt_build_tree (meta gives n_nodes); node_capacity bounds the node arrays.
  * moments_eval (optional) receives the traversal layout used by the *_packed
  * and *_device evaluators: M'_0 = m_0, M'_k = (k-1)! m_k, row stride
@@ -164,12 +165,14 @@ int dt_shard_plan(const double *center, const double *half, const int64_t *start
  * arguments). */
 size_t dt_shard_rows_bytes(int64_t cut_level, int64_t order, int64_t eval_stride);
 /* dt_moments restricted to the plan: leaves above level l, and every node at
- * levels >= l whose sources lie in [src_lo, src_hi).  order <= 31. */
+ * levels >= l whose sources lie in [src_lo, src_hi).  order <= 31; the
+ * workspace is dt_moments_workspace(node_capacity) bytes. */
 int dt_moments_partial(const double *xs, const double *qs, const double *center,
                        const int64_t *start, const int64_t *end, const int64_t *left,
                        const int64_t *right, const int64_t *meta, const int64_t *plan,
                        int64_t order, double *moments, double *moments_eval,
-                       int64_t eval_stride, void *stream);
+                       int64_t eval_stride, int64_t node_capacity, void *workspace,
+                       size_t workspace_bytes, void *stream);
 /* Copy this rank's owned level-l rows into its gather slot `send`. */
 int dt_shard_pack(const int64_t *plan, int rank, int64_t cut_level, int64_t order,
                   const double *moments, const double *moments_eval, int64_t eval_stride,

@@ -81,7 +81,7 @@ SIGNATURES = {
     ),
     "dt_shard_rows_bytes": (_SZ, [_I64, _I64, _I64]),
     "dt_moments_partial": (
-        C.c_int, [_P, _P, _P, _P, _P, _P, _P, _P, _P, _I64, _P, _P, _I64, _P],
+        C.c_int, [_P, _P, _P, _P, _P, _P, _P, _P, _P, _I64, _P, _P, _I64, _I64, _P, _SZ, _P],
     ),
     "dt_shard_pack": (C.c_int, [_P, C.c_int, _I64, _I64, _P, _P, _I64, _P, _P]),
     "dt_shard_finish": (

@@ -21,6 +21,22 @@
 
 namespace cg = cooperative_groups;
 
+#ifndef DT_MOM_V2
+#define DT_MOM_V2 1  // G lanes per leaf P2M + thread-per-node Pascal M2M (order <= 31)
+#endif
+#ifndef DT_P2M_G
+#define DT_P2M_G 4
+#endif
+#ifndef DT_M2M_MODE
+#define DT_M2M_MODE 2  // 0 level-sync, 1 thread dataflow, 2 warp dataflow, 3 narrow/wide phases
+#endif
+#ifndef DT_M2M_W32
+#define DT_M2M_W32 1  // level kernel: 32 parents per warp, rows staged in shared memory
+#endif
+#ifndef DT_M2M_FLOW_CHUNK
+#define DT_M2M_FLOW_CHUNK 32
+#endif
+
 namespace {
 
 constexpr int MOM_THREADS = 128;
@@ -449,6 +465,555 @@ __global__ void __launch_bounds__(128) p2m_thread_kernel(MomArgs a)
     }
 }
 
+// ---- v2: G lanes per leaf (P2M), thread per node (M2M, in-place Pascal) ----
+
+// P2M with G consecutive lanes per leaf: each lane sums every G-th source of
+// the leaf (the group's loads cover contiguous sectors), four sources in
+// flight, then a butterfly over the G lanes.  Leaves are gathered per warp
+// from 32 consecutive node slots (ballot) so no group idles on internal
+// nodes.  Raw power sums S_k = sum q (x - c)^k in registers.
+template <int G>
+__global__ void __launch_bounds__(256) p2m_group_kernel(MomArgs a)
+{
+    const int lane = dt_lane();
+    const int sub = lane & (G - 1), grp = lane / G;
+    const int64_t n = __ldg(a.meta + DT_META_NODES);
+    const int o1 = (int)a.order + 1;
+    int64_t cut_begin = INT64_MAX, lo = 0, hi = 0;
+    if (a.plan) {
+        cut_begin = __ldg(a.plan + DT_PLAN_LEVEL_BEGIN);
+        lo = __ldg(a.plan + DT_PLAN_SRC_LO);
+        hi = __ldg(a.plan + DT_PLAN_SRC_HI);
+    }
+    const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t c0 = gwarp * 32; c0 < n; c0 += nwarps * 32) {
+        const int64_t mine = c0 + lane;
+        bool leaf = false;
+        if (mine < n) {
+            const int64_t l = __ldg(a.left + mine), r = __ldg(a.right + mine);
+            if (a.parent) {  // dataflow M2M bookkeeping (m2m_flow_kernel)
+                a.arrived[mine] = 0;
+                if (l >= 0)
+                    a.parent[l] = (int32_t)mine;
+                if (r >= 0)
+                    a.parent[r] = (int32_t)mine;
+                if (mine == 0)
+                    a.parent[0] = -1;
+            }
+            leaf = l < 0 && r < 0;
+            if (leaf && mine >= cut_begin)
+                leaf = __ldg(a.start + mine) >= lo && __ldg(a.end + mine) <= hi;
+        }
+        unsigned leaves = __ballot_sync(DT_FULL, leaf);
+        while (leaves) {
+            // group grp takes the grp-th remaining leaf
+            unsigned m = leaves;
+            for (int i = 0; i < grp && m; ++i)
+                m &= m - 1;
+            const bool active = m != 0;
+            const int64_t node = c0 + (active ? __ffs(m) - 1 : 0);
+            for (int i = 0; i < 32 / G && leaves; ++i)
+                leaves &= leaves - 1;
+            int64_t s = 0, e = 0;
+            double c = 0.0;
+            if (active) {
+                s = __ldg(a.start + node);
+                e = __ldg(a.end + node);
+                c = __ldg(a.center + node);
+            }
+            double acc[REG_ORDER];
+#pragma unroll
+            for (int k = 0; k < REG_ORDER; ++k)
+                acc[k] = 0.0;
+            int64_t j = s + sub;
+            for (; j + 3 * G < e; j += 4 * G) {
+                const double t0 = __ldg(a.xs + j) - c, t1 = __ldg(a.xs + j + G) - c;
+                const double t2 = __ldg(a.xs + j + 2 * G) - c, t3 = __ldg(a.xs + j + 3 * G) - c;
+                double w0 = __ldg(a.qs + j), w1 = __ldg(a.qs + j + G);
+                double w2 = __ldg(a.qs + j + 2 * G), w3 = __ldg(a.qs + j + 3 * G);
+#pragma unroll
+                for (int k = 0; k < REG_ORDER; ++k) {
+                    if (k < o1) {
+                        acc[k] += (w0 + w1) + (w2 + w3);
+                        w0 *= t0;
+                        w1 *= t1;
+                        w2 *= t2;
+                        w3 *= t3;
+                    }
+                }
+            }
+            for (; j < e; j += G) {
+                const double t0 = __ldg(a.xs + j) - c;
+                double w0 = __ldg(a.qs + j);
+#pragma unroll
+                for (int k = 0; k < REG_ORDER; ++k) {
+                    if (k < o1) {
+                        acc[k] += w0;
+                        w0 *= t0;
+                    }
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < REG_ORDER; ++k) {
+#pragma unroll
+                for (int o = G / 2; o > 0; o >>= 1)
+                    acc[k] += __shfl_xor_sync(DT_FULL, acc[k], o);
+            }
+            if (active) {
+#pragma unroll
+                for (int k = 0; k < REG_ORDER; ++k)
+                    if ((k & (G - 1)) == sub && k < o1)
+                        put_raw_sum(a, node, k, acc[k]);
+            }
+        }
+    }
+}
+
+// Form internal node P from its children, one warp, lane k = order k, on
+// raw power sums S_k = k! m_k: the binomial shift S'_k = sum_j C(k, j)
+// delta^(k-j) S_j is applied in place as 31 passes of S_k += delta S_(k-1)
+// (Pascal's rule; the previous pass's S_(k-1) comes from lane k-1).  Both
+// children run in the same passes.  Same arithmetic, term for term, as the
+// thread-per-node form m2m_level_threads.
+__device__ __forceinline__ void m2m_form_warp(const MomArgs &a, int64_t P)
+{
+    const int lane = dt_lane();
+    const int o1 = (int)a.order + 1;
+    const int64_t l = __ldg(a.left + P), r = __ldg(a.right + P);
+    const double c = __ldg(a.center + P);
+    const double dl = l >= 0 ? __ldg(a.center + l) - c : 0.0;
+    const double dr = r >= 0 ? __ldg(a.center + r) - c : 0.0;
+    const double fk = c_fact_km1[lane + 1];
+    double Sl = (l >= 0 && lane < o1) ? __dmul_rn(__ldcg(a.moments + l * o1 + lane), fk) : 0.0;
+    double Sr = (r >= 0 && lane < o1) ? __dmul_rn(__ldcg(a.moments + r * o1 + lane), fk) : 0.0;
+#pragma unroll
+    for (int i = 1; i < REG_ORDER; ++i) {
+        const double tl = __shfl_up_sync(DT_FULL, Sl, 1);
+        const double tr = __shfl_up_sync(DT_FULL, Sr, 1);
+        if (lane >= i) {
+            Sl = __fma_rn(dl, tl, Sl);
+            Sr = __fma_rn(dr, tr, Sr);
+        }
+    }
+    double out = 0.0;
+    if (l >= 0)
+        out += Sl;
+    if (r >= 0)
+        out += Sr;
+    if (lane < o1)
+        put_raw_sum(a, P, lane, out);
+}
+
+// Upward pass without grid barriers (after the P2M kernel, which also wrote
+// parent[] and zeroed arrived[]): every leaf bumps its parent's arrival
+// counter; the warp whose arrival completes a parent forms it and keeps
+// climbing while it completes the next ancestor.  With a shard plan the
+// climb stops below the cut level and covers the plan's subtrees only.
+__global__ void __launch_bounds__(256) m2m_flow_kernel(MomArgs a)
+{
+    const int lane = dt_lane();
+    const int64_t n = __ldg(a.meta + DT_META_NODES);
+    int64_t cut_begin = 0, lo = 0, hi = 0;
+    if (a.plan) {
+        cut_begin = __ldg(a.plan + DT_PLAN_LEVEL_BEGIN);
+        lo = __ldg(a.plan + DT_PLAN_SRC_LO);
+        hi = __ldg(a.plan + DT_PLAN_SRC_HI);
+    }
+    const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    constexpr int CH = DT_M2M_FLOW_CHUNK;  // nodes scanned per warp step
+    for (int64_t r0 = gwarp * CH; r0 < n; r0 += nwarps * CH) {
+        // deepest levels first: their chains are the critical path
+        const int64_t c0 = n - CH - r0;  // may be negative for the last chunk
+        const int64_t mine = c0 + lane;
+        bool done = false;
+        int64_t par = -1;
+        if (lane < CH && mine >= 0 && mine < n && __ldg(a.left + mine) < 0 &&
+            __ldg(a.right + mine) < 0) {
+            par = __ldcg(a.parent + mine);
+            bool in = par >= cut_begin;
+            if (in && a.plan)
+                in = __ldg(a.start + mine) >= lo && __ldg(a.end + mine) <= hi;
+            if (in) {
+                const int need = (__ldg(a.left + par) >= 0) + (__ldg(a.right + par) >= 0);
+                done = atomicAdd(a.arrived + par, 1) == need - 1;
+            }
+        }
+        unsigned todo = __ballot_sync(DT_FULL, done);
+        while (todo) {
+            const int i = __ffs(todo) - 1;
+            todo &= todo - 1;
+            int64_t P = __shfl_sync(DT_FULL, par, i);
+            while (true) {
+                __threadfence();  // the other children's rows, published before their arrival
+                m2m_form_warp(a, P);
+                __threadfence();  // publish P's row before announcing it
+                int64_t pp = -1;
+                if (lane == 0) {
+                    const int64_t q = __ldcg(a.parent + P);
+                    if (q >= cut_begin && q >= 0) {
+                        const int need = (__ldg(a.left + q) >= 0) + (__ldg(a.right + q) >= 0);
+                        if (atomicAdd(a.arrived + q, 1) == need - 1)
+                            pp = q;
+                    }
+                }
+                pp = __shfl_sync(DT_FULL, pp, 0);
+                if (pp < 0)
+                    break;
+                P = pp;
+            }
+        }
+    }
+}
+
+// Arrival on a parent's counter with acquire-release semantics at GPU scope:
+// publishes this thread's row writes and, for the completing arrival, makes
+// the siblings' rows visible.
+__device__ __forceinline__ int arrive_acq_rel(int32_t *ctr)
+{
+    int old;
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(ctr) : "memory");
+    return old;
+}
+
+// Thread-per-node form of one internal node (same arithmetic as
+// m2m_level_threads / m2m_form_warp).
+__device__ __forceinline__ void m2m_form_thread(const MomArgs &a, int64_t node)
+{
+    const int o1 = (int)a.order + 1;
+    const int64_t l = __ldg(a.left + node), r = __ldg(a.right + node);
+    const double c = __ldg(a.center + node);
+    double out[REG_ORDER];
+#pragma unroll
+    for (int k = 0; k < REG_ORDER; ++k)
+        out[k] = 0.0;
+#pragma unroll 1
+    for (int ci = 0; ci < 2; ++ci) {
+        const int64_t ch = ci == 0 ? l : r;
+        if (ch < 0)
+            continue;
+        const double delta = __ldg(a.center + ch) - c;
+        const double *row = a.moments + ch * o1;
+        double S[REG_ORDER];
+#pragma unroll
+        for (int k = 0; k < REG_ORDER; ++k)
+            S[k] = k < o1 ? __ldcg(row + k) : 0.0;
+#pragma unroll
+        for (int k = 0; k < REG_ORDER; ++k)
+            S[k] = __dmul_rn(S[k], c_fact_km1[k + 1]);
+#pragma unroll
+        for (int i = 1; i < REG_ORDER; ++i) {
+#pragma unroll
+            for (int k = REG_ORDER - 1; k >= i; --k)
+                S[k] = __fma_rn(delta, S[k - 1], S[k]);
+        }
+#pragma unroll
+        for (int k = 0; k < REG_ORDER; ++k)
+            out[k] += S[k];
+    }
+#pragma unroll
+    for (int k = 0; k < REG_ORDER; ++k)
+        if (k < o1)
+            put_raw_sum(a, node, k, out[k]);
+}
+
+// Dataflow upward pass, thread granularity: the thread whose arrival
+// completes a parent forms it (in-register Pascal shift) and climbs on.
+// Sibling leaves sit in the same warp, so the first climbs run 16 lanes wide.
+__global__ void __launch_bounds__(128) m2m_flow_thread_kernel(MomArgs a)
+{
+    const int64_t n = __ldg(a.meta + DT_META_NODES);
+    int64_t cut_begin = 0, lo = 0, hi = 0;
+    if (a.plan) {
+        cut_begin = __ldg(a.plan + DT_PLAN_LEVEL_BEGIN);
+        lo = __ldg(a.plan + DT_PLAN_SRC_LO);
+        hi = __ldg(a.plan + DT_PLAN_SRC_HI);
+    }
+    // deepest levels first: their chains are the critical path
+    for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < n;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t mine = n - 1 - idx;
+        if (__ldg(a.left + mine) >= 0 || __ldg(a.right + mine) >= 0)
+            continue;
+        int64_t P = __ldcg(a.parent + mine);
+        if (P < cut_begin || P < 0)
+            continue;
+        if (a.plan && (__ldg(a.start + mine) < lo || __ldg(a.end + mine) > hi))
+            continue;
+        while (true) {
+            const int need = (__ldg(a.left + P) >= 0) + (__ldg(a.right + P) >= 0);
+            if (arrive_acq_rel(a.arrived + P) != need - 1)
+                break;
+            m2m_form_thread(a, P);
+            const int64_t q = __ldcg(a.parent + P);
+            if (q < cut_begin || q < 0)
+                break;
+            P = q;
+        }
+    }
+}
+
+// M2M of one level with one thread per internal node, on raw power sums:
+// S'_k = sum_j C(k, j) delta^(k-j) S_j (the binomial transform) computed in
+// place by k passes of S_k += delta S_(k-1) over descending k (Pascal's
+// rule), so a child row needs only its own 32 registers.
+__device__ __forceinline__ void m2m_level_threads(const MomArgs &a, int64_t f0, int64_t f1,
+                                                  int64_t tid, int64_t nthreads, bool filter,
+                                                  int64_t src_lo, int64_t src_hi)
+{
+    const int o1 = (int)a.order + 1;
+    for (int64_t node = f0 + tid; node < f1; node += nthreads) {
+        const int64_t l = __ldg(a.left + node), r = __ldg(a.right + node);
+        if (l < 0 && r < 0)
+            continue;
+        if (filter && (__ldg(a.start + node) < src_lo || __ldg(a.end + node) > src_hi))
+            continue;
+        const double c = __ldg(a.center + node);
+        double out[REG_ORDER];
+#pragma unroll
+        for (int k = 0; k < REG_ORDER; ++k)
+            out[k] = 0.0;
+#pragma unroll 1
+        for (int ci = 0; ci < 2; ++ci) {
+            const int64_t ch = ci == 0 ? l : r;
+            if (ch < 0)
+                continue;
+            const double delta = __ldg(a.center + ch) - c;
+            const double *row = a.moments + ch * o1;
+            // L2-coherent loads (the row was formed earlier in this kernel),
+            // all issued before the first use
+            double S[REG_ORDER];
+#pragma unroll
+            for (int k = 0; k < REG_ORDER; ++k)
+#ifdef DT_M2M_NOLOAD
+                S[k] = delta * k;
+#elif defined(DT_M2M_LDG)
+                S[k] = k < o1 ? __ldg(row + k) : 0.0;
+#else
+                S[k] = k < o1 ? __ldcg(row + k) : 0.0;
+#endif
+#pragma unroll
+            for (int k = 0; k < REG_ORDER; ++k)
+                S[k] = __dmul_rn(S[k], c_fact_km1[k + 1]);
+#ifndef DT_M2M_NOPASCAL
+#pragma unroll
+            for (int i = 1; i < REG_ORDER; ++i) {
+#pragma unroll
+                for (int k = REG_ORDER - 1; k >= i; --k)
+                    S[k] = __fma_rn(delta, S[k - 1], S[k]);
+            }
+#endif
+#pragma unroll
+            for (int k = 0; k < REG_ORDER; ++k)
+                out[k] += S[k];
+        }
+#pragma unroll
+        for (int k = 0; k < REG_ORDER; ++k)
+            if (k < o1)
+                put_raw_sum(a, node, k, out[k]);
+    }
+}
+
+// One level, 32 consecutive parents per warp, lane = parent: the children of
+// consecutive parents are consecutive nodes, so their rows (<= 64) are one
+// contiguous block that the warp stages through shared memory with
+// coalesced loads; each lane shifts its children in registers (Pascal's
+// rule on raw sums, same arithmetic as m2m_level_threads) and the 32 output
+// rows leave through shared memory as coalesced (masked) stores.
+constexpr int M2M_BUF = 64 * REG_ORDER;  // doubles of staging per warp
+
+// dst[r * w + c] = buf[r * w + c] for rows r < rows with bit r of mask set
+// (w <= 32: one coalesced store per row).
+__device__ __forceinline__ void masked_rows_store(double *dst, const double *buf, int rows, int w,
+                                                  unsigned mask)
+{
+    const int lane = dt_lane();
+    if (lane >= w)
+        return;
+#pragma unroll 4
+    for (int r = 0; r < rows; ++r)
+        if ((mask >> r) & 1u)
+            dst[r * w + lane] = buf[r * w + lane];
+}
+
+__device__ __forceinline__ void m2m_level_warps32(const MomArgs &a, int64_t f0, int64_t f1,
+                                                  int64_t gwarp, int64_t nwarps, bool filter,
+                                                  int64_t src_lo, int64_t src_hi, double *buf)
+{
+    const int lane = dt_lane();
+    const int o1 = (int)a.order + 1;
+    const int es = a.meval ? (int)a.estride : 0;
+#ifdef DT_M2M_TRACE2
+    unsigned long long *tr = reinterpret_cast<unsigned long long *>(a.arrived) + 64 + 8 * (f0 & 63);
+    const bool rec = blockIdx.x == 0 && threadIdx.x == 0;
+#define TSTAMP(slot)                                                      \
+    if (rec) {                                                            \
+        unsigned long long t_;                                            \
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));           \
+        tr[slot] = t_;                                                    \
+    }
+#else
+#define TSTAMP(slot)
+#endif
+    for (int64_t p0 = f0 + gwarp * 32; p0 < f1; p0 += nwarps * 32) {
+        TSTAMP(0)
+        const int64_t node = p0 + lane;
+        int64_t l = -1, r = -1;
+        bool act = false;
+        if (node < f1) {
+            l = __ldg(a.left + node);
+            r = __ldg(a.right + node);
+            act = l >= 0 || r >= 0;
+            if (act && filter)
+                act = __ldg(a.start + node) >= src_lo && __ldg(a.end + node) <= src_hi;
+        }
+        const unsigned am = __ballot_sync(DT_FULL, act);
+        if (!am)
+            continue;
+        const int first = act ? (int)(l >= 0 ? l : r) : INT32_MAX;
+        const int last = act ? (int)(r >= 0 ? r : l) : -1;
+        const int c_lo = __reduce_min_sync(DT_FULL, first);
+        const int c_hi = __reduce_max_sync(DT_FULL, last) + 1;
+        const double *src = a.moments + (int64_t)c_lo * o1;
+        // one coalesced row per load, 16 rows in flight before the first
+        // shared-memory store
+        const int nrows = c_hi - c_lo;
+        if (lane < o1) {
+            for (int r0 = 0; r0 < nrows; r0 += 16) {
+                double v[16];
+#pragma unroll
+                for (int j = 0; j < 16; ++j)
+                    v[j] = r0 + j < nrows ? __ldcg(src + (r0 + j) * o1 + lane) : 0.0;
+#pragma unroll
+                for (int j = 0; j < 16; ++j)
+                    if (r0 + j < nrows)
+                        buf[(r0 + j) * o1 + lane] = v[j];
+            }
+        }
+        __syncwarp();
+        TSTAMP(1)
+        double out[REG_ORDER];
+#pragma unroll
+        for (int k = 0; k < REG_ORDER; ++k)
+            out[k] = 0.0;
+        if (act) {
+            const double c = __ldg(a.center + node);
+#pragma unroll 1
+            for (int ci = 0; ci < 2; ++ci) {
+                const int64_t ch = ci == 0 ? l : r;
+                if (ch < 0)
+                    continue;
+                const double delta = __ldg(a.center + ch) - c;
+                const double *row = buf + (ch - c_lo) * o1;
+                double S[REG_ORDER];
+#pragma unroll
+                for (int k = 0; k < REG_ORDER; ++k)
+                    S[k] = k < o1 ? __dmul_rn(row[k], c_fact_km1[k + 1]) : 0.0;
+#pragma unroll
+                for (int i = 1; i < REG_ORDER; ++i) {
+#pragma unroll
+                    for (int k = REG_ORDER - 1; k >= i; --k)
+                        S[k] = __fma_rn(delta, S[k - 1], S[k]);
+                }
+#pragma unroll
+                for (int k = 0; k < REG_ORDER; ++k)
+                    out[k] += S[k];
+            }
+        }
+        __syncwarp();
+        TSTAMP(2)
+        // m_k = S_k / k!  (tree.py's moments), coalesced masked store
+        if (act) {
+#pragma unroll
+            for (int k = 0; k < REG_ORDER; ++k)
+                if (k < o1)
+                    buf[lane * o1 + k] = __dmul_rn(out[k], c_inv_fact[k]);
+        }
+        __syncwarp();
+        const int rows = (int)min((int64_t)32, f1 - p0);
+        masked_rows_store(a.moments + p0 * o1, buf, rows, o1, am);
+        if (es) {
+            __syncwarp();
+            // traversal copy M'_k = S_k / k (M'_0 = S_0), zero padded
+            if (act) {
+#pragma unroll
+                for (int k = 0; k < REG_ORDER; ++k)
+                    if (k < es)
+                        buf[lane * es + k] = k == 0 ? out[0]
+                                                    : (k < o1 ? __dmul_rn(out[k], c_inv_k[k]) : 0.0);
+            }
+            __syncwarp();
+            masked_rows_store(a.meval + p0 * es, buf, rows, es, am);
+        }
+        __syncwarp();
+        TSTAMP(3)
+    }
+#undef TSTAMP
+}
+
+// Levels with at most M2M_SMALL nodes are formed by block 0 alone (block
+// barrier); the grid synchronises only around the wide levels.  Whether a
+// level is small is read from meta, so every block takes the same path.
+#ifndef DT_M2M_THREADS
+#define DT_M2M_THREADS 128
+#endif
+constexpr int M2M_THREADS = DT_M2M_THREADS;
+#ifndef DT_M2M_SMALL
+#define DT_M2M_SMALL (4 * M2M_THREADS)
+#endif
+constexpr int64_t M2M_SMALL = DT_M2M_SMALL;
+
+__global__ void __launch_bounds__(M2M_THREADS) m2m_threads_kernel(MomArgs a)
+{
+    cg::grid_group grid = cg::this_grid();
+#if DT_M2M_W32
+    extern __shared__ double m2m_buf[];
+#endif
+    const volatile int64_t *meta = a.meta;
+    const int64_t depth = meta[DT_META_DEPTH];
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
+    int64_t stop = 0, lo = 0, hi = 0;
+    if (a.plan) {
+        stop = __ldg(a.plan + DT_PLAN_CUT);
+        lo = __ldg(a.plan + DT_PLAN_SRC_LO);
+        hi = __ldg(a.plan + DT_PLAN_SRC_HI);
+    }
+    bool prev_small = true;  // nothing formed yet: no barrier before the first level
+    bool first = true;
+    for (int64_t lev = depth - 1; lev >= stop; --lev) {
+        const int64_t f0 = meta[DT_META_LEVEL0 + lev], f1 = meta[DT_META_LEVEL0 + lev + 1];
+        const bool small = f1 - f0 <= M2M_SMALL;
+        if (!first) {
+            if (small && prev_small)
+                __syncthreads();
+            else
+                grid.sync();
+        }
+        first = false;
+#ifdef DT_M2M_TRACE
+        if (tid == 0) {
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            reinterpret_cast<unsigned long long *>(a.arrived)[lev] = t;
+        }
+#endif
+        // one call site keeps the (long, straight-line) formation code once
+#if DT_M2M_W32
+        if (!small || blockIdx.x == 0)
+            m2m_level_warps32(a, f0, f1, small ? (int64_t)(threadIdx.x >> 5) : (tid >> 5),
+                              small ? (int64_t)(blockDim.x >> 5) : (nthreads >> 5),
+                              a.plan != nullptr, lo, hi, m2m_buf + (threadIdx.x >> 5) * M2M_BUF);
+#else
+        if (!small || blockIdx.x == 0)
+            m2m_level_threads(a, f0, f1, small ? (int64_t)threadIdx.x : tid,
+                              small ? (int64_t)blockDim.x : nthreads, a.plan != nullptr, lo, hi);
+#endif
+        prev_small = small;
+    }
+}
+
 // M2M of one level, one warp per internal node, lane k -> order k:
 // m_k(parent) = sum_children sum_{j<=k} m_j(child) pw_{k-j},
 // pw_i = delta^i / i! from a multiplicative warp scan; the child row and pw
@@ -519,6 +1084,81 @@ __global__ void __launch_bounds__(256) m2m_levels_kernel(MomArgs a)
         m2m_level_warps(a, meta[DT_META_LEVEL0 + lev], meta[DT_META_LEVEL0 + lev + 1], gwarp,
                         nwarps, inv_s, pw_s[warp], m_s[warp], a.plan != nullptr, lo, hi);
         grid.sync();
+    }
+}
+
+// ---- level M2M split into narrow / wide phases (no spinning co-runners) ----
+//
+// Bottom-up the tree is narrow (deep refinement), then wide, then narrow
+// again (the top levels).  Narrow levels run in a single-block kernel (block
+// barriers only); the wide levels run in a cooperative kernel (one grid
+// barrier per level).  A block that waits on a grid barrier polls L2, which
+// slows the memory traffic of the blocks still working, so narrow levels are
+// never processed under a grid barrier.  Every kernel derives the same phase
+// boundaries from meta.
+constexpr int M2M_NARROW_THREADS = 256;
+constexpr int64_t M2M_NARROW = 4 * M2M_NARROW_THREADS;
+
+struct M2MPhases {
+    int64_t top, deep_end, wide_end, stop;  // levels [top .. deep_end), [deep_end .. wide_end), ...
+};
+
+__device__ __forceinline__ M2MPhases m2m_phases(const MomArgs &a)
+{
+    const int64_t depth = __ldg(a.meta + DT_META_DEPTH);
+    const int64_t stop = a.plan ? __ldg(a.plan + DT_PLAN_CUT) : 0;
+    auto width = [&](int64_t lev) {
+        return __ldg(a.meta + DT_META_LEVEL0 + lev + 1) - __ldg(a.meta + DT_META_LEVEL0 + lev);
+    };
+    int64_t lev = depth - 1;
+    while (lev >= stop && width(lev) <= M2M_NARROW)
+        --lev;
+    const int64_t deep_end = lev;  // first wide level from the bottom (or stop - 1)
+    while (lev >= stop && width(lev) > M2M_NARROW)
+        --lev;
+    return M2MPhases{depth - 1, deep_end, lev, stop};
+}
+
+// phase 0: narrow deep levels [top .. deep_end); phase 2: [wide_end .. stop]
+template <int PHASE>
+__global__ void __launch_bounds__(M2M_NARROW_THREADS) m2m_narrow_kernel(MomArgs a)
+{
+    extern __shared__ double m2m_nbuf[];
+    const M2MPhases ph = m2m_phases(a);
+    const int64_t from = PHASE == 0 ? ph.top : ph.wide_end;
+    const int64_t to = PHASE == 0 ? ph.deep_end + 1 : ph.stop;
+    int64_t lo = 0, hi = 0;
+    if (a.plan) {
+        lo = __ldg(a.plan + DT_PLAN_SRC_LO);
+        hi = __ldg(a.plan + DT_PLAN_SRC_HI);
+    }
+    for (int64_t lev = from; lev >= to; --lev) {
+        m2m_level_warps32(a, __ldg(a.meta + DT_META_LEVEL0 + lev),
+                          __ldg(a.meta + DT_META_LEVEL0 + lev + 1), threadIdx.x >> 5,
+                          blockDim.x >> 5, a.plan != nullptr, lo, hi,
+                          m2m_nbuf + (threadIdx.x >> 5) * M2M_BUF);
+        __syncthreads();
+    }
+}
+
+__global__ void __launch_bounds__(M2M_NARROW_THREADS) m2m_wide_kernel(MomArgs a)
+{
+    cg::grid_group grid = cg::this_grid();
+    extern __shared__ double m2m_wbuf[];
+    const M2MPhases ph = m2m_phases(a);
+    int64_t lo = 0, hi = 0;
+    if (a.plan) {
+        lo = __ldg(a.plan + DT_PLAN_SRC_LO);
+        hi = __ldg(a.plan + DT_PLAN_SRC_HI);
+    }
+    const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t lev = ph.deep_end; lev > ph.wide_end; --lev) {
+        if (lev != ph.deep_end)
+            grid.sync();
+        m2m_level_warps32(a, __ldg(a.meta + DT_META_LEVEL0 + lev),
+                          __ldg(a.meta + DT_META_LEVEL0 + lev + 1), gw, nw, a.plan != nullptr, lo,
+                          hi, m2m_wbuf + (threadIdx.x >> 5) * M2M_BUF);
     }
 }
 
@@ -667,29 +1307,79 @@ __global__ void __launch_bounds__(256) shard_finish_kernel(MomArgs a, int world,
     }
     __syncthreads();
     const int64_t cut = __ldg(a.plan + DT_PLAN_CUT);
-    const int warp = threadIdx.x >> 5;
     for (int64_t lev = cut - 1; lev >= 0; --lev) {
+#if DT_MOM_V2
+        m2m_level_threads(a, __ldg(a.meta + DT_META_LEVEL0 + lev),
+                          __ldg(a.meta + DT_META_LEVEL0 + lev + 1), threadIdx.x, blockDim.x,
+                          false, 0, 0);
+#else
+        const int warp = threadIdx.x >> 5;
         m2m_level_warps(a, __ldg(a.meta + DT_META_LEVEL0 + lev),
                         __ldg(a.meta + DT_META_LEVEL0 + lev + 1), warp, 8, inv_s, pw_s[warp],
                         m_s[warp]);
+#endif
         __syncthreads();
     }
 }
 
-// P2M (thread per leaf) + cooperative level M2M, honouring a.plan.
+// P2M + cooperative level M2M, honouring a.plan.
 int launch_level_moments(MomArgs &a, cudaStream_t s)
 {
     const int sms = dt_num_sms();
+    void *args[] = {&a};
+    int per_sm = 0;
+#if DT_MOM_V2
+    if (!a.parent)
+        return dt_set_error(DT_ERR_WORKSPACE, "moments workspace missing");
+    p2m_group_kernel<DT_P2M_G><<<sms * 8, 256, 0, s>>>(a);
+    DT_CUDA_TRY(cudaGetLastError());
+#if DT_M2M_MODE == 3
+    {
+        const size_t smem = (size_t)(M2M_NARROW_THREADS / 32) * M2M_BUF * sizeof(double);
+        DT_CUDA_TRY(cudaFuncSetAttribute((const void *)m2m_narrow_kernel<0>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        DT_CUDA_TRY(cudaFuncSetAttribute((const void *)m2m_narrow_kernel<2>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        DT_CUDA_TRY(cudaFuncSetAttribute((const void *)m2m_wide_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        m2m_narrow_kernel<0><<<1, M2M_NARROW_THREADS, smem, s>>>(a);
+        DT_CUDA_TRY(cudaGetLastError());
+        DT_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, m2m_wide_kernel,
+                                                                  M2M_NARROW_THREADS, smem));
+        if (per_sm < 1)
+            return dt_set_error(DT_ERR_CUDA, "m2m kernel cannot be resident");
+        DT_CUDA_TRY(cudaLaunchCooperativeKernel((const void *)m2m_wide_kernel, sms * per_sm,
+                                                M2M_NARROW_THREADS, args, smem, s));
+        m2m_narrow_kernel<2><<<1, M2M_NARROW_THREADS, smem, s>>>(a);
+    }
+#elif DT_M2M_MODE == 0
+    const size_t smem = DT_M2M_W32 ? (size_t)(M2M_THREADS / 32) * M2M_BUF * sizeof(double) : 0;
+    if (smem)
+        DT_CUDA_TRY(cudaFuncSetAttribute((const void *)m2m_threads_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    DT_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, m2m_threads_kernel,
+                                                              M2M_THREADS, smem));
+    if (per_sm < 1)
+        return dt_set_error(DT_ERR_CUDA, "m2m kernel cannot be resident");
+    DT_CUDA_TRY(cudaLaunchCooperativeKernel((const void *)m2m_threads_kernel,
+                                            sms * (per_sm > 2 ? 2 : per_sm), M2M_THREADS, args,
+                                            smem, s));
+#elif DT_M2M_MODE == 1
+    m2m_flow_thread_kernel<<<sms * 8, 128, 0, s>>>(a);
+#else
+    m2m_flow_kernel<<<sms * 8, 256, 0, s>>>(a);
+#endif
+    DT_CUDA_TRY(cudaGetLastError());
+#else
     p2m_thread_kernel<<<sms * 16, 128, 0, s>>>(a);
     DT_CUDA_TRY(cudaGetLastError());
-    int per_sm = 0;
     DT_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, m2m_levels_kernel, 256, 0));
     if (per_sm < 1)
         return dt_set_error(DT_ERR_CUDA, "m2m kernel cannot be resident");
     const int grid = sms * (per_sm > 4 ? 4 : per_sm);
-    void *args[] = {&a};
     DT_CUDA_TRY(
         cudaLaunchCooperativeKernel((const void *)m2m_levels_kernel, grid, 256, args, 0, s));
+#endif
     return DT_OK;
 }
 
@@ -758,15 +1448,19 @@ extern "C" int dt_moments_partial(const double *xs, const double *qs, const doub
                                   const int64_t *start, const int64_t *end, const int64_t *left,
                                   const int64_t *right, const int64_t *meta, const int64_t *plan,
                                   int64_t order, double *moments, double *moments_eval,
-                                  int64_t eval_stride, void *stream)
+                                  int64_t eval_stride, int64_t node_capacity, void *workspace,
+                                  size_t workspace_bytes, void *stream)
 {
     DT_CHECK_ARG(order >= 0 && order + 1 <= REG_ORDER, "sharded moments need order <= 31");
     DT_CHECK_ARG(!moments_eval || (eval_stride >= order + 1 && eval_stride % 2 == 0),
                  "eval_stride must be even and >= order + 1");
+    DT_CHECK_ARG(node_capacity >= 1 && node_capacity < (int64_t)1 << 31, "bad node capacity");
     DT_CHECK_ARG(xs && qs && center && start && end && left && right && meta && plan && moments,
                  "null pointer");
+    if (!workspace || workspace_bytes < dt_moments_workspace(node_capacity))
+        return dt_set_error(DT_ERR_WORKSPACE, "moments workspace too small");
     MomArgs a{xs, qs, center, start, end, left, right, meta, order, moments, moments_eval,
-              eval_stride, nullptr, nullptr, plan};
+              eval_stride, (int32_t *)workspace, (int32_t *)workspace + node_capacity, plan};
     return launch_level_moments(a, (cudaStream_t)stream);
 }
 

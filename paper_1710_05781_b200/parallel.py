@@ -164,7 +164,8 @@ class ShardedMoments:
         _lib.check(L.dt_moments_partial(p(xs), p(qs), p(b.center), p(b.start), p(b.end),
                                         p(b.left), p(b.right), p(b.meta), p(self.plan),
                                         self.order, p(self.moments), p(self.meval),
-                                        self.estride, s), "dt_moments_partial")
+                                        self.estride, b.capacity, p(b.mws), b.mws_bytes, s),
+                   "dt_moments_partial")
         _lib.check(L.dt_shard_pack(p(self.plan), self.rank, self.cut, self.order,
                                    p(self.moments), p(self.meval), self.estride, p(self.send), s),
                    "dt_shard_pack")

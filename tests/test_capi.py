@@ -61,7 +61,8 @@ def test_version_and_errors_without_gpu():
                              None, None) == -1
     assert lib.dt_shard_plan(1, 1, 1, 1, 1, 0, None, 0, 1, 1 / 3, 4, 2, 2, 1, None) == -1
     assert b"rank" in lib.dt_last_error()
-    assert lib.dt_moments_partial(1, 1, 1, 1, 1, 1, 1, 1, 1, 32, 1, None, 34, None) == -1
+    assert lib.dt_moments_partial(1, 1, 1, 1, 1, 1, 1, 1, 1, 32, 1, None, 34, 16, 1, 4096,
+                                  None) == -1
     assert b"order <= 31" in lib.dt_last_error()
     assert lib.dt_shard_rows_bytes(-1, 30, 32) == 0
     assert lib.dt_shard_rows_bytes(4, 30, 32) == 16 * 63 * 8
