@@ -89,6 +89,17 @@ int dt_sign_terms(const double *xs, const double *prefix, int64_t n, const doubl
                   double *e_out, int64_t n_targets, void *workspace, size_t workspace_bytes,
                   void *stream);
 
+/* Input validation in one pass (charges.py:114-132 rejects non-finite
+ * positions/strengths; direct.py:43-49 non-finite targets; charges.py:200
+ * and tree.py use ascending order).  flags[0] += number of non-finite
+ * values, flags[1] += number of descents v[i+1] < v[i]; the caller zeroes
+ * flags (2 int64 in device memory).  dt_unpack_pairs also splits
+ * interleaved (x, q) pairs (16-byte aligned) into xs and qs, counting the
+ * descents of x. */
+int dt_check_values(const double *v, int64_t n, int64_t *flags, void *stream);
+int dt_unpack_pairs(const double *pairs, int64_t n, double *xs, double *qs, int64_t *flags,
+                    void *stream);
+
 /* ---------------------------------------------------------------- (b) */
 
 /* Level-synchronous breadth-first bisection tree over sorted xs[0..n)
@@ -239,6 +250,22 @@ int dt_tree_phi_sum_packed(const void *packed_nodes, int64_t n_nodes, const doub
                            int64_t i1, int accumulate, int psel_mode,
                            const dt_eval_stats *stats, void *workspace,
                            size_t workspace_bytes, void *stream);
+
+/* Whole field E(y) = e(y) + phi(y) (tree.py:340-373) in one kernel: the
+ * sign term is computed per target from the sorted sources xs[0..n_src) and
+ * their inclusive prefix sums exactly as dt_sign_terms does, then added to
+ * the traversal sum as evaluate_all does.  ys and out may live in pinned
+ * host memory (UVA): each target is read once and each value written once
+ * over the host link while the traversal runs.  flags (device int64[2], may
+ * be NULL): flags[0] += number of non-finite targets (those are not
+ * traversed; the caller rejects the call). */
+int dt_tree_field_packed(const void *packed_nodes, int64_t n_nodes, const double *moments,
+                         int64_t moment_stride, const double *xq, const double *xs,
+                         const double *prefix, int64_t n_src, double rd2, double theta,
+                         int64_t p, int adaptive, double tol_share, int64_t p_cap,
+                         const double *cos_tab, const double *sin_tab, int64_t n_samples,
+                         const double *ys, double *out, int64_t i0, int64_t i1,
+                         int64_t *flags, void *workspace, size_t workspace_bytes, void *stream);
 
 /* Same traversal on a tree fresh from dt_build_tree without any host
  * round trip: the tree depth (and so tol_share = tolerance / (3 max(depth,1)),

@@ -66,6 +66,8 @@ SIGNATURES = {
     "dt_prefix_scan": (C.c_int, [_P, _P, _I64, _P, _SZ, _P]),
     "dt_sign_terms_workspace": (_SZ, [_I64]),
     "dt_sign_terms": (C.c_int, [_P, _P, _I64, _P, _P, _I64, _P, _SZ, _P]),
+    "dt_check_values": (C.c_int, [_P, _I64, _P, _P]),
+    "dt_unpack_pairs": (C.c_int, [_P, _I64, _P, _P, _P, _P]),
     "dt_build_workspace": (_SZ, [_I64, _I64]),
     "dt_build_tree": (
         C.c_int,
@@ -99,6 +101,11 @@ SIGNATURES = {
         C.c_int,
         [_P, _I64, _P, _I64, _P, _I64, _D, _D, _I64, C.c_int, _D, _I64, _P, _P, _I64, _P,
          _P, _I64, _I64, C.c_int, C.c_int, C.POINTER(EvalStats), _P, _SZ, _P],
+    ),
+    "dt_tree_field_packed": (
+        C.c_int,
+        [_P, _I64, _P, _I64, _P, _P, _P, _I64, _D, _D, _I64, C.c_int, _D, _I64, _P, _P, _I64,
+         _P, _P, _I64, _I64, _P, _P, _SZ, _P],
     ),
     "dt_tree_eval_device": (
         C.c_int,

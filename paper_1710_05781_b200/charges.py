@@ -100,10 +100,23 @@ def from_sorted(xs, qs) -> ChargeSystem:
     return ChargeSystem(xs=x, qs=q, prefix=pre, total=total)
 
 
+def check_values(v: torch.Tensor, flags: torch.Tensor | None = None) -> torch.Tensor:
+    """Enqueue dt_check_values on a contiguous float64 CUDA tensor: returns
+    the device flags (non-finite count, descent count), accumulated into
+    ``flags`` when given."""
+    if flags is None:
+        flags = torch.zeros(2, dtype=torch.int64, device=v.device)
+    if v.numel():
+        _lib.check(_lib.load().dt_check_values(_lib.ptr(v), v.numel(), _lib.ptr(flags),
+                                               _lib.stream_handle()), "dt_check_values")
+    return flags
+
+
 def from_particles(raw) -> ChargeSystem:
     """Sorted ChargeSystem from (x, q) pairs (charges.py:114-132).
 
-    Duplicates are kept in input order (stable sort); NaN/inf rejected.
+    Duplicates are kept in input order (stable sort); NaN/inf rejected.  One
+    device pass splits the pairs and counts non-finite values and descents.
     """
     if not isinstance(raw, torch.Tensor):
         raw = np.asarray(raw, dtype=np.float64)
@@ -112,11 +125,20 @@ def from_particles(raw) -> ChargeSystem:
     if raw.ndim != 2 or raw.shape[1] != 2:
         raise ValueError(f"expected (x, q) pairs, got array of shape {tuple(raw.shape)}")
     arr = _to_device(raw)
-    if not bool(torch.isfinite(arr).all()):
+    if arr.data_ptr() % 16:
+        arr = arr.clone()
+    n = arr.shape[0]
+    x = torch.empty(n, dtype=torch.float64, device=arr.device)
+    q = torch.empty(n, dtype=torch.float64, device=arr.device)
+    flags = torch.zeros(2, dtype=torch.int64, device=arr.device)
+    if n:
+        _lib.check(_lib.load().dt_unpack_pairs(_lib.ptr(arr), n, _lib.ptr(x), _lib.ptr(q),
+                                               _lib.ptr(flags), _lib.stream_handle()),
+                   "dt_unpack_pairs")
+    bad, desc = flags.tolist()
+    if bad:
         raise ValueError("positions and strengths must all be finite")
-    x = arr[:, 0].contiguous()
-    q = arr[:, 1].contiguous()
-    if x.numel() > 1 and not bool((x[1:] >= x[:-1]).all()):
+    if desc:
         x, order = torch.sort(x, stable=True)
         q = q[order].contiguous()
     return from_sorted(x, q)
@@ -144,7 +166,7 @@ def sign_term_all(system: ChargeSystem, targets):
     """e(y) = sum(q_j, x_j < y) - sum(q_j, x_j >= y) for ascending targets
     (charges.py:190-202).  Returns the same kind of array as ``targets``."""
     t, kind = as_targets(targets, check_finite=False)
-    if t.numel() > 1 and not bool((t[1:] >= t[:-1]).all()):
+    if t.numel() > 1 and check_values(t).tolist()[1]:
         raise ValueError("targets must be sorted ascending")
     return kind(_sign_terms(system, t))
 
@@ -165,6 +187,19 @@ def as_targets(targets, check_finite: bool = True):
             raise ValueError(f"targets must be one-dimensional, got shape {arr.shape}")
         back = lambda v: _to_host(v).numpy()  # noqa: E731
         t = _to_device(arr)
-    if check_finite and t.numel() and not bool(torch.isfinite(t).all()):
+    if check_finite and t.numel() and check_values(t).tolist()[0]:
         raise ValueError("targets must all be finite")
     return t, back
+
+
+def host_targets(targets) -> torch.Tensor | None:
+    """The targets as a 1-D float64 CPU tensor when they live on the host
+    (numpy / sequence / CPU tensor), else None."""
+    if isinstance(targets, torch.Tensor):
+        if targets.is_cuda or targets.ndim != 1:
+            return None
+        return targets.to(torch.float64).contiguous()
+    arr = np.asarray(targets, dtype=np.float64)
+    if arr.ndim != 1:
+        return None
+    return torch.from_numpy(np.ascontiguousarray(arr))

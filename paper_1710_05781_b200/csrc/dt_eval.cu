@@ -88,6 +88,11 @@ struct EvalArgs {
     int psel_mode;
     dt_eval_stats stats;
     unsigned long long *counter;
+    // fused field E = e + phi (dt_tree_field_packed): sign term from the
+    // sorted sources and their prefix sums; vflags[0] counts non-finite targets
+    const double *sign_xs, *sign_prefix;
+    int64_t sign_n;
+    int64_t *vflags;
     const int64_t *meta;  // if set: tol_share = tolerance / (3 max(depth, 1)) on device
     double tolerance;
 };
@@ -643,7 +648,16 @@ __global__ void __launch_bounds__(EVAL_THREADS, DT_EVAL_MINB) tree_eval_kernel(E
             break;
         const int64_t i = i_first + lane;
         const bool valid = i < a.i1;
-        const double y = valid ? __ldg(a.ys + i) : 0.0;
+        // plain load: ys may live in mapped (pinned) host memory
+        const double y = valid ? a.ys[i] : 0.0;
+        bool live = valid;
+        if (a.vflags) {  // non-finite targets are counted and not traversed
+            live = valid && isfinite(y);
+            const unsigned bad = __ballot_sync(DT_FULL, valid && !live);
+            if (bad && lane == 0)
+                atomicAdd(reinterpret_cast<unsigned long long *>(a.vflags),
+                          (unsigned long long)__popc(bad));
+        }
         double acc = 0.0;
         uint64_t hh = 0;
         int64_t c_near = 0, c_far = 0, c_sump = 0, c_p0 = 0, c_exact = 0;
@@ -660,7 +674,7 @@ __global__ void __launch_bounds__(EVAL_THREADS, DT_EVAL_MINB) tree_eval_kernel(E
 #endif
         uint2 *const stk = stack_s[threadIdx.x >> 5];
         int node = 0;
-        unsigned mask = __ballot_sync(DT_FULL, valid);
+        unsigned mask = __ballot_sync(DT_FULL, live);
         while (true) {
             const double4 raw0 = *reinterpret_cast<const double4 *>(a.nodes + node);
             const double center = raw0.x, half = raw0.y;
@@ -746,7 +760,19 @@ __global__ void __launch_bounds__(EVAL_THREADS, DT_EVAL_MINB) tree_eval_kernel(E
                 atomicAdd(g_util + k, u_[k]);
 #endif
         if (valid) {
-            a.out[i] = a.accumulate ? a.out[i] + acc : acc;
+            double v;
+            if (a.sign_xs) {  // e(y) exactly as dt_sign_terms, then e + phi
+                double e = 0.0;
+                if (a.sign_n) {
+                    const int64_t idx = dt_lower_bound(a.sign_xs, 0, a.sign_n, y);
+                    const double below = idx == 0 ? 0.0 : __ldg(a.sign_prefix + idx - 1);
+                    e = __dsub_rn(__dmul_rn(2.0, below), __ldg(a.sign_prefix + a.sign_n - 1));
+                }
+                v = e + acc;
+            } else {
+                v = a.accumulate ? a.out[i] + acc : acc;
+            }
+            a.out[i] = v;
             if (STATS) {
                 if (a.stats.hash)
                     a.stats.hash[i] = hh;
@@ -1013,6 +1039,63 @@ extern "C" int dt_tree_phi_sum_packed(const void *packed_nodes, int64_t n_nodes,
         a.stats = dt_eval_stats{nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
     a.counter = (unsigned long long *)workspace;
     return launch_eval(a, adaptive != 0, stats != nullptr, (cudaStream_t)stream);
+}
+
+extern "C" int dt_tree_field_packed(const void *packed_nodes, int64_t n_nodes,
+                                    const double *moments, int64_t moment_stride,
+                                    const double *xq, const double *xs, const double *prefix,
+                                    int64_t n_src, double rd2, double theta, int64_t p,
+                                    int adaptive, double tol_share, int64_t p_cap,
+                                    const double *cos_tab, const double *sin_tab,
+                                    int64_t n_samples, const double *ys, double *out, int64_t i0,
+                                    int64_t i1, int64_t *flags, void *workspace,
+                                    size_t workspace_bytes, void *stream)
+{
+    int rc = check_eval_args(n_nodes, n_src, p, adaptive, tol_share, p_cap, n_samples, rd2,
+                             theta, i0, i1, moment_stride);
+    if (rc != DT_OK)
+        return rc;
+    if (i1 == i0)
+        return DT_OK;
+    DT_CHECK_ARG(packed_nodes && moments && ys && out && (n_src == 0 || (xq && xs && prefix)),
+                 "null pointer");
+    DT_CHECK_ARG(!adaptive || (cos_tab && sin_tab), "null contour tables");
+    if (!workspace || workspace_bytes < DT_EVAL_COUNTER_BYTES)
+        return dt_set_error(DT_ERR_WORKSPACE, "eval workspace too small");
+    for (const void *ptr : {(const void *)ys, (const void *)out}) {
+        cudaPointerAttributes at;
+        DT_CUDA_TRY(cudaPointerGetAttributes(&at, ptr));
+        DT_CHECK_ARG(at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeHost ||
+                         at.type == cudaMemoryTypeManaged,
+                     "ys and out must be device or pinned host memory");
+    }
+    EvalArgs a{};
+    a.nodes = (const dt_node *)packed_nodes;
+    a.n_nodes = n_nodes;
+    a.moments = moments;
+    a.stride = moment_stride;
+    a.xq = (const double2 *)xq;
+    a.rd2 = rd2;
+    a.theta = theta;
+    a.p = (int)p;
+    a.p_cap = (int)p_cap;
+    a.tol_share = adaptive ? tol_share : 1.0;
+    a.cos_tab = cos_tab;
+    a.sin_tab = sin_tab;
+    a.n_samples = (int)n_samples;
+    a.ys = ys;
+    a.out = out;
+    a.i0 = i0;
+    a.i1 = i1;
+    a.accumulate = 0;
+    a.psel_mode = DT_PSEL_FAST;
+    a.stats = dt_eval_stats{nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+    a.counter = (unsigned long long *)workspace;
+    a.sign_xs = xs ? xs : (const double *)ys;  // non-null selects the fused form
+    a.sign_prefix = prefix;
+    a.sign_n = n_src;
+    a.vflags = flags;
+    return launch_eval(a, adaptive != 0, false, (cudaStream_t)stream);
 }
 
 extern "C" int dt_tree_eval_device(const void *packed_nodes, const int64_t *meta,

@@ -6,6 +6,8 @@
 // calls are bit-identical; it differs from the sequential cumsum by
 // round-off (<= ~1e-15 * sum|q| at 2^24).  HBM traffic: 8N (tile sums) +
 // 16N (scan pass) + 16T (sign terms).
+#include <algorithm>
+
 #include "dt_common.cuh"
 
 namespace {
@@ -280,6 +282,89 @@ extern "C" int dt_sign_terms(const double *xs, const double *prefix, int64_t n, 
     }
     sign_terms_kernel<<<(unsigned)nb, SIGN_THREADS, 0, s>>>(xs, prefix, n, ys, e_out, n_targets,
                                                             bracket, nb);
+    DT_CUDA_TRY(cudaGetLastError());
+    return DT_OK;
+}
+
+// ---- input validation (charges.py:114-132 from_particles, direct.py:43-49
+// _as_targets): one pass counting non-finite values and descents, so the
+// host reads back two integers instead of running several torch reductions.
+
+namespace {
+
+__device__ __forceinline__ void add_flags(unsigned long long bad, unsigned long long desc,
+                                          int64_t *flags)
+{
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        bad += __shfl_xor_sync(DT_FULL, bad, o);
+        desc += __shfl_xor_sync(DT_FULL, desc, o);
+    }
+    if (dt_lane() == 0 && (bad | desc)) {
+        if (bad)
+            atomicAdd(reinterpret_cast<unsigned long long *>(flags), bad);
+        if (desc)
+            atomicAdd(reinterpret_cast<unsigned long long *>(flags + 1), desc);
+    }
+}
+
+__global__ void check_values_kernel(const double *__restrict__ v, int64_t n, int64_t *flags)
+{
+    unsigned long long bad = 0, desc = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const double a = __ldg(v + i);
+        bad += !isfinite(a);
+        if (i + 1 < n)
+            desc += __ldg(v + i + 1) < a;
+    }
+    add_flags(bad, desc, flags);
+}
+
+__global__ void unpack_pairs_kernel(const double2 *__restrict__ xq, int64_t n,
+                                    double *__restrict__ xs, double *__restrict__ qs,
+                                    int64_t *flags)
+{
+    unsigned long long bad = 0, desc = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const double2 p = __ldg(xq + i);
+        xs[i] = p.x;
+        qs[i] = p.y;
+        bad += !isfinite(p.x) + !isfinite(p.y);
+        if (i + 1 < n)
+            desc += __ldg(reinterpret_cast<const double *>(xq) + 2 * (i + 1)) < p.x;
+    }
+    add_flags(bad, desc, flags);
+}
+
+}  // namespace
+
+extern "C" int dt_check_values(const double *v, int64_t n, int64_t *flags, void *stream)
+{
+    DT_CHECK_ARG(n >= 0, "negative size");
+    DT_CHECK_ARG(flags, "null flags");
+    if (n == 0)
+        return DT_OK;
+    DT_CHECK_ARG(v, "null pointer");
+    const int64_t blocks = std::min<int64_t>((n + 255) / 256, (int64_t)dt_num_sms() * 8);
+    check_values_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(v, n, flags);
+    DT_CUDA_TRY(cudaGetLastError());
+    return DT_OK;
+}
+
+extern "C" int dt_unpack_pairs(const double *pairs, int64_t n, double *xs, double *qs,
+                               int64_t *flags, void *stream)
+{
+    DT_CHECK_ARG(n >= 0, "negative size");
+    DT_CHECK_ARG(flags, "null flags");
+    if (n == 0)
+        return DT_OK;
+    DT_CHECK_ARG(pairs && xs && qs, "null pointer");
+    DT_CHECK_ARG(((uintptr_t)pairs & 15) == 0, "pairs must be 16-byte aligned");
+    const int64_t blocks = std::min<int64_t>((n + 255) / 256, (int64_t)dt_num_sms() * 8);
+    unpack_pairs_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(
+        (const double2 *)pairs, n, xs, qs, flags);
     DT_CUDA_TRY(cudaGetLastError());
     return DT_OK;
 }

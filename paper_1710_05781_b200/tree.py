@@ -18,7 +18,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from .charges import ChargeSystem, _sign_terms, as_targets
+from .charges import ChargeSystem, _sign_terms, as_targets, check_values, host_targets
 from .direct import FieldResult
 from .kernel import DEFAULT_CONTOUR_SAMPLES, DEFAULT_P_MAX, DiscKernel
 
@@ -351,15 +351,21 @@ def evaluate_all(tree: Tree, kernel: DiscKernel, config: EvalConfig, system: Cha
     bit-identical for any ``threads`` value and any target order; ``threads``
     is accepted for API compatibility (the GPU grid replaces the CPU pool).
     """
-    t, back = as_targets(targets)
     _check_order(tree, config)
+    host = host_targets(targets)
+    if host is not None and host.numel() >= PIPELINE_MIN_TARGETS and _looks_sorted(host):
+        numpy_out = not isinstance(targets, torch.Tensor)
+        if host.is_pinned():
+            return _evaluate_host_mapped(tree, kernel, config, system, host, numpy_out)
+        return _evaluate_host_pipelined(tree, kernel, config, system, host, numpy_out)
+    t, back = as_targets(targets)
     dev = t.device
     torch.cuda.synchronize(dev)
     start = time.perf_counter()
     values = _sign_terms(system, t)
     T = t.numel()
     if T:
-        if T > 1 and not bool((t[1:] >= t[:-1]).all()):
+        if T > 1 and check_values(t).tolist()[1]:
             ys, perm = torch.sort(t)
             vs = values[perm].contiguous()
             tree_phi_sum(tree, kernel, config, ys.contiguous(), vs)
@@ -369,4 +375,125 @@ def evaluate_all(tree: Tree, kernel: DiscKernel, config: EvalConfig, system: Cha
     torch.cuda.synchronize(dev)
     elapsed = time.perf_counter() - start
     return FieldResult(values=back(values), build_time=tree.build_seconds, eval_time=elapsed,
+                       method="tree")
+
+
+# Host targets of at least this many points are streamed in chunks: the
+# host->device copy of chunk i+1 and the device->host copy of chunk i-1
+# overlap the sign term and traversal of chunk i (three CUDA streams).
+PIPELINE_MIN_TARGETS = 1 << 20
+PIPELINE_CHUNK = 1 << 21
+
+
+def _looks_sorted(host: torch.Tensor) -> bool:
+    """Cheap host-side guess (4097 evenly spaced samples) that the targets
+    are ascending; unsorted targets take the sorting path.  Results never
+    depend on it: the traversal is exact for targets in any order."""
+    n = host.numel()
+    idx = torch.linspace(0, n - 1, min(n, 4097)).to(torch.int64)
+    s = host[idx]
+    return bool((s[1:] >= s[:-1]).all())
+
+
+def _evaluate_host_pipelined(tree: Tree, kernel: DiscKernel, config: EvalConfig,
+                             system: ChargeSystem, host: torch.Tensor,
+                             numpy_out: bool) -> FieldResult:
+    dev = _lib.require_device()
+    T = host.numel()
+    src = host if host.is_pinned() else None
+    out_h = torch.empty(T, dtype=torch.float64, pin_memory=True)
+    d_t = torch.empty(T, dtype=torch.float64, device=dev)
+    d_o = torch.empty(T, dtype=torch.float64, device=dev)
+    flags = torch.zeros(2, dtype=torch.int64, device=dev)
+    chunks = [(i, min(T, i + PIPELINE_CHUNK)) for i in range(0, T, PIPELINE_CHUNK)]
+    L = _lib.load()
+    p = _lib.ptr
+    sign_bytes = int(L.dt_sign_terms_workspace(PIPELINE_CHUNK))
+    # two compute streams in turn: chunk i+1's traversal fills the SMs that
+    # chunk i's tail leaves idle (own workspaces per stream)
+    main = torch.cuda.current_stream(dev)
+    comps = [main, torch.cuda.Stream(dev)]
+    sign_ws = [torch.empty(sign_bytes, dtype=torch.uint8, device=dev) for _ in comps]
+    eval_ws = [torch.empty(_lib.DT_EVAL_COUNTER_BYTES, dtype=torch.uint8, device=dev)
+               for _ in comps]
+    s_in, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    ready = torch.cuda.Event()
+    ready.record(main)
+    comps[1].wait_event(ready)  # the tree and flags were made on the main stream
+    torch.cuda.synchronize(dev)
+    start = time.perf_counter()
+    keep = []  # pinned staging buffers stay alive until the copies finish
+    for c, (i0, i1) in enumerate(chunks):
+        comp, k = comps[c % 2], c % 2
+        with torch.cuda.stream(s_in):
+            if src is None:  # pageable input: stage through pinned memory
+                buf = torch.empty(i1 - i0, dtype=torch.float64, pin_memory=True)
+                buf.copy_(host[i0:i1])
+                keep.append(buf)
+                d_t[i0:i1].copy_(buf, non_blocking=True)
+            else:
+                d_t[i0:i1].copy_(src[i0:i1], non_blocking=True)
+            arrived = torch.cuda.Event()
+            arrived.record(s_in)
+        comp.wait_event(arrived)
+        with torch.cuda.stream(comp):
+            # finiteness and order, including the step into this chunk
+            lo = i0 - 1 if i0 else 0
+            _lib.check(L.dt_check_values(p(d_t[lo:i1]), i1 - lo, p(flags),
+                                         _lib.stream_handle()), "dt_check_values")
+            _lib.check(L.dt_sign_terms(p(system.xs), p(system.prefix), len(system),
+                                       p(d_t[i0:i1]), p(d_o[i0:i1]), i1 - i0, p(sign_ws[k]),
+                                       sign_bytes, _lib.stream_handle()), "dt_sign_terms")
+            tree_phi_sum(tree, kernel, config, d_t, d_o, i0=i0, i1=i1, accumulate=True,
+                         workspace=eval_ws[k])
+            done = torch.cuda.Event()
+            done.record(comp)
+        s_out.wait_event(done)
+        with torch.cuda.stream(s_out):
+            out_h[i0:i1].copy_(d_o[i0:i1], non_blocking=True)
+    s_out.synchronize()
+    fin = torch.cuda.Event()
+    fin.record(comps[1])
+    main.wait_event(fin)
+    bad, _ = flags.tolist()
+    elapsed = time.perf_counter() - start
+    if bad:
+        raise ValueError("targets must all be finite")
+    values = out_h.numpy() if numpy_out else out_h
+    return FieldResult(values=values, build_time=tree.build_seconds, eval_time=elapsed,
+                       method="tree")
+
+
+def _evaluate_host_mapped(tree: Tree, kernel: DiscKernel, config: EvalConfig,
+                          system: ChargeSystem, host: torch.Tensor,
+                          numpy_out: bool) -> FieldResult:
+    """Pinned host targets: one fused kernel (dt_tree_field_packed) reads
+    each target over the host link and writes E(y) = e(y) + phi(y) straight
+    into a pinned result buffer; no device copies of targets or results."""
+    dev = _lib.require_device()
+    T = host.numel()
+    out_h = torch.empty(T, dtype=torch.float64, pin_memory=True)
+    flags = torch.zeros(2, dtype=torch.int64, device=dev)
+    ws = torch.empty(_lib.DT_EVAL_COUNTER_BYTES, dtype=torch.uint8, device=dev)
+    cos_t, sin_t = contour_tables(dev)
+    p = _lib.ptr
+    torch.cuda.synchronize(dev)
+    start = time.perf_counter()
+    _lib.check(
+        _lib.load().dt_tree_field_packed(
+            p(tree.packed), len(tree), p(tree.meval), tree.meval.shape[1], p(tree.xq),
+            p(system.xs), p(system.prefix), len(system), kernel.r_d * kernel.r_d,
+            float(config.theta), int(config.p), int(bool(config.adaptive)),
+            _tol_share(tree, config), int(tree.moment_order), p(cos_t), p(sin_t), cos_t.numel(),
+            host.data_ptr(), out_h.data_ptr(), 0, T, p(flags), p(ws), ws.numel(),
+            _lib.stream_handle(),
+        ),
+        "dt_tree_field_packed",
+    )
+    bad, _ = flags.tolist()  # synchronises
+    elapsed = time.perf_counter() - start
+    if bad:
+        raise ValueError("targets must all be finite")
+    values = out_h.numpy() if numpy_out else out_h
+    return FieldResult(values=values, build_time=tree.build_seconds, eval_time=elapsed,
                        method="tree")
