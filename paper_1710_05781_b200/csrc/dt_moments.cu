@@ -472,8 +472,14 @@ __global__ void __launch_bounds__(128) p2m_thread_kernel(MomArgs a)
 // flight, then a butterfly over the G lanes.  Leaves are gathered per warp
 // from 32 consecutive node slots (ballot) so no group idles on internal
 // nodes.  Raw power sums S_k = sum q (x - c)^k in registers.
+#ifndef DT_P2M_HALVES
+#define DT_P2M_HALVES 0
+#endif
+#ifndef DT_P2M_MINB
+#define DT_P2M_MINB 1
+#endif
 template <int G>
-__global__ void __launch_bounds__(256) p2m_group_kernel(MomArgs a)
+__global__ void __launch_bounds__(256, DT_P2M_MINB) p2m_group_kernel(MomArgs a)
 {
     const int lane = dt_lane();
     const int sub = lane & (G - 1), grp = lane / G;
@@ -522,6 +528,73 @@ __global__ void __launch_bounds__(256) p2m_group_kernel(MomArgs a)
                 e = __ldg(a.end + node);
                 c = __ldg(a.center + node);
             }
+#if DT_P2M_HALVES
+            // orders in two halves of 16 (half the accumulator registers);
+            // the second half starts from q t^16 (four squarings)
+#pragma unroll 1
+            for (int h = 0; h < 2; ++h) {
+                const int kb = 16 * h;
+                if (kb >= o1)
+                    break;
+                double acc[16];
+#pragma unroll
+                for (int k = 0; k < 16; ++k)
+                    acc[k] = 0.0;
+                int64_t j = s + sub;
+                for (; j + 3 * G < e; j += 4 * G) {
+                    const double t0 = __ldg(a.xs + j) - c, t1 = __ldg(a.xs + j + G) - c;
+                    const double t2 = __ldg(a.xs + j + 2 * G) - c;
+                    const double t3 = __ldg(a.xs + j + 3 * G) - c;
+                    double w0 = __ldg(a.qs + j), w1 = __ldg(a.qs + j + G);
+                    double w2 = __ldg(a.qs + j + 2 * G), w3 = __ldg(a.qs + j + 3 * G);
+                    if (h) {
+                        double u0 = t0 * t0, u1 = t1 * t1, u2 = t2 * t2, u3 = t3 * t3;
+                        u0 *= u0; u1 *= u1; u2 *= u2; u3 *= u3;
+                        u0 *= u0; u1 *= u1; u2 *= u2; u3 *= u3;
+                        w0 *= u0 * u0; w1 *= u1 * u1; w2 *= u2 * u2; w3 *= u3 * u3;
+                    }
+#pragma unroll
+                    for (int k = 0; k < 16; ++k) {
+                        if (kb + k < o1) {
+                            acc[k] += (w0 + w1) + (w2 + w3);
+                            w0 *= t0;
+                            w1 *= t1;
+                            w2 *= t2;
+                            w3 *= t3;
+                        }
+                    }
+                }
+                for (; j < e; j += G) {
+                    const double t0 = __ldg(a.xs + j) - c;
+                    double w0 = __ldg(a.qs + j);
+                    if (h) {
+                        double u0 = t0 * t0;
+                        u0 *= u0;
+                        u0 *= u0;
+                        w0 *= u0 * u0;
+                    }
+#pragma unroll
+                    for (int k = 0; k < 16; ++k) {
+                        if (kb + k < o1) {
+                            acc[k] += w0;
+                            w0 *= t0;
+                        }
+                    }
+                }
+#pragma unroll
+                for (int k = 0; k < 16; ++k) {
+#pragma unroll
+                    for (int o = G / 2; o > 0; o >>= 1)
+                        acc[k] += __shfl_xor_sync(DT_FULL, acc[k], o);
+                }
+                if (active) {
+#pragma unroll
+                    for (int k = 0; k < 16; ++k)
+                        if ((k & (G - 1)) == sub && kb + k < o1)
+                            put_raw_sum(a, node, kb + k, acc[k]);
+                }
+            }
+#else
             double acc[REG_ORDER];
 #pragma unroll
             for (int k = 0; k < REG_ORDER; ++k)
@@ -566,6 +639,7 @@ __global__ void __launch_bounds__(256) p2m_group_kernel(MomArgs a)
                     if ((k & (G - 1)) == sub && k < o1)
                         put_raw_sum(a, node, k, acc[k]);
             }
+#endif
         }
     }
 }

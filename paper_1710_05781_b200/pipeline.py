@@ -60,6 +60,8 @@ class TreePipeline:
         self.sign_ws_bytes = int(L.dt_sign_terms_workspace(self.T))
         self.sign_ws = torch.empty(self.sign_ws_bytes, dtype=torch.uint8, device=self.dev)
         self.cos_t, self.sin_t = contour_tables(self.dev)
+        self.side = torch.cuda.Stream(self.dev)
+        self.ev_start, self.ev_scan, self.ev_side = (torch.cuda.Event() for _ in range(3))
         # world > 1: sharded upward pass (one all-gather of cut-level rows)
         self.shard = None
         if world > 1:
@@ -98,21 +100,32 @@ class TreePipeline:
             i1 = ys.numel()
         L = _lib.load()
         p = _lib.ptr
+        main = torch.cuda.current_stream(self.dev)
         s = _lib.stream_handle()
         cfg = self.config
-        _lib.check(L.dt_prefix_scan(p(qs), p(self.prefix), self.n, p(self.scan_ws),
-                                    self.scan_ws_bytes, s), "dt_prefix_scan")
         ys_part = ys[i0:i1]
         out_part = out[i0:i1]
-        _lib.check(L.dt_sign_terms(p(xs), p(self.prefix), self.n, p(ys_part), p(out_part),
-                                   i1 - i0, p(self.sign_ws), self.sign_ws_bytes, s),
-                   "dt_sign_terms")
+        # side stream: (x, q) interleave and, after the scan, the sign term --
+        # both overlap the latency-bound build and upward pass
+        self.ev_start.record(main)
+        self.side.wait_event(self.ev_start)
+        with torch.cuda.stream(self.side):
+            pack_sources(xs, qs, self.xq)
+        _lib.check(L.dt_prefix_scan(p(qs), p(self.prefix), self.n, p(self.scan_ws),
+                                    self.scan_ws_bytes, s), "dt_prefix_scan")
+        self.ev_scan.record(main)
+        self.side.wait_event(self.ev_scan)
+        with torch.cuda.stream(self.side):
+            _lib.check(L.dt_sign_terms(p(xs), p(self.prefix), self.n, p(ys_part), p(out_part),
+                                       i1 - i0, p(self.sign_ws), self.sign_ws_bytes,
+                                       _lib.stream_handle()), "dt_sign_terms")
+            self.ev_side.record(self.side)
         self.bufs.launch(xs, cfg.leaf_capacity)
         if self.shard is None:
             launch_moments(self.bufs, xs, qs, self.order, self.moments, self.meval)
         else:  # this rank's subtrees + all-gather of the cut-level rows
             self.shard.launch(xs, qs, ys_part, targets_sorted=True)
-        pack_sources(xs, qs, self.xq)
+        main.wait_event(self.ev_side)
         if eval_events is not None:
             eval_events[0].record()
         _lib.check(
