@@ -100,6 +100,21 @@ int dt_check_values(const double *v, int64_t n, int64_t *flags, void *stream);
 int dt_unpack_pairs(const double *pairs, int64_t n, double *xs, double *qs, int64_t *flags,
                     void *stream);
 
+/* Charge assembly on the device (SURVEY.md §8(f) "next" #2).
+ * dt_density_nodes: charges.py:135-161 from_density -- one (x, q) pair per
+ * Gauss-Legendre node of each of `cells` cells on [a, b], interleaved into
+ * pairs[2 cells order] in ascending order; values has cells (per-cell
+ * constants) or cells + 1 entries (endpoint tabulation, np.interp); nodes and
+ * weights are leggauss(order) on [-1, 1] (device arrays).  Bit-identical to
+ * the reference's numpy arithmetic.
+ * dt_mirror_charges: charges.py:164-180 with_images for one plane --
+ * xm = 2 plane - xs, qm = -qs, keep = |xm - plane| < gap. */
+int dt_density_nodes(double a, double b, int64_t cells, const double *values, int64_t n_values,
+                     int64_t order, const double *nodes, const double *weights, double eps0,
+                     double *pairs, void *stream);
+int dt_mirror_charges(const double *xs, const double *qs, int64_t n, double plane, double gap,
+                      double *xm, double *qm, uint8_t *keep, void *stream);
+
 /* ---------------------------------------------------------------- (b) */
 
 /* Level-synchronous breadth-first bisection tree over sorted xs[0..n)

@@ -68,6 +68,8 @@ SIGNATURES = {
     "dt_sign_terms": (C.c_int, [_P, _P, _I64, _P, _P, _I64, _P, _SZ, _P]),
     "dt_check_values": (C.c_int, [_P, _I64, _P, _P]),
     "dt_unpack_pairs": (C.c_int, [_P, _I64, _P, _P, _P, _P]),
+    "dt_density_nodes": (C.c_int, [_D, _D, _I64, _P, _I64, _I64, _P, _P, _D, _P, _P]),
+    "dt_mirror_charges": (C.c_int, [_P, _P, _I64, _D, _D, _P, _P, _P, _P]),
     "dt_build_workspace": (_SZ, [_I64, _I64]),
     "dt_build_tree": (
         C.c_int,

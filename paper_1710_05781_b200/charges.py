@@ -203,3 +203,107 @@ def host_targets(targets) -> torch.Tensor | None:
     if arr.ndim != 1:
         return None
     return torch.from_numpy(np.ascontiguousarray(arr))
+
+
+# ---------------------------------------------------------------- assembly
+# Charge assembly on the device (SURVEY.md §8(f) "next" #2): the step before
+# the hot path, so a time-stepping loop never leaves the GPU.
+
+MAX_QUADRATURE_ORDER = 16  # charges.py:111
+
+
+@dataclass(frozen=True)
+class DensitySpec:
+    """Line charge density discretised by Gauss-Legendre quadrature
+    (charges.py:58-88): ``values`` holds one constant per cell (length
+    ``cells``) or endpoint values (length ``cells + 1``, linear in between)."""
+
+    domain: tuple
+    cells: int
+    values: object
+    quadrature_order: int
+    eps0: float = 8.8541878128e-12
+
+    def __post_init__(self) -> None:
+        a, b = self.domain
+        if not (np.isfinite(a) and np.isfinite(b) and a < b):
+            raise ValueError(f"domain must be a finite interval, got {self.domain!r}")
+        if self.cells < 1:
+            raise ValueError(f"cells must be >= 1, got {self.cells!r}")
+        if self.quadrature_order < 1:
+            raise ValueError(f"quadrature_order must be >= 1, got {self.quadrature_order!r}")
+        if self.eps0 <= 0:
+            raise ValueError(f"eps0 must be positive, got {self.eps0!r}")
+        n_values = len(self.values)
+        if n_values not in (self.cells, self.cells + 1):
+            raise ValueError(
+                f"values must have length cells ({self.cells}) for per-cell constants "
+                f"or cells + 1 ({self.cells + 1}) for endpoint tabulation, got {n_values}"
+            )
+
+
+@dataclass(frozen=True)
+class ImageSpec:
+    """Mirror charges across one or two electrode planes (charges.py:91-108)."""
+
+    gap_length: float
+    lower_electrode: float = 0.0
+    reflect_lower: bool = True
+    reflect_upper: bool = True
+
+    def __post_init__(self) -> None:
+        if not (np.isfinite(self.gap_length) and self.gap_length > 0):
+            raise ValueError(f"gap_length must be positive, got {self.gap_length!r}")
+        if not np.isfinite(self.lower_electrode):
+            raise ValueError(f"lower_electrode must be finite, got {self.lower_electrode!r}")
+
+
+def from_density(spec: DensitySpec) -> ChargeSystem:
+    """One charge per Gauss-Legendre node (charges.py:135-161), generated on
+    the device (dt_density_nodes, numpy's arithmetic) and passed through
+    from_particles; positions and strengths are bit-identical to the
+    reference's."""
+    if not 1 <= spec.quadrature_order <= MAX_QUADRATURE_ORDER:
+        raise ValueError(
+            f"quadrature_order must be in 1..{MAX_QUADRATURE_ORDER}, got {spec.quadrature_order}"
+        )
+    dev = _lib.require_device()
+    a, b = spec.domain
+    nodes, weights = np.polynomial.legendre.leggauss(spec.quadrature_order)
+    values = _to_device(spec.values if isinstance(spec.values, torch.Tensor)
+                        else np.asarray(spec.values, dtype=np.float64))
+    nd = torch.from_numpy(nodes).to(dev)
+    wt = torch.from_numpy(weights).to(dev)
+    n = spec.cells * spec.quadrature_order
+    pairs = torch.empty((n, 2), dtype=torch.float64, device=dev)
+    _lib.check(_lib.load().dt_density_nodes(
+        float(a), float(b), int(spec.cells), _lib.ptr(values), values.numel(),
+        int(spec.quadrature_order), _lib.ptr(nd), _lib.ptr(wt), float(spec.eps0),
+        _lib.ptr(pairs), _lib.stream_handle()), "dt_density_nodes")
+    return from_particles(pairs)
+
+
+def with_images(system: ChargeSystem, spec: ImageSpec) -> ChargeSystem:
+    """Add sign-flipped mirror charges across the enabled electrode planes
+    (charges.py:164-180): originals, then the kept lower images, then the
+    kept upper images, stably sorted (from_particles)."""
+    planes = []
+    if spec.reflect_lower:
+        planes.append(spec.lower_electrode)
+    if spec.reflect_upper:
+        planes.append(spec.lower_electrode + spec.gap_length)
+    xs_parts, qs_parts = [system.xs], [system.qs]
+    n = len(system)
+    for plane in planes:
+        xm = torch.empty_like(system.xs)
+        qm = torch.empty_like(system.qs)
+        keep = torch.empty(n, dtype=torch.uint8, device=system.xs.device)
+        _lib.check(_lib.load().dt_mirror_charges(
+            _lib.ptr(system.xs), _lib.ptr(system.qs), n, float(plane), float(spec.gap_length),
+            _lib.ptr(xm), _lib.ptr(qm), _lib.ptr(keep), _lib.stream_handle()),
+            "dt_mirror_charges")
+        k = keep.bool()
+        xs_parts.append(xm[k])
+        qs_parts.append(qm[k])
+    pairs = torch.stack([torch.cat(xs_parts), torch.cat(qs_parts)], dim=1).contiguous()
+    return from_particles(pairs)

@@ -368,3 +368,118 @@ extern "C" int dt_unpack_pairs(const double *pairs, int64_t n, double *xs, doubl
     DT_CUDA_TRY(cudaGetLastError());
     return DT_OK;
 }
+
+// ---- charge assembly on the device (SURVEY.md §8(f) "next" #2) ----
+//
+// from_density (charges.py:135-161): one charge per Gauss-Legendre node,
+// x = mid_c + (dx/2) node_j, q = ((0.5 w_j) sigma(x)) dx / (2 eps0), with
+// numpy's operation order (edges = a + dx*i, mids = 0.5 (e_c + e_c+1),
+// np.interp for endpoint tabulation: slope (x - e_j) + v_j).  The pairs come
+// out interleaved, in ascending cell/node order, ready for dt_unpack_pairs.
+// with_images (charges.py:164-180): mirrored = 2 plane - x, kept iff
+// |mirrored - plane| < gap.
+
+namespace {
+
+__global__ void density_nodes_kernel(double a, double dx, int64_t cells,
+                                     const double *__restrict__ values, int per_cell, int order,
+                                     const double *__restrict__ nodes,
+                                     const double *__restrict__ weights, double two_eps0,
+                                     double2 *__restrict__ pairs)
+{
+    const int64_t n = cells * order;
+    const double hdx = __dmul_rn(0.5, dx);
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t c = i / order;
+        const int j = (int)(i - c * order);
+        const double e0 = __dadd_rn(a, __dmul_rn(dx, (double)c));
+        const double e1 = __dadd_rn(a, __dmul_rn(dx, (double)(c + 1)));
+        const double x = __dadd_rn(__dmul_rn(0.5, __dadd_rn(e0, e1)), __dmul_rn(hdx, nodes[j]));
+        double sigma;
+        if (per_cell) {
+            sigma = values[c];
+        } else {
+            // np.interp(x, edges, values): k = last edge <= x (edges ascending)
+            int64_t lo = 0, hi = cells + 1;  // search in [0, cells]
+            while (hi - lo > 1) {
+                const int64_t mid = (lo + hi) >> 1;
+                const double em = __dadd_rn(a, __dmul_rn(dx, (double)mid));
+                if (em <= x)
+                    lo = mid;
+                else
+                    hi = mid;
+            }
+            const int64_t k = lo;
+            const double ek = __dadd_rn(a, __dmul_rn(dx, (double)k));
+            if (x < __dadd_rn(a, 0.0) || k >= cells) {
+                sigma = x < a ? values[0] : values[cells];
+            } else if (ek == x) {
+                sigma = values[k];
+            } else {
+                const double ek1 = __dadd_rn(a, __dmul_rn(dx, (double)(k + 1)));
+                const double slope = __ddiv_rn(__dsub_rn(values[k + 1], values[k]),
+                                               __dsub_rn(ek1, ek));
+                sigma = __dadd_rn(__dmul_rn(slope, __dsub_rn(x, ek)), values[k]);
+                if (isnan(sigma)) {
+                    sigma = __dadd_rn(__dmul_rn(slope, __dsub_rn(x, ek1)), values[k + 1]);
+                    if (isnan(sigma) && values[k] == values[k + 1])
+                        sigma = values[k];
+                }
+            }
+        }
+        const double q = __ddiv_rn(
+            __dmul_rn(__dmul_rn(__dmul_rn(0.5, weights[j]), sigma), dx), two_eps0);
+        pairs[i] = make_double2(x, q);
+    }
+}
+
+__global__ void mirror_kernel(const double *__restrict__ xs, const double *__restrict__ qs,
+                              int64_t n, double plane, double gap, double *__restrict__ xm,
+                              double *__restrict__ qm, uint8_t *__restrict__ keep)
+{
+    const double two_plane = __dmul_rn(2.0, plane);
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const double m = __dsub_rn(two_plane, xs[i]);
+        xm[i] = m;
+        qm[i] = -qs[i];
+        keep[i] = fabs(__dsub_rn(m, plane)) < gap;
+    }
+}
+
+}  // namespace
+
+extern "C" int dt_density_nodes(double a, double b, int64_t cells, const double *values,
+                                int64_t n_values, int64_t order, const double *nodes,
+                                const double *weights, double eps0, double *pairs, void *stream)
+{
+    DT_CHECK_ARG(cells >= 1 && order >= 1 && order <= 16, "bad cells / quadrature order");
+    DT_CHECK_ARG(n_values == cells || n_values == cells + 1, "values must have cells or cells+1 entries");
+    DT_CHECK_ARG(eps0 > 0.0 && a < b, "bad eps0 / domain");
+    DT_CHECK_ARG(values && nodes && weights && pairs, "null pointer");
+    DT_CHECK_ARG(((uintptr_t)pairs & 15) == 0, "pairs must be 16-byte aligned");
+    const double dx = (b - a) / (double)cells;  // host IEEE division, as numpy
+    const int64_t n = cells * order;
+    const int64_t blocks = std::min<int64_t>((n + 255) / 256, (int64_t)dt_num_sms() * 8);
+    density_nodes_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(
+        a, dx, cells, values, n_values == cells ? 1 : 0, (int)order, nodes, weights, 2.0 * eps0,
+        (double2 *)pairs);
+    DT_CUDA_TRY(cudaGetLastError());
+    return DT_OK;
+}
+
+extern "C" int dt_mirror_charges(const double *xs, const double *qs, int64_t n, double plane,
+                                 double gap, double *xm, double *qm, uint8_t *keep, void *stream)
+{
+    DT_CHECK_ARG(n >= 0, "negative size");
+    if (n == 0)
+        return DT_OK;
+    DT_CHECK_ARG(xs && qs && xm && qm && keep, "null pointer");
+    DT_CHECK_ARG(gap > 0.0, "gap_length must be positive");
+    const int64_t blocks = std::min<int64_t>((n + 255) / 256, (int64_t)dt_num_sms() * 8);
+    mirror_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(xs, qs, n, plane, gap, xm,
+                                                                      qm, keep);
+    DT_CUDA_TRY(cudaGetLastError());
+    return DT_OK;
+}
