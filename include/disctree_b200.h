@@ -219,6 +219,13 @@ typedef struct dt_eval_stats {
     int64_t *sum_p;      /* sum of truncation orders over accepted far nodes     */
     int64_t *n_p0;       /* accepted far nodes with p_use == 0                   */
     int64_t *n_exact;    /* far nodes whose order came from the exact replica    */
+    /* a-posteriori bound audit (SURVEY.md §8(f) "next" #4): per target the sum
+     * over accepted far nodes of bound_value(M, R, h, p_use) * sum_node |q|
+     * (kernel.py:130-182, test_tree.py:216-250) with M the exact contour
+     * supremum (rigorous); needs abs_prefix = inclusive prefix sums of |q_j|
+     * over the sorted sources. */
+    double *bound;
+    const double *abs_prefix;
 } dt_eval_stats;
 
 /* Interleave (x_j, q_j) into xq[2n] for the traversal kernel. */

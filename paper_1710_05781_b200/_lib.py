@@ -54,6 +54,8 @@ class EvalStats(C.Structure):
         ("sum_p", _P),
         ("n_p0", _P),
         ("n_exact", _P),
+        ("bound", _P),
+        ("abs_prefix", _P),
     ]
 
 

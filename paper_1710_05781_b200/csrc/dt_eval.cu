@@ -562,6 +562,22 @@ __device__ __forceinline__ double near_field(const double2 *__restrict__ xq, int
     return (a0 + a1) + (a2 + a3);
 }
 
+// a-posteriori audit: the paper's truncation bound bound_value(M, R, h, p) =
+// M R/(R-h) (h/R)^(p+1) (kernel.py:130-134) times sum_node |q|, with M the
+// exact supremum of |f| on the contour (kernel.py:147-150, test_kernel.py:
+// 153-163): sqrt(R/r_d) if r_d <= 2R, else 2R/sqrt(4R^2 + r_d^2).  The
+// reference's sampled contour maximum can fall below the supremum when
+// r_d << R, so the exact value makes the audit rigorous.
+__device__ double audit_bound(const EvalArgs &a, double R, double h, int p, int s, int e)
+{
+    const double rd = sqrt(a.rd2);
+    const double M = rd <= 2.0 * R ? sqrt(R / rd) : 2.0 * R / sqrt(4.0 * R * R + a.rd2);
+    const double value = M * (R / (R - h)) * pow(h / R, (double)(p + 1));
+    const double qa =
+        __ldg(a.stats.abs_prefix + e - 1) - (s > 0 ? __ldg(a.stats.abs_prefix + s - 1) : 0.0);
+    return value * qa;
+}
+
 // interaction-set hash (see oracle.c): sum of splitmix64 over event codes
 __device__ __forceinline__ uint64_t mix64(uint64_t z)
 {
@@ -661,6 +677,7 @@ __global__ void __launch_bounds__(EVAL_THREADS, DT_EVAL_MINB) tree_eval_kernel(E
         double acc = 0.0;
         uint64_t hh = 0;
         int64_t c_near = 0, c_far = 0, c_sump = 0, c_p0 = 0, c_exact = 0;
+        double c_bound = 0.0;
 
         // Warp-uniform DFS (left subtree first, _kernels.py:199-264) over the
         // union of the 32 targets' traversals, one lane mask per entry.  An
@@ -723,6 +740,8 @@ __global__ void __launch_bounds__(EVAL_THREADS, DT_EVAL_MINB) tree_eval_kernel(E
                         ++c_far;
                         c_sump += pu;
                         c_p0 += pu == 0;
+                        if (a.stats.bound)
+                            c_bound += audit_bound(a, big_r, half, pu, se.x, se.y);
                     }
                 }
             }
@@ -786,6 +805,8 @@ __global__ void __launch_bounds__(EVAL_THREADS, DT_EVAL_MINB) tree_eval_kernel(E
                     a.stats.n_p0[i] = c_p0;
                 if (a.stats.n_exact)
                     a.stats.n_exact[i] = c_exact;
+                if (a.stats.bound)
+                    a.stats.bound[i] = c_bound;
             }
         }
     }
@@ -1036,7 +1057,7 @@ extern "C" int dt_tree_phi_sum_packed(const void *packed_nodes, int64_t n_nodes,
     if (stats)
         a.stats = *stats;
     else
-        a.stats = dt_eval_stats{nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+        a.stats = dt_eval_stats{nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
     a.counter = (unsigned long long *)workspace;
     return launch_eval(a, adaptive != 0, stats != nullptr, (cudaStream_t)stream);
 }
@@ -1089,7 +1110,7 @@ extern "C" int dt_tree_field_packed(const void *packed_nodes, int64_t n_nodes,
     a.i1 = i1;
     a.accumulate = 0;
     a.psel_mode = DT_PSEL_FAST;
-    a.stats = dt_eval_stats{nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+    a.stats = dt_eval_stats{nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
     a.counter = (unsigned long long *)workspace;
     a.sign_xs = xs ? xs : (const double *)ys;  // non-null selects the fused form
     a.sign_prefix = prefix;
@@ -1140,7 +1161,7 @@ extern "C" int dt_tree_eval_device(const void *packed_nodes, const int64_t *meta
     a.i1 = i1;
     a.accumulate = accumulate;
     a.psel_mode = DT_PSEL_FAST;
-    a.stats = dt_eval_stats{nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+    a.stats = dt_eval_stats{nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
     a.counter = (unsigned long long *)workspace;
     return launch_eval(a, adaptive != 0, false, (cudaStream_t)stream);
 }

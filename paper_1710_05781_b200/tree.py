@@ -497,3 +497,27 @@ def _evaluate_host_mapped(tree: Tree, kernel: DiscKernel, config: EvalConfig,
     values = out_h.numpy() if numpy_out else out_h
     return FieldResult(values=values, build_time=tree.build_seconds, eval_time=elapsed,
                        method="tree")
+
+
+def evaluate_with_bound(tree: Tree, kernel: DiscKernel, config: EvalConfig,
+                        system: ChargeSystem, targets: torch.Tensor):
+    """Field and a-posteriori truncation bound per target on the device
+    (SURVEY.md §8(f) "next" #4): E(y) as evaluate_all, plus
+    B(y) = sum over accepted far nodes of bound_value(M, R, h, p_use) *
+    sum_node |q| (kernel.py:130-182) with the exact contour supremum M, so
+    |E_tree(y) - E_direct(y)| <= B(y) up to round-off can be checked at any
+    size without a CPU replay (test_tree.py:216-250 does it node by node).
+    Returns (values, bounds) as device tensors."""
+    from .charges import prefix_sum
+
+    t, _ = as_targets(targets)
+    _check_order(tree, config)
+    values = _sign_terms(system, t)
+    bounds = torch.zeros_like(t)
+    if t.numel():
+        abs_pre = prefix_sum(system.qs.abs())
+        st = _lib.EvalStats(None, None, None, None, None, None, bounds.data_ptr(),
+                            abs_pre.data_ptr())
+        tree_phi_sum(tree, kernel, config, t, values, stats=st)
+        torch.cuda.synchronize(t.device)
+    return values, bounds
