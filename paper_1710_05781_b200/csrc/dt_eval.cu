@@ -420,19 +420,26 @@ __device__ __forceinline__ double far_sum(const FarPre &f, const double2 *__rest
     const double g1 = f.g1, g2 = f.g2, g3 = f.g3;
     const double2 m01 = __ldg(M2);
     double acc = f.g0 * m01.x;
-    if (pmax < 1)
-        return acc;
-    if (pu >= 1)
+    if (pmin >= 3) {  // every far lane needs orders 0..3: no guards
+        const double2 m23 = __ldg(M2 + 1);
         acc = __fma_rn(g1, m01.y, acc);
-    if (pmax < 2)
-        return acc;
-    const double2 m23 = __ldg(M2 + 1);
-    if (pu >= 2)
         acc = __fma_rn(g2, m23.x, acc);
-    if (pmax < 3)
-        return acc;
-    if (pu >= 3)
         acc = __fma_rn(g3, m23.y, acc);
+    } else {
+        if (pmax < 1)
+            return acc;
+        if (pu >= 1)
+            acc = __fma_rn(g1, m01.y, acc);
+        if (pmax < 2)
+            return acc;
+        const double2 m23 = __ldg(M2 + 1);
+        if (pu >= 2)
+            acc = __fma_rn(g2, m23.x, acc);
+        if (pmax < 3)
+            return acc;
+        if (pu >= 3)
+            acc = __fma_rn(g3, m23.y, acc);
+    }
     // The g_{k-2}, g_{k-3} part of each step is formed off the critical
     // path: the recurrence carries one dependent DFMA per order; a second
     // accumulator halves the accumulation chain.
