@@ -24,7 +24,10 @@ namespace cg = cooperative_groups;
 namespace {
 
 constexpr int BUILD_THREADS = 512;
-constexpr int SMALL_LEVEL = 4 * BUILD_THREADS;  // nodes handled by block 0 alone
+#ifndef DT_BUILD_SMALL
+#define DT_BUILD_SMALL (2 * BUILD_THREADS)
+#endif
+constexpr int SMALL_LEVEL = DT_BUILD_SMALL;  // nodes handled by block 0 alone
 
 struct BuildArgs {
     const double *xs;
@@ -39,7 +42,19 @@ struct BuildArgs {
     int32_t *scratch_off;    // [capacity] local exclusive offset within the block chunk
     int32_t *scratch_split;  // [capacity] split index found in phase A
     int64_t *block_total;    // [gridDim]
+    int64_t *dy_split;       // [DYADIC] global lower_bound of each top dyadic midpoint
+    double *dy_mid;          // [DYADIC] that midpoint
 };
+
+// Splits of the top dyadic levels, all at once.  The bisection intervals do
+// not depend on the data (only which of them become nodes does), and for a
+// node with source range [s, e) and midpoint mid,
+//     lower_bound(xs[s:e], mid) = clamp(lower_bound(xs[0:n], mid), s, e)
+// because xs is sorted.  So the lower_bounds of the 2^(K+1) - 1 midpoints of
+// levels 0..K are found by independent searches in one parallel phase
+// instead of K + 1 dependent rounds of DRAM-latency binary searches.
+constexpr int DYADIC_LEVELS = 12;  // levels 0..11
+constexpr int DYADIC = (1 << DYADIC_LEVELS) - 1;
 
 __device__ __forceinline__ double mid_of(double lo, double hi)
 {
@@ -77,6 +92,40 @@ __device__ void write_node(const BuildArgs &a, int64_t c, double lo, double hi, 
 __device__ __forceinline__ int64_t ld_cg(const int64_t *p) { return __ldcg(p); }
 __device__ __forceinline__ double ld_cg(const double *p) { return __ldcg(p); }
 
+// Root interval (tree.py:173-175): [x0 - pad, x_last + pad].
+__device__ __forceinline__ void root_interval(const BuildArgs &a, double *lo, double *hi)
+{
+    const double x0 = a.xs[0], xl = a.xs[a.n - 1];
+    const double m = fmax(1.0, fmax(fabs(x0), fabs(xl)));
+    const double pad = __dmul_rn(1e-12, m);
+    *lo = __dsub_rn(x0, pad);
+    *hi = __dadd_rn(xl, pad);
+}
+
+// Phase 0: dy_mid / dy_split for dyadic interval idx (level L = floor(log2(idx + 1)),
+// position k = idx + 1 - 2^L), following the same midpoint arithmetic as the build.
+__device__ void dyadic_splits(const BuildArgs &a)
+{
+    double lo0, hi0;
+    root_interval(a, &lo0, &hi0);
+    for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < DYADIC;
+         idx += gridDim.x * blockDim.x) {
+        const int L = 31 - __clz(idx + 1);
+        const int k = idx + 1 - (1 << L);
+        double lo = lo0, hi = hi0;
+        for (int b = L - 1; b >= 0; --b) {
+            const double mid = mid_of(lo, hi);
+            if ((k >> b) & 1)
+                lo = mid;
+            else
+                hi = mid;
+        }
+        const double mid = mid_of(lo, hi);
+        a.dy_mid[idx] = mid;
+        a.dy_split[idx] = dt_lower_bound(a.xs, 0, a.n, mid);
+    }
+}
+
 // Number of children of frontier node `node` (0 if it is a leaf) and split.
 __device__ __forceinline__ int node_children(const BuildArgs &a, int64_t node, int64_t lev,
                                              int64_t *split_out)
@@ -84,8 +133,25 @@ __device__ __forceinline__ int node_children(const BuildArgs &a, int64_t node, i
     int64_t s = ld_cg(a.start + node), e = ld_cg(a.end + node);
     if (e - s <= a.leaf_capacity || lev >= a.max_depth)
         return 0;
-    double mid = mid_of(ld_cg(a.lo + node), ld_cg(a.hi + node));
-    int64_t split = dt_lower_bound(a.xs, s, e, mid);
+    const double lo = ld_cg(a.lo + node), hi = ld_cg(a.hi + node);
+    double mid = mid_of(lo, hi);
+    int64_t split = -1;
+    if (lev < DYADIC_LEVELS) {
+        // dyadic position of the node from its lower bound; used only if the
+        // recorded midpoint is exactly this node's midpoint
+        double lo0 = ld_cg(a.lo + 0), hi0 = ld_cg(a.hi + 0);
+        const double pos = (lo - lo0) / (hi0 - lo0) * (double)(1 << lev);
+        const int k = (int)rint(pos);
+        if (k >= 0 && k < (1 << lev)) {
+            const int idx = (1 << lev) - 1 + k;
+            if (__ldcg(a.dy_mid + idx) == mid) {
+                const int64_t g = __ldcg(a.dy_split + idx);
+                split = g < s ? s : (g > e ? e : g);
+            }
+        }
+    }
+    if (split < 0)
+        split = dt_lower_bound(a.xs, s, e, mid);
     *split_out = split;
     return (split > s) + (e > split);
 }
@@ -193,15 +259,22 @@ __global__ void __launch_bounds__(BUILD_THREADS) build_kernel(BuildArgs a)
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         // tree.py:173-175: pad = 1e-12 * max(1.0, |x0|, |x_last|)
-        const double x0 = a.xs[0], xl = a.xs[a.n - 1];
-        const double m = fmax(1.0, fmax(fabs(x0), fabs(xl)));
-        const double pad = __dmul_rn(1e-12, m);
-        write_node(a, 0, __dsub_rn(x0, pad), __dadd_rn(xl, pad), 0, 0, a.n);
+        double lo0, hi0;
+        root_interval(a, &lo0, &hi0);
+        write_node(a, 0, lo0, hi0, 0, 0, a.n);
     }
+    dyadic_splits(a);
     grid.sync();
 
     int64_t lev = 0;
     while (lev <= a.max_depth) {
+#ifdef DT_BUILD_TRACE
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            a.block_total[2048 + lev] = (int64_t)t;
+        }
+#endif
         int64_t f0 = meta[DT_META_LEVEL0 + lev];
         int64_t f1 = meta[DT_META_LEVEL0 + lev + 1];
         int64_t F = f1 - f0;
@@ -218,6 +291,13 @@ __global__ void __launch_bounds__(BUILD_THREADS) build_kernel(BuildArgs a)
                     int64_t Fl = g1 - g0;
                     if (Fl == 0 || Fl > SMALL_LEVEL || l > a.max_depth)
                         break;
+#ifdef DT_BUILD_TRACE
+                    if (threadIdx.x == 0) {
+                        unsigned long long t;
+                        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+                        a.block_total[2048 + l] = (int64_t)t;
+                    }
+#endif
                     int64_t made = level_in_block(a, g0, g1, l, warp_sums, &leaves);
                     __syncthreads();
                     if (made < 0) {
@@ -327,7 +407,8 @@ __global__ void __launch_bounds__(BUILD_THREADS) build_kernel(BuildArgs a)
 extern "C" size_t dt_build_workspace(int64_t n, int64_t node_capacity)
 {
     (void)n;
-    return (size_t)node_capacity * 2 * sizeof(int32_t) + 4096 * sizeof(int64_t) + 16;
+    return (size_t)node_capacity * 2 * sizeof(int32_t) + 4096 * sizeof(int64_t) + 16 +
+           (size_t)DYADIC * (sizeof(int64_t) + sizeof(double));
 }
 
 extern "C" int dt_build_tree(const double *xs, int64_t n, int64_t leaf_capacity, int64_t max_depth, int64_t node_capacity,
@@ -370,6 +451,8 @@ extern "C" int dt_build_tree(const double *xs, int64_t n, int64_t leaf_capacity,
     a.block_total = (int64_t *)((char *)workspace + (size_t)node_capacity * 2 * sizeof(int32_t));
     // 8-byte align block_total
     a.block_total = (int64_t *)(((uintptr_t)a.block_total + 7) & ~(uintptr_t)7);
+    a.dy_split = a.block_total + 4096;
+    a.dy_mid = (double *)(a.dy_split + DYADIC);
 
     int dev = 0, per_sm = 0;
     DT_CUDA_TRY(cudaGetDevice(&dev));

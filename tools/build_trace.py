@@ -1,0 +1,26 @@
+"""Per-level timestamps of build_kernel (variant DT_BUILD_TRACE; dev aid)."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+
+from paper_1710_05781_b200 import workloads as W
+from paper_1710_05781_b200.tree import TreeBuffers, initial_node_capacity
+
+w = W.cfg2()
+xs = torch.from_numpy(w.xs).cuda()
+bufs = TreeBuffers(len(xs), initial_node_capacity(len(xs), 64), xs.device)
+for _ in range(3):
+    bufs.launch(xs, 64)
+torch.cuda.synchronize()
+cap = bufs.capacity
+# workspace: scratch_off[cap] i32, scratch_split[cap] i32, block_total[4096] i64
+bt = bufs.ws.view(torch.uint8)[cap * 8: cap * 8 + 4096 * 8].view(torch.int64).cpu().numpy()
+depth = int(bufs.meta[1])
+t = bt[2048: 2048 + depth + 2]
+lv = bufs.meta[8: 8 + depth + 2].cpu().numpy()
+print("per-level us (level: nodes us):")
+for l in range(depth + 1):
+    print(l, int(lv[l + 1] - lv[l]), round((t[l + 1] - t[l]) / 1e3, 1) if t[l + 1] > t[l] else None)
