@@ -211,6 +211,11 @@ def build_sharded(system, kernel, config, ys_local: torch.Tensor, world: int, ra
         ys_local = ys_local.to(system.xs.device, non_blocking=True)
 
     def upward(bufs, order, moments, meval):
+        if order + 1 > 32:  # the sharded pass covers orders <= 31: form every row
+            from .tree import launch_moments
+
+            launch_moments(bufs, system.xs, system.qs, order, moments, meval)
+            return
         moments.fill_(float("nan"))
         meval.fill_(float("nan"))
         ShardedMoments(bufs, order, moments, meval, meval.shape[1], config.theta, world, rank,

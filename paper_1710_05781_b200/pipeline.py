@@ -64,7 +64,7 @@ class TreePipeline:
         self.ev_start, self.ev_scan, self.ev_side = (torch.cuda.Event() for _ in range(3))
         # world > 1: sharded upward pass (one all-gather of cut-level rows)
         self.shard = None
-        if world > 1:
+        if world > 1 and self.order + 1 <= 32:  # higher orders: replicated moments
             from .parallel import ShardedMoments
 
             self.shard = ShardedMoments(self.bufs, self.order, self.moments, self.meval,

@@ -343,3 +343,45 @@ def test_sharded_evaluation_is_partition_invariant(dt):
     for world in (2, 3, 8):
         parts = [run(*shard_bounds(ys.numel(), world, r)) for r in range(world)]
         assert torch.equal(torch.cat(parts), base)
+
+
+@pytest.mark.parametrize("p,adaptive,tol", [(40, False, 1e-10), (45, True, 1e-14),
+                                             (64, False, 1e-10)])
+def test_high_order_paths(dt, p, adaptive, tol):
+    """Moment orders above 31: the warp-per-leaf dataflow upward pass and the
+    wide (rolled) far-field loop.  Interaction lists hash-identical to the
+    oracle, moments and field within the usual tolerances."""
+    from oracle import oracle as O
+    from paper_1710_05781_b200 import _lib
+    from paper_1710_05781_b200.tree import tree_phi_sum
+
+    g = load_case("rand_default")
+    xs, qs = g["xs"], g["qs"]
+    system = dt.from_sorted(xs, qs)
+    r_d = 0.05
+    kernel = dt.DiscKernel(r_d)
+    cfg = dt.EvalConfig(p=p, leaf_capacity=16, adaptive=adaptive, tolerance=tol)
+    tree = dt.build(system, kernel, cfg)
+    assert tree.moment_order == p
+    otree = O.build(xs, qs, p, 16, adaptive)
+    m, om = tree.moments.cpu().numpy(), otree.moments
+    # relative to each row's scale sum|q| r^k / k!
+    r = np.maximum(np.abs(otree.hi - otree.center), np.abs(otree.center - otree.lo))
+    from math import factorial
+    scale = np.array([[np.abs(qs[s:e]).sum() * rk ** k / factorial(k) for k in range(p + 1)]
+                      for s, e, rk in zip(otree.start, otree.end, r)])
+    assert np.max(np.abs(m - om) / np.maximum(scale, 1e-300)) <= 1e-12
+    t = np.sort(np.random.default_rng(4).uniform(xs[0] - 0.1, xs[-1] + 0.1, 3000))
+    ys = torch.from_numpy(t).cuda()
+    out = torch.zeros_like(ys)
+    names = ("hash", "near_pairs", "n_far", "sum_p", "n_p0", "n_exact")
+    bufs = {k: torch.zeros(len(t), dtype=torch.int64, device="cuda") for k in names}
+    st = _lib.EvalStats(*[bufs[k].data_ptr() for k in names])
+    tree_phi_sum(tree, kernel, cfg, ys, out, accumulate=False, stats=st)
+    otree.moments = m  # same moments: the difference is the far-field arithmetic only
+    phi_o, ost = O.tree_phi_sum(otree, xs, qs, r_d ** 2, cfg.theta, p, adaptive,
+                                O.tol_share(tol, otree.depth), t, instrument=True)
+    np.testing.assert_array_equal(bufs["hash"].cpu().numpy().view(np.uint64), ost.hash)
+    np.testing.assert_array_equal(bufs["sum_p"].cpu().numpy(), ost.sum_p)
+    assert bufs["sum_p"].sum().item() > 0
+    assert np.max(np.abs(out.cpu().numpy() - phi_o)) <= 1e-12 * np.abs(qs).sum()
