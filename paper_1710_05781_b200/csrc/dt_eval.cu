@@ -51,9 +51,6 @@ namespace {
 #define DT_EVAL_SEGMENTS 148  // per-SM task segments (0: one global counter)
 #endif
 static_assert(DT_EVAL_SEGMENTS * 4 <= DT_EVAL_COUNTER_BYTES, "counter slot too small");
-#ifndef DT_FAR_MASKED_CHUNKS
-#define DT_FAR_MASKED_CHUNKS 0
-#endif
 #ifndef DT_EVAL_UTIL
 #define DT_EVAL_UTIL 0  // development: lane-utilisation counters (variant builds only)
 #endif
@@ -460,33 +457,6 @@ __device__ __forceinline__ double far_sum(const FarPre &f, const double2 *__rest
         else                                                                      \
             acc = __fma_rn(OUT, mm_.x, acc);                                      \
     }
-#if DT_FAR_MASKED_CHUNKS
-        // one loop to the warp maximum: orders above a lane's own pu are
-        // computed but not accumulated (predicated FMA)
-#define DT_FAR_MSTEP(KK, G3, G2, G1, OUT)                                         \
-    const double OUT = __fma_rn(__fma_rn(a0, c_rcp[(KK) - 1], -ci), G1,           \
-                                __fma_rn(-ir3, G2, -inv * G3));                   \
-    if ((KK) <= pu) {                                                             \
-        const double2 mm_ = __ldg(M2 + (KK) / 2);                                 \
-        if ((KK) & 1)                                                             \
-            acc1 = __fma_rn(OUT, mm_.y, acc1);                                    \
-        else                                                                      \
-            acc = __fma_rn(OUT, mm_.x, acc);                                      \
-    }
-#pragma unroll
-        for (int kk = 4; kk + 2 <= 31; kk += 3) {
-            if (kk > pmax)
-                break;
-            DT_FAR_MSTEP(kk, gm3, gm2, gm1, v0)
-            DT_FAR_MSTEP(kk + 1, gm2, gm1, v0, v1)
-            DT_FAR_MSTEP(kk + 2, gm1, v0, v1, v2)
-            gm3 = v0;
-            gm2 = v1;
-            gm1 = v2;
-            k = kk + 3;
-        }
-#undef DT_FAR_MSTEP
-#else
 #pragma unroll
         for (int kk = 4; kk + 2 <= 31; kk += 3) {
             if (kk + 2 > pmin)
@@ -499,7 +469,6 @@ __device__ __forceinline__ double far_sum(const FarPre &f, const double2 *__rest
             gm1 = v2;
             k = kk + 3;
         }
-#endif
 #undef DT_FAR_STEP
     }
     // remaining orders up to the warp maximum, masked per lane; even orders
@@ -530,23 +499,13 @@ __device__ __forceinline__ double far_field(double d, double rd2, const double2 
     return far_sum<WIDE>(far_setup(d, rd2), M2, pu, pmin, pmax);
 }
 
-#ifndef DT_NEAR_FMA
-#define DT_NEAR_FMA 0
-#endif
-#if DT_NEAR_FMA
-// acc + q (x - y) / sqrt((x - y)^2 + r_d^2): 9 FP64 instructions + MUFU
-__device__ __forceinline__ double near_term(double2 u, double y, double rd2, double acc)
-{
-    const double du = u.x - y;
-    return __fma_rn(u.y * du, dt_rsqrt(__fma_rn(du, du, rd2)), acc);
-}
-#else
+// acc + q (x - y) / sqrt((x - y)^2 + r_d^2) (nvcc contracts the final
+// product and sum into one DFMA): 9 FP64 instructions + MUFU
 __device__ __forceinline__ double near_term(double2 u, double y, double rd2, double acc)
 {
     const double du = u.x - y;
     return acc + u.y * du * dt_rsqrt(__fma_rn(du, du, rd2));
 }
-#endif
 
 // Leaf sources [s, e): four (x, q) broadcast loads in flight per step.
 __device__ __forceinline__ double near_field(const double2 *__restrict__ xq, int s, int e,

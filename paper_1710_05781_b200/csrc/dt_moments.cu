@@ -1,40 +1,31 @@
-// (c) Upward pass: P2M at the leaves, M2M (binomial shift) per level.
+// (c) Upward pass: P2M at the leaves, M2M (binomial shift) bottom-up.
 //
 // Reference: tree.py:224-238 computes every node's moments
 //     m_k = sum_j q_j (x_j - c)^k / k!,   k = 0..order,
 // directly from its own sources, level by level (O(depth * N * order)).
-// Here each leaf is formed from its sources (one warp per leaf, coalesced
-// loads, per-lane register accumulators, smem transpose-reduce), then each
-// internal node is the sum of its children shifted to its center:
+// Here each leaf is formed from its sources and each internal node is the
+// sum of its children shifted to its center,
 //     m_k(parent) = sum_{j<=k} m_j(child) * delta^(k-j) / (k-j)!,
 //     delta = c_child - c_parent,
-// bottom-up as a dataflow, with no grid barriers: the warp that finishes a
-// node bumps its parent's arrival counter, and the warp that completes the
-// parent's last child goes on to form the parent (BVH-refit style).
+// computed on raw power sums S_k = k! m_k, where the shift is the binomial
+// transform S'_k = sum_j C(k,j) delta^(k-j) S_j, applied in place as 31
+// passes of Pascal's rule S_k += delta S_(k-1).
+//   order + 1 <= 32: P2M with 4 lanes per leaf (p2m_group_kernel), then a
+//     barrier-free dataflow (m2m_flow_kernel): every leaf bumps its parent's
+//     arrival counter; the warp whose arrival completes a parent forms it
+//     (lane k = order k) and climbs on.  The shard plan (multi-GPU) restricts
+//     both to one rank's subtrees; shard_finish_kernel forms the levels above
+//     the cut with the same arithmetic, thread per node.
+//   higher orders: warp per leaf + the same dataflow with a Toeplitz shift.
 // The shift is exact algebra; round-off differs from the reference's direct
 // sums at the 1e-16 level of sum|q| r^k / k!.
 // Algorithmic HBM bytes: P2M 16 N + 8 (order+1) leaves; M2M 24 (order+1)
 // per internal node (two child rows read, one row written).
-#include <cooperative_groups.h>
 
 #include "dt_common.cuh"
 
-namespace cg = cooperative_groups;
-
-#ifndef DT_MOM_V2
-#define DT_MOM_V2 1  // G lanes per leaf P2M + thread-per-node Pascal M2M (order <= 31)
-#endif
 #ifndef DT_P2M_G
 #define DT_P2M_G 4
-#endif
-#ifndef DT_M2M_MODE
-#define DT_M2M_MODE 2  // 0 level-sync, 1 thread dataflow, 2 warp dataflow, 3 narrow/wide phases
-#endif
-#ifndef DT_M2M_W32
-#define DT_M2M_W32 1  // level kernel: 32 parents per warp, rows staged in shared memory
-#endif
-#ifndef DT_M2M_FLOW_CHUNK
-#define DT_M2M_FLOW_CHUNK 32
 #endif
 
 namespace {
@@ -390,96 +381,15 @@ __global__ void __launch_bounds__(MOM_THREADS) moments_kernel(MomArgs a)
     }
 }
 
-// ---- order + 1 <= 32: thread-per-leaf P2M + level-synchronous M2M ----
-
-// P2M with one thread per leaf: raw power sums S_k = sum q (x - c)^k in
-// registers, two sources in flight (independent multiply chains), no
-// shuffles or shared memory.
-__global__ void __launch_bounds__(128) p2m_thread_kernel(MomArgs a)
-{
-    const int64_t n = __ldg(a.meta + DT_META_NODES);
-    const int o1 = (int)a.order + 1;
-    // shard plan: leaves above the cut always, below it only inside [lo, hi)
-    int64_t cut_begin = INT64_MAX, lo = 0, hi = 0;
-    if (a.plan) {
-        cut_begin = __ldg(a.plan + DT_PLAN_LEVEL_BEGIN);
-        lo = __ldg(a.plan + DT_PLAN_SRC_LO);
-        hi = __ldg(a.plan + DT_PLAN_SRC_HI);
-    }
-    for (int64_t node = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; node < n;
-         node += (int64_t)gridDim.x * blockDim.x) {
-        if (__ldg(a.left + node) >= 0 || __ldg(a.right + node) >= 0)
-            continue;
-        const int64_t s = __ldg(a.start + node), e = __ldg(a.end + node);
-        if (node >= cut_begin && (s < lo || e > hi))
-            continue;
-        const double c = __ldg(a.center + node);
-        double acc[REG_ORDER];
-#pragma unroll
-        for (int k = 0; k < REG_ORDER; ++k)
-            acc[k] = 0.0;
-        int64_t j = s;
-        for (; j + 3 < e; j += 4) {
-            const double t0 = __ldg(a.xs + j) - c, t1 = __ldg(a.xs + j + 1) - c;
-            const double t2 = __ldg(a.xs + j + 2) - c, t3 = __ldg(a.xs + j + 3) - c;
-            double w0 = __ldg(a.qs + j), w1 = __ldg(a.qs + j + 1);
-            double w2 = __ldg(a.qs + j + 2), w3 = __ldg(a.qs + j + 3);
-#pragma unroll
-            for (int k = 0; k < REG_ORDER; ++k) {
-                if (k < o1) {
-                    acc[k] += (w0 + w1) + (w2 + w3);
-                    w0 *= t0;
-                    w1 *= t1;
-                    w2 *= t2;
-                    w3 *= t3;
-                }
-            }
-        }
-        for (; j + 1 < e; j += 2) {
-            const double t0 = __ldg(a.xs + j) - c, t1 = __ldg(a.xs + j + 1) - c;
-            double w0 = __ldg(a.qs + j), w1 = __ldg(a.qs + j + 1);
-#pragma unroll
-            for (int k = 0; k < REG_ORDER; ++k) {
-                if (k < o1) {
-                    acc[k] += w0 + w1;
-                    w0 *= t0;
-                    w1 *= t1;
-                }
-            }
-        }
-        if (j < e) {
-            const double t0 = __ldg(a.xs + j) - c;
-            double w0 = __ldg(a.qs + j);
-#pragma unroll
-            for (int k = 0; k < REG_ORDER; ++k) {
-                if (k < o1) {
-                    acc[k] += w0;
-                    w0 *= t0;
-                }
-            }
-        }
-#pragma unroll
-        for (int k = 0; k < REG_ORDER; ++k)
-            if (k < o1)
-                put_raw_sum(a, node, k, acc[k]);
-    }
-}
-
-// ---- v2: G lanes per leaf (P2M), thread per node (M2M, in-place Pascal) ----
+// ---- order + 1 <= 32: G lanes per leaf (P2M), dataflow M2M (in-place Pascal) ----
 
 // P2M with G consecutive lanes per leaf: each lane sums every G-th source of
 // the leaf (the group's loads cover contiguous sectors), four sources in
 // flight, then a butterfly over the G lanes.  Leaves are gathered per warp
 // from 32 consecutive node slots (ballot) so no group idles on internal
 // nodes.  Raw power sums S_k = sum q (x - c)^k in registers.
-#ifndef DT_P2M_HALVES
-#define DT_P2M_HALVES 0
-#endif
-#ifndef DT_P2M_MINB
-#define DT_P2M_MINB 1
-#endif
 template <int G>
-__global__ void __launch_bounds__(256, DT_P2M_MINB) p2m_group_kernel(MomArgs a)
+__global__ void __launch_bounds__(256) p2m_group_kernel(MomArgs a)
 {
     const int lane = dt_lane();
     const int sub = lane & (G - 1), grp = lane / G;
@@ -528,73 +438,6 @@ __global__ void __launch_bounds__(256, DT_P2M_MINB) p2m_group_kernel(MomArgs a)
                 e = __ldg(a.end + node);
                 c = __ldg(a.center + node);
             }
-#if DT_P2M_HALVES
-            // orders in two halves of 16 (half the accumulator registers);
-            // the second half starts from q t^16 (four squarings)
-#pragma unroll 1
-            for (int h = 0; h < 2; ++h) {
-                const int kb = 16 * h;
-                if (kb >= o1)
-                    break;
-                double acc[16];
-#pragma unroll
-                for (int k = 0; k < 16; ++k)
-                    acc[k] = 0.0;
-                int64_t j = s + sub;
-                for (; j + 3 * G < e; j += 4 * G) {
-                    const double t0 = __ldg(a.xs + j) - c, t1 = __ldg(a.xs + j + G) - c;
-                    const double t2 = __ldg(a.xs + j + 2 * G) - c;
-                    const double t3 = __ldg(a.xs + j + 3 * G) - c;
-                    double w0 = __ldg(a.qs + j), w1 = __ldg(a.qs + j + G);
-                    double w2 = __ldg(a.qs + j + 2 * G), w3 = __ldg(a.qs + j + 3 * G);
-                    if (h) {
-                        double u0 = t0 * t0, u1 = t1 * t1, u2 = t2 * t2, u3 = t3 * t3;
-                        u0 *= u0; u1 *= u1; u2 *= u2; u3 *= u3;
-                        u0 *= u0; u1 *= u1; u2 *= u2; u3 *= u3;
-                        w0 *= u0 * u0; w1 *= u1 * u1; w2 *= u2 * u2; w3 *= u3 * u3;
-                    }
-#pragma unroll
-                    for (int k = 0; k < 16; ++k) {
-                        if (kb + k < o1) {
-                            acc[k] += (w0 + w1) + (w2 + w3);
-                            w0 *= t0;
-                            w1 *= t1;
-                            w2 *= t2;
-                            w3 *= t3;
-                        }
-                    }
-                }
-                for (; j < e; j += G) {
-                    const double t0 = __ldg(a.xs + j) - c;
-                    double w0 = __ldg(a.qs + j);
-                    if (h) {
-                        double u0 = t0 * t0;
-                        u0 *= u0;
-                        u0 *= u0;
-                        w0 *= u0 * u0;
-                    }
-#pragma unroll
-                    for (int k = 0; k < 16; ++k) {
-                        if (kb + k < o1) {
-                            acc[k] += w0;
-                            w0 *= t0;
-                        }
-                    }
-                }
-#pragma unroll
-                for (int k = 0; k < 16; ++k) {
-#pragma unroll
-                    for (int o = G / 2; o > 0; o >>= 1)
-                        acc[k] += __shfl_xor_sync(DT_FULL, acc[k], o);
-                }
-                if (active) {
-#pragma unroll
-                    for (int k = 0; k < 16; ++k)
-                        if ((k & (G - 1)) == sub && kb + k < o1)
-                            put_raw_sum(a, node, kb + k, acc[k]);
-                }
-            }
-#else
             double acc[REG_ORDER];
 #pragma unroll
             for (int k = 0; k < REG_ORDER; ++k)
@@ -639,7 +482,6 @@ __global__ void __launch_bounds__(256, DT_P2M_MINB) p2m_group_kernel(MomArgs a)
                     if ((k & (G - 1)) == sub && k < o1)
                         put_raw_sum(a, node, k, acc[k]);
             }
-#endif
         }
     }
 }
@@ -696,7 +538,7 @@ __global__ void __launch_bounds__(256) m2m_flow_kernel(MomArgs a)
     }
     const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    constexpr int CH = DT_M2M_FLOW_CHUNK;  // nodes scanned per warp step
+    constexpr int CH = 32;  // nodes scanned per warp step
     for (int64_t r0 = gwarp * CH; r0 < n; r0 += nwarps * CH) {
         // deepest levels first: their chains are the critical path
         const int64_t c0 = n - CH - r0;  // may be negative for the last chunk
@@ -741,93 +583,6 @@ __global__ void __launch_bounds__(256) m2m_flow_kernel(MomArgs a)
     }
 }
 
-// Arrival on a parent's counter with acquire-release semantics at GPU scope:
-// publishes this thread's row writes and, for the completing arrival, makes
-// the siblings' rows visible.
-__device__ __forceinline__ int arrive_acq_rel(int32_t *ctr)
-{
-    int old;
-    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(ctr) : "memory");
-    return old;
-}
-
-// Thread-per-node form of one internal node (same arithmetic as
-// m2m_level_threads / m2m_form_warp).
-__device__ __forceinline__ void m2m_form_thread(const MomArgs &a, int64_t node)
-{
-    const int o1 = (int)a.order + 1;
-    const int64_t l = __ldg(a.left + node), r = __ldg(a.right + node);
-    const double c = __ldg(a.center + node);
-    double out[REG_ORDER];
-#pragma unroll
-    for (int k = 0; k < REG_ORDER; ++k)
-        out[k] = 0.0;
-#pragma unroll 1
-    for (int ci = 0; ci < 2; ++ci) {
-        const int64_t ch = ci == 0 ? l : r;
-        if (ch < 0)
-            continue;
-        const double delta = __ldg(a.center + ch) - c;
-        const double *row = a.moments + ch * o1;
-        double S[REG_ORDER];
-#pragma unroll
-        for (int k = 0; k < REG_ORDER; ++k)
-            S[k] = k < o1 ? __ldcg(row + k) : 0.0;
-#pragma unroll
-        for (int k = 0; k < REG_ORDER; ++k)
-            S[k] = __dmul_rn(S[k], c_fact_km1[k + 1]);
-#pragma unroll
-        for (int i = 1; i < REG_ORDER; ++i) {
-#pragma unroll
-            for (int k = REG_ORDER - 1; k >= i; --k)
-                S[k] = __fma_rn(delta, S[k - 1], S[k]);
-        }
-#pragma unroll
-        for (int k = 0; k < REG_ORDER; ++k)
-            out[k] += S[k];
-    }
-#pragma unroll
-    for (int k = 0; k < REG_ORDER; ++k)
-        if (k < o1)
-            put_raw_sum(a, node, k, out[k]);
-}
-
-// Dataflow upward pass, thread granularity: the thread whose arrival
-// completes a parent forms it (in-register Pascal shift) and climbs on.
-// Sibling leaves sit in the same warp, so the first climbs run 16 lanes wide.
-__global__ void __launch_bounds__(128) m2m_flow_thread_kernel(MomArgs a)
-{
-    const int64_t n = __ldg(a.meta + DT_META_NODES);
-    int64_t cut_begin = 0, lo = 0, hi = 0;
-    if (a.plan) {
-        cut_begin = __ldg(a.plan + DT_PLAN_LEVEL_BEGIN);
-        lo = __ldg(a.plan + DT_PLAN_SRC_LO);
-        hi = __ldg(a.plan + DT_PLAN_SRC_HI);
-    }
-    // deepest levels first: their chains are the critical path
-    for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < n;
-         idx += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t mine = n - 1 - idx;
-        if (__ldg(a.left + mine) >= 0 || __ldg(a.right + mine) >= 0)
-            continue;
-        int64_t P = __ldcg(a.parent + mine);
-        if (P < cut_begin || P < 0)
-            continue;
-        if (a.plan && (__ldg(a.start + mine) < lo || __ldg(a.end + mine) > hi))
-            continue;
-        while (true) {
-            const int need = (__ldg(a.left + P) >= 0) + (__ldg(a.right + P) >= 0);
-            if (arrive_acq_rel(a.arrived + P) != need - 1)
-                break;
-            m2m_form_thread(a, P);
-            const int64_t q = __ldcg(a.parent + P);
-            if (q < cut_begin || q < 0)
-                break;
-            P = q;
-        }
-    }
-}
-
 // M2M of one level with one thread per internal node, on raw power sums:
 // S'_k = sum_j C(k, j) delta^(k-j) S_j (the binomial transform) computed in
 // place by k passes of S_k += delta S_(k-1) over descending k (Pascal's
@@ -860,24 +615,16 @@ __device__ __forceinline__ void m2m_level_threads(const MomArgs &a, int64_t f0, 
             double S[REG_ORDER];
 #pragma unroll
             for (int k = 0; k < REG_ORDER; ++k)
-#ifdef DT_M2M_NOLOAD
-                S[k] = delta * k;
-#elif defined(DT_M2M_LDG)
-                S[k] = k < o1 ? __ldg(row + k) : 0.0;
-#else
                 S[k] = k < o1 ? __ldcg(row + k) : 0.0;
-#endif
 #pragma unroll
             for (int k = 0; k < REG_ORDER; ++k)
                 S[k] = __dmul_rn(S[k], c_fact_km1[k + 1]);
-#ifndef DT_M2M_NOPASCAL
 #pragma unroll
             for (int i = 1; i < REG_ORDER; ++i) {
 #pragma unroll
                 for (int k = REG_ORDER - 1; k >= i; --k)
                     S[k] = __fma_rn(delta, S[k - 1], S[k]);
             }
-#endif
 #pragma unroll
             for (int k = 0; k < REG_ORDER; ++k)
                 out[k] += S[k];
@@ -886,353 +633,6 @@ __device__ __forceinline__ void m2m_level_threads(const MomArgs &a, int64_t f0, 
         for (int k = 0; k < REG_ORDER; ++k)
             if (k < o1)
                 put_raw_sum(a, node, k, out[k]);
-    }
-}
-
-// One level, 32 consecutive parents per warp, lane = parent: the children of
-// consecutive parents are consecutive nodes, so their rows (<= 64) are one
-// contiguous block that the warp stages through shared memory with
-// coalesced loads; each lane shifts its children in registers (Pascal's
-// rule on raw sums, same arithmetic as m2m_level_threads) and the 32 output
-// rows leave through shared memory as coalesced (masked) stores.
-constexpr int M2M_BUF = 64 * REG_ORDER;  // doubles of staging per warp
-
-// dst[r * w + c] = buf[r * w + c] for rows r < rows with bit r of mask set
-// (w <= 32: one coalesced store per row).
-__device__ __forceinline__ void masked_rows_store(double *dst, const double *buf, int rows, int w,
-                                                  unsigned mask)
-{
-    const int lane = dt_lane();
-    if (lane >= w)
-        return;
-#pragma unroll 4
-    for (int r = 0; r < rows; ++r)
-        if ((mask >> r) & 1u)
-            dst[r * w + lane] = buf[r * w + lane];
-}
-
-__device__ __forceinline__ void m2m_level_warps32(const MomArgs &a, int64_t f0, int64_t f1,
-                                                  int64_t gwarp, int64_t nwarps, bool filter,
-                                                  int64_t src_lo, int64_t src_hi, double *buf)
-{
-    const int lane = dt_lane();
-    const int o1 = (int)a.order + 1;
-    const int es = a.meval ? (int)a.estride : 0;
-#ifdef DT_M2M_TRACE2
-    unsigned long long *tr = reinterpret_cast<unsigned long long *>(a.arrived) + 64 + 8 * (f0 & 63);
-    const bool rec = blockIdx.x == 0 && threadIdx.x == 0;
-#define TSTAMP(slot)                                                      \
-    if (rec) {                                                            \
-        unsigned long long t_;                                            \
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));           \
-        tr[slot] = t_;                                                    \
-    }
-#else
-#define TSTAMP(slot)
-#endif
-    for (int64_t p0 = f0 + gwarp * 32; p0 < f1; p0 += nwarps * 32) {
-        TSTAMP(0)
-        const int64_t node = p0 + lane;
-        int64_t l = -1, r = -1;
-        bool act = false;
-        if (node < f1) {
-            l = __ldg(a.left + node);
-            r = __ldg(a.right + node);
-            act = l >= 0 || r >= 0;
-            if (act && filter)
-                act = __ldg(a.start + node) >= src_lo && __ldg(a.end + node) <= src_hi;
-        }
-        const unsigned am = __ballot_sync(DT_FULL, act);
-        if (!am)
-            continue;
-        const int first = act ? (int)(l >= 0 ? l : r) : INT32_MAX;
-        const int last = act ? (int)(r >= 0 ? r : l) : -1;
-        const int c_lo = __reduce_min_sync(DT_FULL, first);
-        const int c_hi = __reduce_max_sync(DT_FULL, last) + 1;
-        const double *src = a.moments + (int64_t)c_lo * o1;
-        // one coalesced row per load, 16 rows in flight before the first
-        // shared-memory store
-        const int nrows = c_hi - c_lo;
-        if (lane < o1) {
-            for (int r0 = 0; r0 < nrows; r0 += 16) {
-                double v[16];
-#pragma unroll
-                for (int j = 0; j < 16; ++j)
-                    v[j] = r0 + j < nrows ? __ldcg(src + (r0 + j) * o1 + lane) : 0.0;
-#pragma unroll
-                for (int j = 0; j < 16; ++j)
-                    if (r0 + j < nrows)
-                        buf[(r0 + j) * o1 + lane] = v[j];
-            }
-        }
-        __syncwarp();
-        TSTAMP(1)
-        double out[REG_ORDER];
-#pragma unroll
-        for (int k = 0; k < REG_ORDER; ++k)
-            out[k] = 0.0;
-        if (act) {
-            const double c = __ldg(a.center + node);
-#pragma unroll 1
-            for (int ci = 0; ci < 2; ++ci) {
-                const int64_t ch = ci == 0 ? l : r;
-                if (ch < 0)
-                    continue;
-                const double delta = __ldg(a.center + ch) - c;
-                const double *row = buf + (ch - c_lo) * o1;
-                double S[REG_ORDER];
-#pragma unroll
-                for (int k = 0; k < REG_ORDER; ++k)
-                    S[k] = k < o1 ? __dmul_rn(row[k], c_fact_km1[k + 1]) : 0.0;
-#pragma unroll
-                for (int i = 1; i < REG_ORDER; ++i) {
-#pragma unroll
-                    for (int k = REG_ORDER - 1; k >= i; --k)
-                        S[k] = __fma_rn(delta, S[k - 1], S[k]);
-                }
-#pragma unroll
-                for (int k = 0; k < REG_ORDER; ++k)
-                    out[k] += S[k];
-            }
-        }
-        __syncwarp();
-        TSTAMP(2)
-        // m_k = S_k / k!  (tree.py's moments), coalesced masked store
-        if (act) {
-#pragma unroll
-            for (int k = 0; k < REG_ORDER; ++k)
-                if (k < o1)
-                    buf[lane * o1 + k] = __dmul_rn(out[k], c_inv_fact[k]);
-        }
-        __syncwarp();
-        const int rows = (int)min((int64_t)32, f1 - p0);
-        masked_rows_store(a.moments + p0 * o1, buf, rows, o1, am);
-        if (es) {
-            __syncwarp();
-            // traversal copy M'_k = S_k / k (M'_0 = S_0), zero padded
-            if (act) {
-#pragma unroll
-                for (int k = 0; k < REG_ORDER; ++k)
-                    if (k < es)
-                        buf[lane * es + k] = k == 0 ? out[0]
-                                                    : (k < o1 ? __dmul_rn(out[k], c_inv_k[k]) : 0.0);
-            }
-            __syncwarp();
-            masked_rows_store(a.meval + p0 * es, buf, rows, es, am);
-        }
-        __syncwarp();
-        TSTAMP(3)
-    }
-#undef TSTAMP
-}
-
-// Levels with at most M2M_SMALL nodes are formed by block 0 alone (block
-// barrier); the grid synchronises only around the wide levels.  Whether a
-// level is small is read from meta, so every block takes the same path.
-#ifndef DT_M2M_THREADS
-#define DT_M2M_THREADS 128
-#endif
-constexpr int M2M_THREADS = DT_M2M_THREADS;
-#ifndef DT_M2M_SMALL
-#define DT_M2M_SMALL (4 * M2M_THREADS)
-#endif
-constexpr int64_t M2M_SMALL = DT_M2M_SMALL;
-
-__global__ void __launch_bounds__(M2M_THREADS) m2m_threads_kernel(MomArgs a)
-{
-    cg::grid_group grid = cg::this_grid();
-#if DT_M2M_W32
-    extern __shared__ double m2m_buf[];
-#endif
-    const volatile int64_t *meta = a.meta;
-    const int64_t depth = meta[DT_META_DEPTH];
-    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
-    int64_t stop = 0, lo = 0, hi = 0;
-    if (a.plan) {
-        stop = __ldg(a.plan + DT_PLAN_CUT);
-        lo = __ldg(a.plan + DT_PLAN_SRC_LO);
-        hi = __ldg(a.plan + DT_PLAN_SRC_HI);
-    }
-    bool prev_small = true;  // nothing formed yet: no barrier before the first level
-    bool first = true;
-    for (int64_t lev = depth - 1; lev >= stop; --lev) {
-        const int64_t f0 = meta[DT_META_LEVEL0 + lev], f1 = meta[DT_META_LEVEL0 + lev + 1];
-        const bool small = f1 - f0 <= M2M_SMALL;
-        if (!first) {
-            if (small && prev_small)
-                __syncthreads();
-            else
-                grid.sync();
-        }
-        first = false;
-#ifdef DT_M2M_TRACE
-        if (tid == 0) {
-            unsigned long long t;
-            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-            reinterpret_cast<unsigned long long *>(a.arrived)[lev] = t;
-        }
-#endif
-        // one call site keeps the (long, straight-line) formation code once
-#if DT_M2M_W32
-        if (!small || blockIdx.x == 0)
-            m2m_level_warps32(a, f0, f1, small ? (int64_t)(threadIdx.x >> 5) : (tid >> 5),
-                              small ? (int64_t)(blockDim.x >> 5) : (nthreads >> 5),
-                              a.plan != nullptr, lo, hi, m2m_buf + (threadIdx.x >> 5) * M2M_BUF);
-#else
-        if (!small || blockIdx.x == 0)
-            m2m_level_threads(a, f0, f1, small ? (int64_t)threadIdx.x : tid,
-                              small ? (int64_t)blockDim.x : nthreads, a.plan != nullptr, lo, hi);
-#endif
-        prev_small = small;
-    }
-}
-
-// M2M of one level, one warp per internal node, lane k -> order k:
-// m_k(parent) = sum_children sum_{j<=k} m_j(child) pw_{k-j},
-// pw_i = delta^i / i! from a multiplicative warp scan; the child row and pw
-// are staged in shared memory (row reads broadcast, pw reads conflict-free).
-__device__ __forceinline__ void m2m_level_warps(const MomArgs &a, int64_t f0, int64_t f1,
-                                                int64_t gwarp, int64_t nwarps,
-                                                const double *inv_s, double *pw_s, double *m_s,
-                                                bool filter = false, int64_t src_lo = 0,
-                                                int64_t src_hi = 0)
-{
-    const int lane = dt_lane();
-    const int o1 = (int)a.order + 1;
-    for (int64_t node = f0 + gwarp; node < f1; node += nwarps) {
-        const int64_t l = __ldg(a.left + node), r = __ldg(a.right + node);
-        if (l < 0 && r < 0)
-            continue;
-        if (filter && (__ldg(a.start + node) < src_lo || __ldg(a.end + node) > src_hi))
-            continue;
-        const double c = __ldg(a.center + node);
-        double out = 0.0;
-#pragma unroll
-        for (int ci = 0; ci < 2; ++ci) {
-            const int64_t ch = ci == 0 ? l : r;
-            if (ch < 0)
-                continue;
-            const double delta = __ldg(a.center + ch) - c;
-            double v = lane == 0 ? 1.0 : delta * inv_s[lane];
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const double t = __shfl_up_sync(DT_FULL, v, o);
-                if (lane >= o)
-                    v *= t;
-            }
-            pw_s[lane] = v;
-            m_s[lane] = lane < o1 ? __ldcg(a.moments + ch * o1 + lane) : 0.0;
-            __syncwarp();
-            double acc = 0.0;
-            for (int j = 0; j <= lane && j < o1; ++j)
-                acc = __fma_rn(m_s[j], pw_s[lane - j], acc);
-            out += acc;
-            __syncwarp();
-        }
-        if (lane < o1)
-            put_moment(a, node, lane, out);
-    }
-}
-
-__global__ void __launch_bounds__(256) m2m_levels_kernel(MomArgs a)
-{
-    cg::grid_group grid = cg::this_grid();
-    __shared__ double inv_s[32];
-    __shared__ double pw_s[8][32], m_s[8][32];
-    if (threadIdx.x < 32)
-        inv_s[threadIdx.x] = c_inv_k[threadIdx.x];
-    __syncthreads();
-    const volatile int64_t *meta = a.meta;
-    const int64_t depth = meta[DT_META_DEPTH];
-    const int warp = threadIdx.x >> 5;
-    const int64_t gwarp = (int64_t)blockIdx.x * 8 + warp;
-    const int64_t nwarps = (int64_t)gridDim.x * 8;
-    int64_t stop = 0, lo = 0, hi = 0;
-    if (a.plan) {  // levels >= cut, this rank's subtrees only
-        stop = __ldg(a.plan + DT_PLAN_CUT);
-        lo = __ldg(a.plan + DT_PLAN_SRC_LO);
-        hi = __ldg(a.plan + DT_PLAN_SRC_HI);
-    }
-    for (int64_t lev = depth - 1; lev >= stop; --lev) {
-        m2m_level_warps(a, meta[DT_META_LEVEL0 + lev], meta[DT_META_LEVEL0 + lev + 1], gwarp,
-                        nwarps, inv_s, pw_s[warp], m_s[warp], a.plan != nullptr, lo, hi);
-        grid.sync();
-    }
-}
-
-// ---- level M2M split into narrow / wide phases (no spinning co-runners) ----
-//
-// Bottom-up the tree is narrow (deep refinement), then wide, then narrow
-// again (the top levels).  Narrow levels run in a single-block kernel (block
-// barriers only); the wide levels run in a cooperative kernel (one grid
-// barrier per level).  A block that waits on a grid barrier polls L2, which
-// slows the memory traffic of the blocks still working, so narrow levels are
-// never processed under a grid barrier.  Every kernel derives the same phase
-// boundaries from meta.
-constexpr int M2M_NARROW_THREADS = 256;
-constexpr int64_t M2M_NARROW = 4 * M2M_NARROW_THREADS;
-
-struct M2MPhases {
-    int64_t top, deep_end, wide_end, stop;  // levels [top .. deep_end), [deep_end .. wide_end), ...
-};
-
-__device__ __forceinline__ M2MPhases m2m_phases(const MomArgs &a)
-{
-    const int64_t depth = __ldg(a.meta + DT_META_DEPTH);
-    const int64_t stop = a.plan ? __ldg(a.plan + DT_PLAN_CUT) : 0;
-    auto width = [&](int64_t lev) {
-        return __ldg(a.meta + DT_META_LEVEL0 + lev + 1) - __ldg(a.meta + DT_META_LEVEL0 + lev);
-    };
-    int64_t lev = depth - 1;
-    while (lev >= stop && width(lev) <= M2M_NARROW)
-        --lev;
-    const int64_t deep_end = lev;  // first wide level from the bottom (or stop - 1)
-    while (lev >= stop && width(lev) > M2M_NARROW)
-        --lev;
-    return M2MPhases{depth - 1, deep_end, lev, stop};
-}
-
-// phase 0: narrow deep levels [top .. deep_end); phase 2: [wide_end .. stop]
-template <int PHASE>
-__global__ void __launch_bounds__(M2M_NARROW_THREADS) m2m_narrow_kernel(MomArgs a)
-{
-    extern __shared__ double m2m_nbuf[];
-    const M2MPhases ph = m2m_phases(a);
-    const int64_t from = PHASE == 0 ? ph.top : ph.wide_end;
-    const int64_t to = PHASE == 0 ? ph.deep_end + 1 : ph.stop;
-    int64_t lo = 0, hi = 0;
-    if (a.plan) {
-        lo = __ldg(a.plan + DT_PLAN_SRC_LO);
-        hi = __ldg(a.plan + DT_PLAN_SRC_HI);
-    }
-    for (int64_t lev = from; lev >= to; --lev) {
-        m2m_level_warps32(a, __ldg(a.meta + DT_META_LEVEL0 + lev),
-                          __ldg(a.meta + DT_META_LEVEL0 + lev + 1), threadIdx.x >> 5,
-                          blockDim.x >> 5, a.plan != nullptr, lo, hi,
-                          m2m_nbuf + (threadIdx.x >> 5) * M2M_BUF);
-        __syncthreads();
-    }
-}
-
-__global__ void __launch_bounds__(M2M_NARROW_THREADS) m2m_wide_kernel(MomArgs a)
-{
-    cg::grid_group grid = cg::this_grid();
-    extern __shared__ double m2m_wbuf[];
-    const M2MPhases ph = m2m_phases(a);
-    int64_t lo = 0, hi = 0;
-    if (a.plan) {
-        lo = __ldg(a.plan + DT_PLAN_SRC_LO);
-        hi = __ldg(a.plan + DT_PLAN_SRC_HI);
-    }
-    const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t lev = ph.deep_end; lev > ph.wide_end; --lev) {
-        if (lev != ph.deep_end)
-            grid.sync();
-        m2m_level_warps32(a, __ldg(a.meta + DT_META_LEVEL0 + lev),
-                          __ldg(a.meta + DT_META_LEVEL0 + lev + 1), gw, nw, a.plan != nullptr, lo,
-                          hi, m2m_wbuf + (threadIdx.x >> 5) * M2M_BUF);
     }
 }
 
@@ -1358,14 +758,12 @@ __global__ void shard_pack_kernel(const int64_t *plan, int rank, int64_t o1, con
     }
 }
 
-// One block: scatter every owner's level-l rows, then M2M levels cut-1 .. 0.
+// One block: scatter every owner's level-l rows, then M2M levels cut-1 .. 0
+// (thread per node; the same arithmetic as m2m_form_warp, so the rows match
+// the single-GPU pass bit for bit).
 __global__ void __launch_bounds__(256) shard_finish_kernel(MomArgs a, int world, int64_t slot_rows,
                                                            const double *recv)
 {
-    __shared__ double inv_s[32];
-    __shared__ double pw_s[8][32], m_s[8][32];
-    if (threadIdx.x < 32)
-        inv_s[threadIdx.x] = c_inv_k[threadIdx.x];
     const int64_t o1 = a.order + 1, es = a.meval ? a.estride : 0, w = o1 + es;
     for (int r = 0; r < world; ++r) {
         const int64_t a0 = __ldg(a.plan + DT_PLAN_OWNER0 + r);
@@ -1382,78 +780,27 @@ __global__ void __launch_bounds__(256) shard_finish_kernel(MomArgs a, int world,
     __syncthreads();
     const int64_t cut = __ldg(a.plan + DT_PLAN_CUT);
     for (int64_t lev = cut - 1; lev >= 0; --lev) {
-#if DT_MOM_V2
         m2m_level_threads(a, __ldg(a.meta + DT_META_LEVEL0 + lev),
                           __ldg(a.meta + DT_META_LEVEL0 + lev + 1), threadIdx.x, blockDim.x,
                           false, 0, 0);
-#else
-        const int warp = threadIdx.x >> 5;
-        m2m_level_warps(a, __ldg(a.meta + DT_META_LEVEL0 + lev),
-                        __ldg(a.meta + DT_META_LEVEL0 + lev + 1), warp, 8, inv_s, pw_s[warp],
-                        m_s[warp]);
-#endif
         __syncthreads();
     }
 }
 
-// P2M + cooperative level M2M, honouring a.plan.
+// Upward pass for order + 1 <= 32 (honouring a.plan): P2M, then the
+// barrier-free M2M dataflow.  Level-synchronous M2M variants (grid barrier
+// per level, one launch per level, narrow/wide phases) all measured slower
+// on configs[2] (0.47-0.95 ms against 0.36 ms): a grid barrier costs ~5 us
+// and the tree is 32 levels deep.
 int launch_level_moments(MomArgs &a, cudaStream_t s)
 {
     const int sms = dt_num_sms();
-    void *args[] = {&a};
-    int per_sm = 0;
-#if DT_MOM_V2
     if (!a.parent)
         return dt_set_error(DT_ERR_WORKSPACE, "moments workspace missing");
     p2m_group_kernel<DT_P2M_G><<<sms * 8, 256, 0, s>>>(a);
     DT_CUDA_TRY(cudaGetLastError());
-#if DT_M2M_MODE == 3
-    {
-        const size_t smem = (size_t)(M2M_NARROW_THREADS / 32) * M2M_BUF * sizeof(double);
-        DT_CUDA_TRY(cudaFuncSetAttribute((const void *)m2m_narrow_kernel<0>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        DT_CUDA_TRY(cudaFuncSetAttribute((const void *)m2m_narrow_kernel<2>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        DT_CUDA_TRY(cudaFuncSetAttribute((const void *)m2m_wide_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        m2m_narrow_kernel<0><<<1, M2M_NARROW_THREADS, smem, s>>>(a);
-        DT_CUDA_TRY(cudaGetLastError());
-        DT_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, m2m_wide_kernel,
-                                                                  M2M_NARROW_THREADS, smem));
-        if (per_sm < 1)
-            return dt_set_error(DT_ERR_CUDA, "m2m kernel cannot be resident");
-        DT_CUDA_TRY(cudaLaunchCooperativeKernel((const void *)m2m_wide_kernel, sms * per_sm,
-                                                M2M_NARROW_THREADS, args, smem, s));
-        m2m_narrow_kernel<2><<<1, M2M_NARROW_THREADS, smem, s>>>(a);
-    }
-#elif DT_M2M_MODE == 0
-    const size_t smem = DT_M2M_W32 ? (size_t)(M2M_THREADS / 32) * M2M_BUF * sizeof(double) : 0;
-    if (smem)
-        DT_CUDA_TRY(cudaFuncSetAttribute((const void *)m2m_threads_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    DT_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, m2m_threads_kernel,
-                                                              M2M_THREADS, smem));
-    if (per_sm < 1)
-        return dt_set_error(DT_ERR_CUDA, "m2m kernel cannot be resident");
-    DT_CUDA_TRY(cudaLaunchCooperativeKernel((const void *)m2m_threads_kernel,
-                                            sms * (per_sm > 2 ? 2 : per_sm), M2M_THREADS, args,
-                                            smem, s));
-#elif DT_M2M_MODE == 1
-    m2m_flow_thread_kernel<<<sms * 8, 128, 0, s>>>(a);
-#else
     m2m_flow_kernel<<<sms * 8, 256, 0, s>>>(a);
-#endif
     DT_CUDA_TRY(cudaGetLastError());
-#else
-    p2m_thread_kernel<<<sms * 16, 128, 0, s>>>(a);
-    DT_CUDA_TRY(cudaGetLastError());
-    DT_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, m2m_levels_kernel, 256, 0));
-    if (per_sm < 1)
-        return dt_set_error(DT_ERR_CUDA, "m2m kernel cannot be resident");
-    const int grid = sms * (per_sm > 4 ? 4 : per_sm);
-    DT_CUDA_TRY(
-        cudaLaunchCooperativeKernel((const void *)m2m_levels_kernel, grid, 256, args, 0, s));
-#endif
     return DT_OK;
 }
 
