@@ -388,7 +388,10 @@ __global__ void __launch_bounds__(MOM_THREADS) moments_kernel(MomArgs a)
 // flight, then a butterfly over the G lanes.  Leaves are gathered per warp
 // from 32 consecutive node slots (ballot) so no group idles on internal
 // nodes.  Raw power sums S_k = sum q (x - c)^k in registers.
-template <int G>
+// KMAX: orders computed, a multiple of 8 >= order + 1, fixed at compile time
+// so the order loop has no per-step guard (a uniform branch per order step
+// costs 25% of the instructions and splits the scheduling window).
+template <int G, int KMAX>
 __global__ void __launch_bounds__(256) p2m_group_kernel(MomArgs a)
 {
     const int lane = dt_lane();
@@ -438,9 +441,9 @@ __global__ void __launch_bounds__(256) p2m_group_kernel(MomArgs a)
                 e = __ldg(a.end + node);
                 c = __ldg(a.center + node);
             }
-            double acc[REG_ORDER];
+            double acc[KMAX];
 #pragma unroll
-            for (int k = 0; k < REG_ORDER; ++k)
+            for (int k = 0; k < KMAX; ++k)
                 acc[k] = 0.0;
             int64_t j = s + sub;
             for (; j + 3 * G < e; j += 4 * G) {
@@ -449,36 +452,32 @@ __global__ void __launch_bounds__(256) p2m_group_kernel(MomArgs a)
                 double w0 = __ldg(a.qs + j), w1 = __ldg(a.qs + j + G);
                 double w2 = __ldg(a.qs + j + 2 * G), w3 = __ldg(a.qs + j + 3 * G);
 #pragma unroll
-                for (int k = 0; k < REG_ORDER; ++k) {
-                    if (k < o1) {
-                        acc[k] += (w0 + w1) + (w2 + w3);
-                        w0 *= t0;
-                        w1 *= t1;
-                        w2 *= t2;
-                        w3 *= t3;
-                    }
+                for (int k = 0; k < KMAX; ++k) {
+                    acc[k] += (w0 + w1) + (w2 + w3);
+                    w0 *= t0;
+                    w1 *= t1;
+                    w2 *= t2;
+                    w3 *= t3;
                 }
             }
             for (; j < e; j += G) {
                 const double t0 = __ldg(a.xs + j) - c;
                 double w0 = __ldg(a.qs + j);
 #pragma unroll
-                for (int k = 0; k < REG_ORDER; ++k) {
-                    if (k < o1) {
-                        acc[k] += w0;
-                        w0 *= t0;
-                    }
+                for (int k = 0; k < KMAX; ++k) {
+                    acc[k] += w0;
+                    w0 *= t0;
                 }
             }
 #pragma unroll
-            for (int k = 0; k < REG_ORDER; ++k) {
+            for (int k = 0; k < KMAX; ++k) {
 #pragma unroll
                 for (int o = G / 2; o > 0; o >>= 1)
                     acc[k] += __shfl_xor_sync(DT_FULL, acc[k], o);
             }
             if (active) {
 #pragma unroll
-                for (int k = 0; k < REG_ORDER; ++k)
+                for (int k = 0; k < KMAX; ++k)
                     if ((k & (G - 1)) == sub && k < o1)
                         put_raw_sum(a, node, k, acc[k]);
             }
@@ -797,7 +796,15 @@ int launch_level_moments(MomArgs &a, cudaStream_t s)
     const int sms = dt_num_sms();
     if (!a.parent)
         return dt_set_error(DT_ERR_WORKSPACE, "moments workspace missing");
-    p2m_group_kernel<DT_P2M_G><<<sms * 8, 256, 0, s>>>(a);
+    const int64_t o1 = a.order + 1;
+    if (o1 <= 8)
+        p2m_group_kernel<DT_P2M_G, 8><<<sms * 8, 256, 0, s>>>(a);
+    else if (o1 <= 16)
+        p2m_group_kernel<DT_P2M_G, 16><<<sms * 8, 256, 0, s>>>(a);
+    else if (o1 <= 24)
+        p2m_group_kernel<DT_P2M_G, 24><<<sms * 8, 256, 0, s>>>(a);
+    else
+        p2m_group_kernel<DT_P2M_G, 32><<<sms * 8, 256, 0, s>>>(a);
     DT_CUDA_TRY(cudaGetLastError());
     m2m_flow_kernel<<<sms * 8, 256, 0, s>>>(a);
     DT_CUDA_TRY(cudaGetLastError());
