@@ -10,7 +10,7 @@
 // computed on raw power sums S_k = k! m_k, where the shift is the binomial
 // transform S'_k = sum_j C(k,j) delta^(k-j) S_j, applied in place as 31
 // passes of Pascal's rule S_k += delta S_(k-1).
-//   order + 1 <= 32: P2M with 4 lanes per leaf (p2m_group_kernel), then a
+//   order + 1 <= 32: P2M with 2 lanes per leaf (p2m_group_kernel), then a
 //     barrier-free dataflow (m2m_flow_kernel): every leaf bumps its parent's
 //     arrival counter; the warp whose arrival completes a parent forms it
 //     (lane k = order k) and climbs on.  The shard plan (multi-GPU) restricts
@@ -25,7 +25,7 @@
 #include "dt_common.cuh"
 
 #ifndef DT_P2M_G
-#define DT_P2M_G 4
+#define DT_P2M_G 2
 #endif
 
 namespace {
