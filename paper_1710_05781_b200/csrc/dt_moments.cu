@@ -12,8 +12,9 @@
 // passes of Pascal's rule S_k += delta S_(k-1).
 //   order + 1 <= 32: P2M with 2 lanes per leaf (p2m_group_kernel), then a
 //     barrier-free dataflow (m2m_flow_kernel): every leaf bumps its parent's
-//     arrival counter; the warp whose arrival completes a parent forms it
-//     (lane k = order k) and climbs on.  The shard plan (multi-GPU) restricts
+//     arrival counter; the lane whose arrival completes a parent keeps it,
+//     and the warp forms four kept parents at a time (8 lanes each, 4 orders
+//     per lane) before those lanes climb on.  The shard plan (multi-GPU) restricts
 //     both to one rank's subtrees; shard_finish_kernel forms the levels above
 //     the cut with the same arithmetic, thread per node.
 //   higher orders: warp per leaf + the same dataflow with a Toeplitz shift.
@@ -520,6 +521,64 @@ __device__ __forceinline__ void m2m_form_warp(const MomArgs &a, int64_t P)
         put_raw_sum(a, P, lane, out);
 }
 
+// Four parents per warp at once: lanes [8g, 8g + 8) form parent P (of group
+// g), lane l of a group holding orders 4l .. 4l + 3 of both children.  A
+// Pascal pass then needs one neighbour value per lane (the last order of
+// lane l - 1), so a parent costs 8x fewer shuffles than with one order per
+// lane.  Same arithmetic, term for term, as m2m_form_warp / the thread form.
+__device__ __forceinline__ void m2m_form_group8(const MomArgs &a, int64_t P)
+{
+    const int gl = dt_lane() & 7;  // lane within the group
+    const int o1 = (int)a.order + 1;
+    int64_t l = -1, r = -1;
+    double dl = 0.0, dr = 0.0;
+    double Sl[4], Sr[4];
+    if (P >= 0) {
+        l = __ldg(a.left + P);
+        r = __ldg(a.right + P);
+        const double c = __ldg(a.center + P);
+        if (l >= 0)
+            dl = __ldg(a.center + l) - c;
+        if (r >= 0)
+            dr = __ldg(a.center + r) - c;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        const int k = 4 * gl + u;
+        const double fk = c_fact_km1[k + 1];
+        Sl[u] = (l >= 0 && k < o1) ? __dmul_rn(__ldcg(a.moments + l * o1 + k), fk) : 0.0;
+        Sr[u] = (r >= 0 && k < o1) ? __dmul_rn(__ldcg(a.moments + r * o1 + k), fk) : 0.0;
+    }
+    const unsigned mask = DT_FULL;
+#pragma unroll
+    for (int i = 1; i < REG_ORDER; ++i) {
+        const double nl = __shfl_up_sync(mask, Sl[3], 1, 8);
+        const double nr = __shfl_up_sync(mask, Sr[3], 1, 8);
+        // descending within the lane: every update reads the previous pass
+#pragma unroll
+        for (int u = 3; u >= 0; --u) {
+            const int k = 4 * gl + u;
+            if (k >= i) {
+                Sl[u] = __fma_rn(dl, u ? Sl[u - 1] : nl, Sl[u]);
+                Sr[u] = __fma_rn(dr, u ? Sr[u - 1] : nr, Sr[u]);
+            }
+        }
+    }
+    if (P < 0)
+        return;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        const int k = 4 * gl + u;
+        double out = 0.0;
+        if (l >= 0)
+            out += Sl[u];
+        if (r >= 0)
+            out += Sr[u];
+        if (k < o1)
+            put_raw_sum(a, P, k, out);
+    }
+}
+
 // Upward pass without grid barriers (after the P2M kernel, which also wrote
 // parent[] and zeroed arrived[]): every leaf bumps its parent's arrival
 // counter; the warp whose arrival completes a parent forms it and keeps
@@ -555,28 +614,41 @@ __global__ void __launch_bounds__(256) m2m_flow_kernel(MomArgs a)
                 done = atomicAdd(a.arrived + par, 1) == need - 1;
             }
         }
-        unsigned todo = __ballot_sync(DT_FULL, done);
-        while (todo) {
-            const int i = __ffs(todo) - 1;
-            todo &= todo - 1;
-            int64_t P = __shfl_sync(DT_FULL, par, i);
-            while (true) {
-                __threadfence();  // the other children's rows, published before their arrival
-                m2m_form_warp(a, P);
-                __threadfence();  // publish P's row before announcing it
-                int64_t pp = -1;
-                if (lane == 0) {
-                    const int64_t q = __ldcg(a.parent + P);
-                    if (q >= cut_begin && q >= 0) {
-                        const int need = (__ldg(a.left + q) >= 0) + (__ldg(a.right + q) >= 0);
-                        if (atomicAdd(a.arrived + q, 1) == need - 1)
-                            pp = q;
-                    }
+        // lanes hold the parents they completed; four of them are formed at a
+        // time (one per 8-lane group), then each of those lanes arrives at its
+        // own grandparent and keeps it if the arrival completes it
+        if (!done)
+            par = -1;
+        while (true) {
+            const unsigned todo = __ballot_sync(DT_FULL, par >= 0);
+            if (!todo)
+                break;
+            unsigned sel = 0, t = todo;
+            int64_t mine_p = -1;
+#pragma unroll
+            for (int g = 0; g < 4; ++g) {
+                int64_t pg = -1;
+                if (t) {
+                    const int src = __ffs(t) - 1;
+                    t &= t - 1;
+                    sel |= 1u << src;
+                    pg = __shfl_sync(DT_FULL, par, src);
                 }
-                pp = __shfl_sync(DT_FULL, pp, 0);
-                if (pp < 0)
-                    break;
-                P = pp;
+                if ((lane >> 3) == g)
+                    mine_p = pg;
+            }
+            __threadfence();  // the other children's rows, published before their arrival
+            m2m_form_group8(a, mine_p);
+            __threadfence();  // publish the rows before announcing them
+            if ((sel >> lane) & 1u) {
+                const int64_t q = __ldcg(a.parent + par);
+                int64_t nxt = -1;
+                if (q >= cut_begin && q >= 0) {
+                    const int need = (__ldg(a.left + q) >= 0) + (__ldg(a.right + q) >= 0);
+                    if (atomicAdd(a.arrived + q, 1) == need - 1)
+                        nxt = q;
+                }
+                par = nxt;
             }
         }
     }
