@@ -42,3 +42,33 @@ lines = subprocess.run([sys.executable, os.path.join(REPO, "tools", "ncu_lines.p
                        capture_output=True, text=True).stdout
 open(os.path.join(prof, f"{tag}_ncu_eval_cfg2_lines.txt"), "w").write(lines)
 print(json.dumps(d, indent=1))
+
+# optional 5th argument: ncu report of the build / moments kernels
+if len(sys.argv) > 5:
+    raw = subprocess.run(["ncu", "-i", sys.argv[5], "--page", "raw", "--csv"],
+                         capture_output=True, text=True).stdout
+    r = list(csv.reader(io.StringIO(raw)))
+    h, u = r[0], r[1]
+    nodes, leaves = b["config"]["nodes"], b["config"]["leaves"]
+    alg = {"build_kernel": 8 * 2**24 + 72 * nodes,
+           "p2m_group_kernel": 16 * 2**24 + 8 * (31 + 32) * leaves,
+           "m2m_flow_kernel": 8 * (2 * 31 + 31 + 32) * (nodes - leaves)}
+    aux = {"capture": "ncu --set full --clock-control none -k regex:'p2m|m2m|build_kernel' "
+                      "-s 3 -c 3 python tools/moments_time.py (configs[2])", "kernels": []}
+    for v in r[2:]:
+        gv = lambda k: float(v[h.index(k)]) * scale.get(u[h.index(k)], 1)
+        name = v[h.index("Kernel Name")]
+        key = next(k for k in alg if k in name)
+        t = float(v[h.index("gpu__time_duration.sum")]) * (
+            1e-3 if u[h.index("gpu__time_duration.sum")] == "us" else 1)
+        aux["kernels"].append({
+            "kernel": name.split("(")[0], "duration_ms": t,
+            "dram_bytes": gv("dram__bytes_read.sum") + gv("dram__bytes_write.sum"),
+            "algorithmic_bytes": alg[key], "algorithmic_GBps": alg[key] / (t * 1e-3) / 1e9,
+            "fp64_pipe_active_pct": float(v[h.index("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active")]),
+            "issue_active_pct": float(v[h.index("smsp__issue_active.avg.pct_of_peak_sustained_active")]),
+            "warps_active_pct": float(v[h.index("sm__warps_active.avg.pct_of_peak_sustained_active")]),
+        })
+    json.dump(aux, open(os.path.join(prof, f"{tag}_ncu_aux_cfg2.json"), "w"), indent=1)
+    for kk in aux["kernels"]:
+        print(kk["kernel"], "%.3f ms" % kk["duration_ms"], "%.0f GB/s" % kk["algorithmic_GBps"])
