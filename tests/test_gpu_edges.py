@@ -1,0 +1,88 @@
+"""Edge cases of the public API on the GPU paths added for speed: unaligned
+pair views, host/device target kinds at the pipeline threshold, far-away and
+non-finite targets, empty systems for the assembly helpers."""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def dt():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1710_05781_b200 as pkg
+
+    return pkg
+
+
+def test_unaligned_pair_view(dt):
+    rng = np.random.default_rng(1)
+    pairs = torch.from_numpy(np.column_stack([rng.uniform(0, 1, 1001), rng.normal(size=1001)]))
+    dev = pairs.cuda()
+    view = dev.view(-1)[1:-1].view(-1, 2)  # 8-byte offset: (q0, x1), (q1, x2), ...
+    assert view.data_ptr() % 16 == 8
+    s = dt.from_particles(view)
+    want = dt.from_particles(view.cpu().numpy())
+    assert torch.equal(s.xs, want.xs) and torch.equal(s.qs, want.qs)
+
+
+def test_targets_far_outside_and_at_sources(dt):
+    rng = np.random.default_rng(2)
+    x = np.sort(rng.uniform(-1, 1, 3000))
+    q = rng.normal(size=3000)
+    s = dt.from_sorted(x, q)
+    k = dt.DiscKernel(0.01)
+    cfg = dt.EvalConfig(p=12, leaf_capacity=16, adaptive=True, tolerance=1e-10)
+    tree = dt.build(s, k, cfg)
+    t = np.concatenate([[-1e6, -50.0, -1.0 - 1e-12], x[::7], [x[-1], 1.0 + 1e-9, 3.5, 1e5]])
+    got = dt.evaluate_all(tree, k, cfg, s, t).values
+    ref = dt.evaluate_direct(s, k, t).values
+    assert np.max(np.abs(got - ref)) <= 1e-10 * np.abs(q).sum()
+
+
+@pytest.mark.parametrize("n", [(1 << 20) - 1, 1 << 20])
+def test_pipeline_threshold_paths_agree(dt, n):
+    """Just below / at the host-pipeline threshold: pinned, pageable and
+    device targets give identical values."""
+    from paper_1710_05781_b200 import workloads as W
+
+    w = W.cfg1(cells=1 << 18)
+    s = dt.from_sorted(w.xs, w.qs)
+    k = dt.DiscKernel(w.r_d)
+    cfg = dt.EvalConfig(p=8, leaf_capacity=64, adaptive=True, tolerance=1e-10)
+    tree = dt.build(s, k, cfg)
+    t = np.sort(np.random.default_rng(3).uniform(-1.1, 1.1, n))
+    dev = dt.evaluate_all(tree, k, cfg, s, torch.from_numpy(t).cuda()).values.cpu().numpy()
+    host = dt.evaluate_all(tree, k, cfg, s, t).values
+    pinned = dt.evaluate_all(tree, k, cfg, s, torch.from_numpy(t).pin_memory()).values.numpy()
+    np.testing.assert_array_equal(host, dev)
+    np.testing.assert_array_equal(pinned, dev)
+
+
+def test_non_finite_targets_rejected_everywhere(dt):
+    s = dt.from_particles([(0.1, 1.0), (0.4, -2.0), (0.9, 0.5)])
+    k = dt.DiscKernel(0.05)
+    cfg = dt.EvalConfig(p=6, leaf_capacity=1)
+    tree = dt.build(s, k, cfg)
+    for bad in (np.nan, np.inf, -np.inf):
+        t = np.array([0.2, bad, 0.7])
+        with pytest.raises(ValueError):
+            dt.evaluate_all(tree, k, cfg, s, t)
+        with pytest.raises(ValueError):
+            dt.evaluate_all(tree, k, cfg, s, torch.from_numpy(t).cuda())
+        with pytest.raises(ValueError):
+            dt.evaluate_direct(s, k, t)
+
+
+def test_assembly_edges(dt):
+    empty = dt.from_particles([])
+    im = dt.with_images(empty, dt.ImageSpec(gap_length=1.0))
+    assert len(im) == 0
+    one = dt.from_density(dt.DensitySpec(domain=(0.0, 2.0), cells=1, values=[3.0],
+                                         quadrature_order=1, eps0=1.0))
+    # one node at the cell middle with q = (w/2) sigma dx / (2 eps0) = 1 * 3 * 2 / 2
+    assert one.xs.tolist() == [1.0] and one.qs.tolist() == [3.0]
