@@ -325,11 +325,10 @@ __device__ int psel_fast(double big_r, double h, const EvalArgs &a, const float 
     const float lx = (fmaf(-0.25f, __log2f(emin + sstar), log_c) - __log2f(1.0f - ratio)) + fr;
     const float L = -((float)er + fr);         // -log2(ratio) > 0
     const float iL = fast_rcp(L);
-    const float pstar_approx = (lx + (float)er) * iL;
-    if (pstar_approx < -1.0f)
-        return 0;
-    if (pstar_approx > (float)a.p_cap + 1.0f)
-        return a.p_cap;
+    // candidate order, clamped to [-1, p_cap]: outside, the decision below
+    // gives 0 resp. p_cap and never reports an ambiguity
+    const float pstar_approx =
+        fminf(fmaxf((lx + (float)er) * iL, -1.0f), (float)a.p_cap);
     const int n = __float2int_rn(pstar_approx);
     // residual log2(value_n / tol) = lx + (n + 1) er + n fr, integer part exact
     const float resid = fmaf((float)n, fr, lx) + (float)((n + 1) * er);
