@@ -280,8 +280,8 @@ __device__ __forceinline__ void split_log2(float x, int *e, float *f)
 __device__ int psel_fast(double big_r, double h, const EvalArgs &a, const float *isig,
                          float rd2f, float log_c)
 {
-    if (h == 0.0)
-        return 0;  // value == 0 <= tol at cand 0
+    // h == 0 (a node of coincident sources) gives ratio 0, which the range
+    // guard sends to the exact replica (value 0 there, p = 0)
     const float Rf = f32_of(big_r);
     const float hf = f32_of(h);
     const float iR = fast_rcp(Rf);
