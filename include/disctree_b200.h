@@ -280,7 +280,11 @@ int dt_tree_phi_sum_packed(const void *packed_nodes, int64_t n_nodes, const doub
  * host memory (UVA): each target is read once and each value written once
  * over the host link while the traversal runs.  flags (device int64[2], may
  * be NULL): flags[0] += number of non-finite targets (those are not
- * traversed; the caller rejects the call). */
+ * traversed; the caller rejects the call).  The workspace holds the task
+ * counters; with dt_tree_field_workspace(i1 - i0) bytes it also holds the
+ * lower_bound of every 1024th target, which brackets the sign-term searches
+ * of sorted targets (checked per target, so any order stays correct). */
+size_t dt_tree_field_workspace(int64_t n_targets);
 int dt_tree_field_packed(const void *packed_nodes, int64_t n_nodes, const double *moments,
                          int64_t moment_stride, const double *xq, const double *xs,
                          const double *prefix, int64_t n_src, double rd2, double theta,

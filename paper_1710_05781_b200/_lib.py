@@ -106,6 +106,7 @@ SIGNATURES = {
         [_P, _I64, _P, _I64, _P, _I64, _D, _D, _I64, C.c_int, _D, _I64, _P, _P, _I64, _P,
          _P, _I64, _I64, C.c_int, C.c_int, C.POINTER(EvalStats), _P, _SZ, _P],
     ),
+    "dt_tree_field_workspace": (_SZ, [_I64]),
     "dt_tree_field_packed": (
         C.c_int,
         [_P, _I64, _P, _I64, _P, _P, _P, _I64, _D, _D, _I64, C.c_int, _D, _I64, _P, _P, _I64,

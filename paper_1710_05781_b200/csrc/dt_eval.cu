@@ -61,6 +61,7 @@ __device__ unsigned long long g_util[16];
 #define UTIL_ADD(k, v) ((void)0)
 #endif
 constexpr int EVAL_THREADS = DT_EVAL_THREADS;
+constexpr int64_t FIELD_TILE = 1024;  // targets per sign-term bracket (dt_tree_field_packed)
 constexpr int EVAL_WARPS = EVAL_THREADS / 32;
 constexpr int MAX_SAMPLES = 256;
 constexpr float PSEL_MARGIN_LOG2 = 2e-4f;  // ambiguity band of log2(value_n / tol)
@@ -90,6 +91,9 @@ struct EvalArgs {
     const double *sign_xs, *sign_prefix;
     int64_t sign_n;
     int64_t *vflags;
+    // optional: lower_bound of every FIELD_TILE-th target (and of the last),
+    // bracketing the search of the targets in between when they are sorted
+    const int64_t *sign_bracket;
     const int64_t *meta;  // if set: tol_share = tolerance / (3 max(depth, 1)) on device
     double tolerance;
 };
@@ -768,7 +772,19 @@ __global__ void __launch_bounds__(EVAL_THREADS, DT_EVAL_MINB) tree_eval_kernel(E
             if (a.sign_xs) {  // e(y) exactly as dt_sign_terms, then e + phi
                 double e = 0.0;
                 if (a.sign_n) {
-                    const int64_t idx = dt_lower_bound(a.sign_xs, 0, a.sign_n, y);
+                    int64_t idx = -1;
+                    if (a.sign_bracket) {
+                        // the tile's bracket, confirmed by the sources on both
+                        // sides (fails safe for unsorted targets)
+                        const int64_t tile = (i - a.i0) / FIELD_TILE;
+                        const int64_t lo = __ldg(a.sign_bracket + tile);
+                        const int64_t hi = min(a.sign_n, __ldg(a.sign_bracket + tile + 1) + 1);
+                        if (lo <= hi && (lo == 0 || __ldg(a.sign_xs + lo - 1) < y) &&
+                            (hi == a.sign_n || __ldg(a.sign_xs + hi) >= y))
+                            idx = dt_lower_bound(a.sign_xs, lo, hi, y);
+                    }
+                    if (idx < 0)
+                        idx = dt_lower_bound(a.sign_xs, 0, a.sign_n, y);
                     const double below = idx == 0 ? 0.0 : __ldg(a.sign_prefix + idx - 1);
                     e = __dsub_rn(__dmul_rn(2.0, below), __ldg(a.sign_prefix + a.sign_n - 1));
                 }
@@ -837,6 +853,20 @@ __global__ void scale_moments_kernel(const double *__restrict__ m, int64_t strid
             v = __dmul_rn(v, f);
     }
     out[i] = v;
+}
+
+// bracket[b] = lower_bound(xs, ys[i0 + b FIELD_TILE]) for b < nb, and of the
+// last target for b = nb (ys may be mapped host memory: one read per tile)
+__global__ void field_bracket_kernel(const double *__restrict__ xs, int64_t n,
+                                     const double *ys, int64_t i0, int64_t i1,
+                                     int64_t *__restrict__ bracket, int64_t nb)
+{
+    const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (b > nb)
+        return;
+    const int64_t i = b < nb ? i0 + b * FIELD_TILE : i1 - 1;
+    const double y = ys[i];
+    bracket[b] = isfinite(y) ? dt_lower_bound(xs, 0, n, y) : 0;
 }
 
 __global__ void pack_sources_kernel(const double *__restrict__ xs, const double *__restrict__ qs,
@@ -1047,6 +1077,12 @@ extern "C" int dt_tree_phi_sum_packed(const void *packed_nodes, int64_t n_nodes,
     return launch_eval(a, adaptive != 0, stats != nullptr, (cudaStream_t)stream);
 }
 
+extern "C" size_t dt_tree_field_workspace(int64_t n_targets)
+{
+    return DT_EVAL_COUNTER_BYTES +
+           (size_t)((n_targets + FIELD_TILE - 1) / FIELD_TILE + 1) * sizeof(int64_t);
+}
+
 extern "C" int dt_tree_field_packed(const void *packed_nodes, int64_t n_nodes,
                                     const double *moments, int64_t moment_stride,
                                     const double *xq, const double *xs, const double *prefix,
@@ -1101,6 +1137,15 @@ extern "C" int dt_tree_field_packed(const void *packed_nodes, int64_t n_nodes,
     a.sign_prefix = prefix;
     a.sign_n = n_src;
     a.vflags = flags;
+    const int64_t nb = (i1 - i0 + FIELD_TILE - 1) / FIELD_TILE;
+    const size_t bracket_bytes = (size_t)(nb + 1) * sizeof(int64_t);
+    if (n_src > 0 && workspace_bytes >= DT_EVAL_COUNTER_BYTES + bracket_bytes) {
+        int64_t *br = (int64_t *)((char *)workspace + DT_EVAL_COUNTER_BYTES);
+        field_bracket_kernel<<<(unsigned)((nb + 1 + 127) / 128), 128, 0, (cudaStream_t)stream>>>(
+            xs, n_src, ys, i0, i1, br, nb);
+        DT_CUDA_TRY(cudaGetLastError());
+        a.sign_bracket = br;
+    }
     return launch_eval(a, adaptive != 0, false, (cudaStream_t)stream);
 }
 

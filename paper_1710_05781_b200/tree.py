@@ -474,7 +474,7 @@ def _evaluate_host_mapped(tree: Tree, kernel: DiscKernel, config: EvalConfig,
     T = host.numel()
     out_h = torch.empty(T, dtype=torch.float64, pin_memory=True)
     flags = torch.zeros(2, dtype=torch.int64, device=dev)
-    ws = torch.empty(_lib.DT_EVAL_COUNTER_BYTES, dtype=torch.uint8, device=dev)
+    ws = torch.empty(int(_lib.load().dt_tree_field_workspace(T)), dtype=torch.uint8, device=dev)
     cos_t, sin_t = contour_tables(dev)
     p = _lib.ptr
     torch.cuda.synchronize(dev)

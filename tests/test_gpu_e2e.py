@@ -88,6 +88,21 @@ def test_field_packed_abi_device_and_host(dt, case):
         np.testing.assert_array_equal(got[3:-5], want[3:-5])
         assert np.isnan(got[:3]).all() and np.isnan(got[-5:]).all()
         assert flags.tolist() == [0, 0]
+    # with the bracket workspace, sorted and shuffled targets alike
+    big = torch.empty(int(L.dt_tree_field_workspace(len(w.targets))), dtype=torch.uint8,
+                      device="cuda")
+    perm = np.random.default_rng(8).permutation(len(w.targets))
+    for order in (np.arange(len(w.targets)), perm):
+        ys = torch.from_numpy(w.targets[order].copy()).cuda()
+        out = torch.full_like(ys, float("nan"))
+        rc = L.dt_tree_field_packed(
+            p(tree.packed), len(tree), p(tree.meval), tree.meval.shape[1], p(tree.xq),
+            p(system.xs), p(system.prefix), len(system), kernel.r_d ** 2, float(cfg.theta),
+            int(cfg.p), 1, _tol_share(tree, cfg), int(tree.moment_order), p(cos_t), p(sin_t),
+            cos_t.numel(), ys.data_ptr(), out.data_ptr(), 0, len(ys), None, p(big), big.numel(),
+            None)
+        assert rc == 0
+        np.testing.assert_array_equal(out.cpu().numpy(), want[order])
     # pageable host memory is refused before any device work
     ys = torch.from_numpy(w.targets.copy())
     out = torch.empty_like(ys)
