@@ -66,6 +66,16 @@ __device__ __forceinline__ double dt_rcp(double x)
     return __fma_rn(r, e, r);
 }
 
+// one 256-bit read-only load (LDG.E.ENL2.256); p must be 32-byte aligned
+__device__ __forceinline__ double4 dt_ldg256(const void *p)
+{
+    double4 r;
+    asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];"
+        : "=d"(r.x), "=d"(r.y), "=d"(r.z), "=d"(r.w)
+        : "l"(p));
+    return r;
+}
+
 __device__ __forceinline__ int dt_lane() { return threadIdx.x & (DT_WARP - 1); }
 
 __device__ __forceinline__ unsigned dt_smid()

@@ -682,7 +682,7 @@ __global__ void __launch_bounds__(EVAL_THREADS, DT_EVAL_MINB) tree_eval_kernel(E
         int node = 0;
         unsigned mask = __ballot_sync(DT_FULL, live);
         while (true) {
-            const double4 raw0 = *reinterpret_cast<const double4 *>(a.nodes + node);
+            const double4 raw0 = dt_ldg256(a.nodes + node);  // one 256-bit load
             const double center = raw0.x, half = raw0.y;
             const int2 lr = make_int2(__double2loint(raw0.z), __double2hiint(raw0.z));
             const int2 se = make_int2(__double2loint(raw0.w), __double2hiint(raw0.w));
@@ -1047,6 +1047,9 @@ extern "C" int dt_tree_phi_sum_packed(const void *packed_nodes, int64_t n_nodes,
         return DT_OK;
     DT_CHECK_ARG(packed_nodes && moments && ys && out && (n_src == 0 || xq), "null pointer");
     DT_CHECK_ARG(!adaptive || (cos_tab && sin_tab), "null contour tables");
+    DT_CHECK_ARG(((uintptr_t)packed_nodes & 31) == 0 && ((uintptr_t)xq & 15) == 0 &&
+                     ((uintptr_t)moments & 15) == 0,
+                 "packed nodes must be 32-byte aligned, sources and moments 16-byte aligned");
     if (!workspace || workspace_bytes < DT_EVAL_COUNTER_BYTES)
         return dt_set_error(DT_ERR_WORKSPACE, "eval workspace too small");
     EvalArgs a{};
@@ -1102,6 +1105,9 @@ extern "C" int dt_tree_field_packed(const void *packed_nodes, int64_t n_nodes,
     DT_CHECK_ARG(packed_nodes && moments && ys && out && (n_src == 0 || (xq && xs && prefix)),
                  "null pointer");
     DT_CHECK_ARG(!adaptive || (cos_tab && sin_tab), "null contour tables");
+    DT_CHECK_ARG(((uintptr_t)packed_nodes & 31) == 0 && ((uintptr_t)xq & 15) == 0 &&
+                     ((uintptr_t)moments & 15) == 0,
+                 "packed nodes must be 32-byte aligned, sources and moments 16-byte aligned");
     if (!workspace || workspace_bytes < DT_EVAL_COUNTER_BYTES)
         return dt_set_error(DT_ERR_WORKSPACE, "eval workspace too small");
     for (const void *ptr : {(const void *)ys, (const void *)out}) {
@@ -1167,6 +1173,9 @@ extern "C" int dt_tree_eval_device(const void *packed_nodes, const int64_t *meta
         return DT_OK;
     DT_CHECK_ARG(packed_nodes && moments && ys && out && (n_src == 0 || xq), "null pointer");
     DT_CHECK_ARG(!adaptive || (cos_tab && sin_tab), "null contour tables");
+    DT_CHECK_ARG(((uintptr_t)packed_nodes & 31) == 0 && ((uintptr_t)xq & 15) == 0 &&
+                     ((uintptr_t)moments & 15) == 0,
+                 "packed nodes must be 32-byte aligned, sources and moments 16-byte aligned");
     if (!workspace || workspace_bytes < DT_EVAL_COUNTER_BYTES)
         return dt_set_error(DT_ERR_WORKSPACE, "eval workspace too small");
     EvalArgs a{};

@@ -112,6 +112,17 @@ def test_field_packed_abi_device_and_host(dt, case):
         _tol_share(tree, cfg), int(tree.moment_order), p(cos_t), p(sin_t), cos_t.numel(),
         ys.data_ptr(), out.data_ptr(), 0, len(ys), None, p(ws), ws.numel(), None)
     assert rc == -1 and b"pinned" in L.dt_last_error()
+    # misaligned node records (32-byte loads) and moment rows are refused
+    ys = torch.from_numpy(w.targets.copy()).cuda()
+    out = torch.empty_like(ys)
+    for shift_nodes, shift_m in ((16, 0), (0, 8)):
+        rc = L.dt_tree_field_packed(
+            tree.packed.data_ptr() + shift_nodes, len(tree), tree.meval.data_ptr() + shift_m,
+            tree.meval.shape[1], p(tree.xq), p(system.xs), p(system.prefix), len(system),
+            kernel.r_d ** 2, float(cfg.theta), int(cfg.p), 1, _tol_share(tree, cfg),
+            int(tree.moment_order), p(cos_t), p(sin_t), cos_t.numel(), ys.data_ptr(),
+            out.data_ptr(), 0, len(ys), None, p(ws), ws.numel(), None)
+        assert rc == -1 and b"aligned" in L.dt_last_error()
 
 
 def test_unsorted_host_targets_take_the_sorting_path(dt, case):
