@@ -231,7 +231,7 @@ typedef struct dt_eval_stats {
 /* Interleave (x_j, q_j) into xq[2n] for the traversal kernel.  The packed
  * evaluators read the node records with 32-byte loads and xq and the moment
  * rows with 16-byte loads: packed must be 32-byte aligned, xq and moments
- * 16-byte aligned (DT_ERR_INVALID otherwise). */
+ * 16-byte aligned and the moment stride even (DT_ERR_INVALID otherwise). */
 int dt_pack_sources(const double *xs, const double *qs, int64_t n, double *xq, void *stream);
 /* Pack the SoA node arrays into 32-byte records (`packed`, n_nodes). */
 int dt_pack_tree(const double *centers, const double *halves, const int64_t *starts,

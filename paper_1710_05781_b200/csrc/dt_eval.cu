@@ -1050,6 +1050,7 @@ extern "C" int dt_tree_phi_sum_packed(const void *packed_nodes, int64_t n_nodes,
     DT_CHECK_ARG(((uintptr_t)packed_nodes & 31) == 0 && ((uintptr_t)xq & 15) == 0 &&
                      ((uintptr_t)moments & 15) == 0,
                  "packed nodes must be 32-byte aligned, sources and moments 16-byte aligned");
+    DT_CHECK_ARG((moment_stride & 1) == 0, "moment_stride must be even (16-byte rows)");
     if (!workspace || workspace_bytes < DT_EVAL_COUNTER_BYTES)
         return dt_set_error(DT_ERR_WORKSPACE, "eval workspace too small");
     EvalArgs a{};
@@ -1108,6 +1109,7 @@ extern "C" int dt_tree_field_packed(const void *packed_nodes, int64_t n_nodes,
     DT_CHECK_ARG(((uintptr_t)packed_nodes & 31) == 0 && ((uintptr_t)xq & 15) == 0 &&
                      ((uintptr_t)moments & 15) == 0,
                  "packed nodes must be 32-byte aligned, sources and moments 16-byte aligned");
+    DT_CHECK_ARG((moment_stride & 1) == 0, "moment_stride must be even (16-byte rows)");
     if (!workspace || workspace_bytes < DT_EVAL_COUNTER_BYTES)
         return dt_set_error(DT_ERR_WORKSPACE, "eval workspace too small");
     for (const void *ptr : {(const void *)ys, (const void *)out}) {
@@ -1176,6 +1178,7 @@ extern "C" int dt_tree_eval_device(const void *packed_nodes, const int64_t *meta
     DT_CHECK_ARG(((uintptr_t)packed_nodes & 31) == 0 && ((uintptr_t)xq & 15) == 0 &&
                      ((uintptr_t)moments & 15) == 0,
                  "packed nodes must be 32-byte aligned, sources and moments 16-byte aligned");
+    DT_CHECK_ARG((moment_stride & 1) == 0, "moment_stride must be even (16-byte rows)");
     if (!workspace || workspace_bytes < DT_EVAL_COUNTER_BYTES)
         return dt_set_error(DT_ERR_WORKSPACE, "eval workspace too small");
     EvalArgs a{};

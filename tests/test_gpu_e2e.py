@@ -123,6 +123,12 @@ def test_field_packed_abi_device_and_host(dt, case):
             int(tree.moment_order), p(cos_t), p(sin_t), cos_t.numel(), ys.data_ptr(),
             out.data_ptr(), 0, len(ys), None, p(ws), ws.numel(), None)
         assert rc == -1 and b"aligned" in L.dt_last_error()
+    rc = L.dt_tree_field_packed(
+        p(tree.packed), len(tree), p(tree.meval), tree.meval.shape[1] - 1, p(tree.xq),
+        p(system.xs), p(system.prefix), len(system), kernel.r_d ** 2, float(cfg.theta),
+        int(cfg.p), 1, _tol_share(tree, cfg), int(tree.moment_order), p(cos_t), p(sin_t),
+        cos_t.numel(), ys.data_ptr(), out.data_ptr(), 0, len(ys), None, p(ws), ws.numel(), None)
+    assert rc == -1 and b"even" in L.dt_last_error()
 
 
 def test_unsorted_host_targets_take_the_sorting_path(dt, case):
