@@ -478,20 +478,31 @@ __device__ __forceinline__ double far_sum(const FarPre &f, const double2 *__rest
     // go to acc and odd ones to acc1 on both paths, so a target's result does
     // not depend on which warp (pmin) evaluated it
     const double *M = reinterpret_cast<const double *>(M2);
-#pragma unroll 1
-    for (; k <= pmax; ++k) {
-        const double pa = __fma_rn(-ir3, gm2, -inv * gm3);
-        const double t = __fma_rn(__fma_rn(a0, c_rcp[k - 1], -ci), gm1, pa);
-        if (k <= pu) {
-            if (k & 1)
-                acc1 = __fma_rn(t, __ldg(M + k), acc1);
-            else
-                acc = __fma_rn(t, __ldg(M + k), acc);
-        }
-        gm3 = gm2;
-        gm2 = gm1;
-        gm1 = t;
+    // three orders per trip (the recurrence values rotate through the same
+    // registers, no moves), leaving after any order: nothing is live after
+#define DT_TAIL_STEP(KK, G3, G2, G1, OUT)                                         \
+    const double OUT = __fma_rn(__fma_rn(a0, c_rcp[(KK) - 1], -ci), G1,           \
+                                __fma_rn(-ir3, G2, -inv * G3));                   \
+    if ((KK) <= pu) {                                                             \
+        if ((KK) & 1)                                                             \
+            acc1 = __fma_rn(OUT, __ldg(M + (KK)), acc1);                          \
+        else                                                                      \
+            acc = __fma_rn(OUT, __ldg(M + (KK)), acc);                            \
     }
+#pragma unroll 1
+    for (; k <= pmax; k += 3) {
+        DT_TAIL_STEP(k, gm3, gm2, gm1, t0)
+        if (k + 1 > pmax)
+            break;
+        DT_TAIL_STEP(k + 1, gm2, gm1, t0, t1)
+        if (k + 2 > pmax)
+            break;
+        DT_TAIL_STEP(k + 2, gm1, t0, t1, t2)
+        gm3 = t0;
+        gm2 = t1;
+        gm1 = t2;
+    }
+#undef DT_TAIL_STEP
     return acc + acc1;
 }
 
