@@ -141,7 +141,9 @@ int dt_build_tree(const double *xs, int64_t n, int64_t leaf_capacity, int64_t ma
  * produced by
  * dt_build_tree (meta gives n_nodes); node_capacity bounds the node arrays.
  * moments_eval (optional) receives the traversal layout used by the *_packed
- * and *_device evaluators: M'_0 = m_0, M'_k = (k-1)! m_k, row stride
+ * and *_device evaluators: M_0 = m_0, M_k = (k-1)! gamma_(k-1) m_k with
+ * gamma_0 = gamma_1 = 1, gamma_n = (n+1)/n gamma_(n-2) (the scaling of the
+ * three-term far-field recurrence, csrc/dt_farcoef.cuh), row stride
  * eval_stride (even, >= order + 1; padding zeroed). */
 size_t dt_moments_workspace(int64_t node_capacity);
 int dt_moments(const double *xs, const double *qs, const double *center, const int64_t *start,
@@ -263,7 +265,7 @@ int dt_tree_phi_sum(const double *centers, const double *halves, const int64_t *
                     void *workspace, size_t workspace_bytes, void *stream);
 
 /* Same, on pre-packed nodes/sources and traversal-layout moments (dt_moments
- * moments_eval: M'_k = (k-1)! m_k, even stride); what the Python layer uses.
+ * moments_eval, even stride); what the Python layer uses.
  * `stats`
  * (host struct of device pointers, indexed by target) may be NULL; psel_mode
  * is DT_PSEL_FAST or DT_PSEL_EXACT. */

@@ -38,6 +38,7 @@
 #include <algorithm>
 
 #include "dt_common.cuh"
+#include "dt_farcoef.cuh"
 
 namespace {
 
@@ -344,173 +345,86 @@ __device__ int psel_fast(double big_r, double h, const EvalArgs &a, const float 
 
 // ------------------------------------------------------------------ far / near
 
-__constant__ double c_rcp[128] = {  // 1/k (k >= 1)
-    0.0, 0x1.0000000000000p+0, 0x1.0000000000000p-1, 0x1.5555555555555p-2,
-    0x1.0000000000000p-2, 0x1.999999999999ap-3, 0x1.5555555555555p-3, 0x1.2492492492492p-3,
-    0x1.0000000000000p-3, 0x1.c71c71c71c71cp-4, 0x1.999999999999ap-4, 0x1.745d1745d1746p-4,
-    0x1.5555555555555p-4, 0x1.3b13b13b13b14p-4, 0x1.2492492492492p-4, 0x1.1111111111111p-4,
-    0x1.0000000000000p-4, 0x1.e1e1e1e1e1e1ep-5, 0x1.c71c71c71c71cp-5, 0x1.af286bca1af28p-5,
-    0x1.999999999999ap-5, 0x1.8618618618618p-5, 0x1.745d1745d1746p-5, 0x1.642c8590b2164p-5,
-    0x1.5555555555555p-5, 0x1.47ae147ae147bp-5, 0x1.3b13b13b13b14p-5, 0x1.2f684bda12f68p-5,
-    0x1.2492492492492p-5, 0x1.1a7b9611a7b96p-5, 0x1.1111111111111p-5, 0x1.0842108421084p-5,
-    0x1.0000000000000p-5, 0x1.f07c1f07c1f08p-6, 0x1.e1e1e1e1e1e1ep-6, 0x1.d41d41d41d41dp-6,
-    0x1.c71c71c71c71cp-6, 0x1.bacf914c1bad0p-6, 0x1.af286bca1af28p-6, 0x1.a41a41a41a41ap-6,
-    0x1.999999999999ap-6, 0x1.8f9c18f9c18fap-6, 0x1.8618618618618p-6, 0x1.7d05f417d05f4p-6,
-    0x1.745d1745d1746p-6, 0x1.6c16c16c16c17p-6, 0x1.642c8590b2164p-6, 0x1.5c9882b931057p-6,
-    0x1.5555555555555p-6, 0x1.4e5e0a72f0539p-6, 0x1.47ae147ae147bp-6, 0x1.4141414141414p-6,
-    0x1.3b13b13b13b14p-6, 0x1.3521cfb2b78c1p-6, 0x1.2f684bda12f68p-6, 0x1.29e4129e4129ep-6,
-    0x1.2492492492492p-6, 0x1.1f7047dc11f70p-6, 0x1.1a7b9611a7b96p-6, 0x1.15b1e5f75270dp-6,
-    0x1.1111111111111p-6, 0x1.0c9714fbcda3bp-6, 0x1.0842108421084p-6, 0x1.0410410410410p-6,
-    0x1.0000000000000p-6, 0x1.f81f81f81f820p-7, 0x1.f07c1f07c1f08p-7, 0x1.e9131abf0b767p-7,
-    0x1.e1e1e1e1e1e1ep-7, 0x1.dae6076b981dbp-7, 0x1.d41d41d41d41dp-7, 0x1.cd85689039b0bp-7,
-    0x1.c71c71c71c71cp-7, 0x1.c0e070381c0e0p-7, 0x1.bacf914c1bad0p-7, 0x1.b4e81b4e81b4fp-7,
-    0x1.af286bca1af28p-7, 0x1.a98ef606a63bep-7, 0x1.a41a41a41a41ap-7, 0x1.9ec8e951033d9p-7,
-    0x1.999999999999ap-7, 0x1.948b0fcd6e9e0p-7, 0x1.8f9c18f9c18fap-7, 0x1.8acb90f6bf3aap-7,
-    0x1.8618618618618p-7, 0x1.8181818181818p-7, 0x1.7d05f417d05f4p-7, 0x1.78a4c8178a4c8p-7,
-    0x1.745d1745d1746p-7, 0x1.702e05c0b8170p-7, 0x1.6c16c16c16c17p-7, 0x1.6816816816817p-7,
-    0x1.642c8590b2164p-7, 0x1.6058160581606p-7, 0x1.5c9882b931057p-7, 0x1.58ed2308158edp-7,
-    0x1.5555555555555p-7, 0x1.51d07eae2f815p-7, 0x1.4e5e0a72f0539p-7, 0x1.4afd6a052bf5bp-7,
-    0x1.47ae147ae147bp-7, 0x1.446f86562d9fbp-7, 0x1.4141414141414p-7, 0x1.3e22cbce4a902p-7,
-    0x1.3b13b13b13b14p-7, 0x1.3813813813814p-7, 0x1.3521cfb2b78c1p-7, 0x1.323e34a2b10bfp-7,
-    0x1.2f684bda12f68p-7, 0x1.2c9fb4d812ca0p-7, 0x1.29e4129e4129ep-7, 0x1.27350b8812735p-7,
-    0x1.2492492492492p-7, 0x1.21fb78121fb78p-7, 0x1.1f7047dc11f70p-7, 0x1.1cf06ada2811dp-7,
-    0x1.1a7b9611a7b96p-7, 0x1.1811811811812p-7, 0x1.15b1e5f75270dp-7, 0x1.135c81135c811p-7,
-    0x1.1111111111111p-7, 0x1.0ecf56be69c90p-7, 0x1.0c9714fbcda3bp-7, 0x1.0a6810a6810a7p-7,
-    0x1.0842108421084p-7, 0x1.0624dd2f1a9fcp-7, 0x1.0410410410410p-7, 0x1.0204081020408p-7,
-};
-
 // sum_k Phi^(k)(c, y) m_k, k <= pu (lanes share pmax = max pu over the warp).
-// Phi^(k) follows the reference's recurrence (kernel.py:92-127, Eq. 10) in the
-// scaled variable g_k = Phi^(k) / (k-1)!:
-//   g_k = (a0/(k-1) - ci) g_{k-1} - ir3 g_{k-2} - inv g_{k-3},   k >= 4,
-//   a0 = rd2/(d s2), ci = (3d^2 + rd2)/(d s2), ir3 = 3/s2, inv = 1/(d s2),
-// with g_2, g_3 from the same formula without the vanishing terms.  The
-// matching moments M'_k = (k-1)! m_k come from dt_moments (row stride even,
-// 16-byte aligned, read two at a time).  5 FP64 instructions per order.
-struct FarPre {
-    double g0, g1, g2, g3, a0, ci, ir3, inv;
-};
-
-__device__ __forceinline__ FarPre far_setup(double d, double rd2)
-{
-    FarPre f;
-    const double s2 = __fma_rn(d, d, rd2);
-    const double r = dt_rsqrt(s2);
-    const double ir2 = r * r;
-    f.g0 = d * r;
-    f.g1 = rd2 * r * ir2;
-    f.inv = ir2 * dt_rcp(d);
-    f.a0 = rd2 * f.inv;
-    f.ci = __fma_rn(3.0 * d, d, rd2) * f.inv;
-    f.ir3 = 3.0 * ir2;
-    f.g2 = (f.a0 - f.ci) * f.g1;
-    f.g3 = __fma_rn(-f.ir3, f.g1, __fma_rn(f.a0, 0.5, -f.ci) * f.g2);
-    return f;
-}
-
-template <bool WIDE>
-__device__ __forceinline__ double far_field(double d, double rd2, const double2 *__restrict__ M2,
-                                            int pu, int pmin, int pmax);
-
-template <bool WIDE>
-__device__ __forceinline__ double far_sum(const FarPre &f, const double2 *__restrict__ M2,
-                                          int pu, int pmin, int pmax)
-{
-    const double a0 = f.a0, ci = f.ci, ir3 = f.ir3, inv = f.inv;
-    const double g1 = f.g1, g2 = f.g2, g3 = f.g3;
-    const double2 m01 = __ldg(M2);
-    double acc = f.g0 * m01.x;
-    if (pmin >= 3) {  // every far lane needs orders 0..3: no guards
-        const double2 m23 = __ldg(M2 + 1);
-        acc = __fma_rn(g1, m01.y, acc);
-        acc = __fma_rn(g2, m23.x, acc);
-        acc = __fma_rn(g3, m23.y, acc);
-    } else {
-        if (pmax < 1)
-            return acc;
-        if (pu >= 1)
-            acc = __fma_rn(g1, m01.y, acc);
-        if (pmax < 2)
-            return acc;
-        const double2 m23 = __ldg(M2 + 1);
-        if (pu >= 2)
-            acc = __fma_rn(g2, m23.x, acc);
-        if (pmax < 3)
-            return acc;
-        if (pu >= 3)
-            acc = __fma_rn(g3, m23.y, acc);
-    }
-    // The g_{k-2}, g_{k-3} part of each step is formed off the critical
-    // path: the recurrence carries one dependent DFMA per order; a second
-    // accumulator halves the accumulation chain.
-    double gm3 = g1, gm2 = g2, gm1 = g3;
-    double acc1 = 0.0;
-    int k = 4;
-    if (!WIDE) {
-        // orders every far lane of the warp needs (k <= pmin): no masking.
-        // Exits every three orders, so each recurrence value is live at one
-        // exit only and needs no register moves.
-#define DT_FAR_STEP(KK, G3, G2, G1, OUT)                                          \
-    const double OUT = __fma_rn(__fma_rn(a0, c_rcp[(KK) - 1], -ci), G1,           \
-                                __fma_rn(-ir3, G2, -inv * G3));                   \
-    {                                                                             \
-        const double2 mm_ = __ldg(M2 + (KK) / 2);                                 \
-        if ((KK) & 1)                                                             \
-            acc1 = __fma_rn(OUT, mm_.y, acc1);                                    \
-        else                                                                      \
-            acc = __fma_rn(OUT, mm_.x, acc);                                      \
-    }
-#pragma unroll
-        for (int kk = 4; kk + 2 <= 31; kk += 3) {
-            if (kk + 2 > pmin)
-                break;
-            DT_FAR_STEP(kk, gm3, gm2, gm1, v0)
-            DT_FAR_STEP(kk + 1, gm2, gm1, v0, v1)
-            DT_FAR_STEP(kk + 2, gm1, v0, v1, v2)
-            gm3 = v0;
-            gm2 = v1;
-            gm1 = v2;
-            k = kk + 3;
-        }
-#undef DT_FAR_STEP
-    }
-    // remaining orders up to the warp maximum, masked per lane; even orders
-    // go to acc and odd ones to acc1 on both paths, so a target's result does
-    // not depend on which warp (pmin) evaluated it
-    const double *M = reinterpret_cast<const double *>(M2);
-    // three orders per trip (the recurrence values rotate through the same
-    // registers, no moves), leaving after any order: nothing is live after
-#define DT_TAIL_STEP(KK, G3, G2, G1, OUT)                                         \
-    const double OUT = __fma_rn(__fma_rn(a0, c_rcp[(KK) - 1], -ci), G1,           \
-                                __fma_rn(-ir3, G2, -inv * G3));                   \
-    if ((KK) <= pu) {                                                             \
-        if ((KK) & 1)                                                             \
-            acc1 = __fma_rn(OUT, __ldg(M + (KK)), acc1);                          \
-        else                                                                      \
-            acc = __fma_rn(OUT, __ldg(M + (KK)), acc);                            \
-    }
-#pragma unroll 1
-    for (; k <= pmax; k += 3) {
-        DT_TAIL_STEP(k, gm3, gm2, gm1, t0)
-        if (k + 1 > pmax)
-            break;
-        DT_TAIL_STEP(k + 1, gm2, gm1, t0, t1)
-        if (k + 2 > pmax)
-            break;
-        DT_TAIL_STEP(k + 2, gm1, t0, t1, t2)
-        gm3 = t0;
-        gm2 = t1;
-        gm1 = t2;
-    }
-#undef DT_TAIL_STEP
-    return acc + acc1;
-}
-
+// The reference evaluates Phi^(k) by the four-term recurrence of Eq. 10
+// (kernel.py:92-127); the same derivatives obey the three-term Gegenbauer
+// recurrence of dt_farcoef.cuh, which needs no 1/d and costs four FP64
+// instructions per order (two DMUL off the critical path, the recurrence
+// DFMA, the moment DFMA) against five:
+//   h_k = c_hcoef[k] u h_(k-1) - w h_(k-2),   u = d/s2, w = 1/s2, s2 = d^2 + r_d^2,
+// h_1 = r_d^2 / s2^(3/2), h_2 = -3 u h_1, with the traversal moments M_k
+// scaled to match (dt_moments, row stride even, 16-byte aligned, read two at
+// a time).  The sum agrees with the reference's to round-off.  Orders every
+// far lane of the warp needs (k <= pmin) run unmasked in unrolled pairs;
+// the rest up to the warp maximum is masked per lane.  Even orders go to acc
+// and odd ones to acc1 on both paths, so a target's result depends on its
+// own p only, not on which warp (pmin, pmax) evaluated it.
 template <bool WIDE>
 __device__ __forceinline__ double far_field(double d, double rd2, const double2 *__restrict__ M2,
                                             int pu, int pmin, int pmax)
 {
-    return far_sum<WIDE>(far_setup(d, rd2), M2, pu, pmin, pmax);
+    const double s2 = __fma_rn(d, d, rd2);
+    const double r = dt_rsqrt(s2);
+    const double w = r * r;
+    const double u = d * w;
+    const double2 m01 = __ldg(M2);
+    double acc = (d * r) * m01.x;
+    double acc1 = 0.0;
+    if (pmax < 1)
+        return acc;
+    const double h1 = rd2 * r * w;
+    if (pu >= 1)
+        acc1 = __fma_rn(h1, m01.y, acc1);
+    if (pmax < 2)
+        return acc + acc1;
+    const double h2 = (-3.0 * u) * h1;
+    if (pu >= 2)
+        acc = __fma_rn(h2, __ldg(M2 + 1).x, acc);
+    double hm2 = h1, hm1 = h2;
+    int k = 3;
+#define DT_FAR_STEP(KK, H2, H1, OUT)                                              \
+    const double OUT = __fma_rn(u * c_hcoef[KK], H1, -(w * H2));
+    if (!WIDE) {
+        // unmasked pairs (odd, even): the two recurrence values swap roles
+        // every order, so each pair ends with them back in place
+#pragma unroll
+        for (int kk = 3; kk + 1 <= 31; kk += 2) {
+            if (kk + 1 > pmin)
+                break;
+            DT_FAR_STEP(kk, hm2, hm1, v0)
+            DT_FAR_STEP(kk + 1, hm1, v0, v1)
+            // kk odd: M_kk = M2[kk / 2].y, M_(kk+1) = M2[(kk + 1) / 2].x
+            acc1 = __fma_rn(v0, __ldg(M2 + kk / 2).y, acc1);
+            acc = __fma_rn(v1, __ldg(M2 + (kk + 1) / 2).x, acc);
+            hm2 = v0;
+            hm1 = v1;
+            k = kk + 2;
+        }
+    }
+    const double *M = reinterpret_cast<const double *>(M2);
+#pragma unroll 1
+    for (; k <= pmax; k += 2) {
+        DT_FAR_STEP(k, hm2, hm1, t0)
+        if (k <= pu) {
+            if (k & 1)
+                acc1 = __fma_rn(t0, __ldg(M + k), acc1);
+            else
+                acc = __fma_rn(t0, __ldg(M + k), acc);
+        }
+        if (k + 1 > pmax)
+            break;
+        DT_FAR_STEP(k + 1, hm1, t0, t1)
+        if (k + 1 <= pu) {
+            if ((k + 1) & 1)
+                acc1 = __fma_rn(t1, __ldg(M + k + 1), acc1);
+            else
+                acc = __fma_rn(t1, __ldg(M + k + 1), acc);
+        }
+        hm2 = t0;
+        hm1 = t1;
+    }
+#undef DT_FAR_STEP
+    return acc + acc1;
 }
 
 // acc + q (x - y) / sqrt((x - y)^2 + r_d^2) (nvcc contracts the final
@@ -844,8 +758,9 @@ __global__ void pack_tree_kernel(const double *__restrict__ c, const double *__r
     out[i] = nd;
 }
 
-// Reference-semantics moments [n][stride] -> traversal layout M'_0 = m_0,
-// M'_k = (k-1)! m_k, even stride (for the seam mirror dt_tree_phi_sum).
+// Reference-semantics moments [n][stride] -> traversal layout M_0 = m_0,
+// M_k = c_mev_m[k] m_k (dt_farcoef.cuh), even stride (for the seam mirror
+// dt_tree_phi_sum).
 __global__ void scale_moments_kernel(const double *__restrict__ m, int64_t stride, int64_t n,
                                      double *__restrict__ out, int64_t estride)
 {
@@ -857,11 +772,8 @@ __global__ void scale_moments_kernel(const double *__restrict__ m, int64_t strid
     double v = 0.0;
     if (k < stride) {
         v = m[node * stride + k];
-        double f = 1.0;
-        for (int j = 2; j < k; ++j)
-            f *= (double)j;
         if (k >= 1)
-            v = __dmul_rn(v, f);
+            v = __dmul_rn(v, c_mev_m[k]);
     }
     out[i] = v;
 }

@@ -24,6 +24,7 @@
 // per internal node (two child rows read, one row written).
 
 #include "dt_common.cuh"
+#include "dt_farcoef.cuh"
 
 #ifndef DT_P2M_G
 #define DT_P2M_G 2
@@ -41,7 +42,7 @@ struct MomArgs {
     const int64_t *start, *end, *left, *right, *meta;
     int64_t order;
     double *moments;
-    double *meval;     // optional traversal copy: M'_0 = m_0, M'_k = (k-1)! m_k
+    double *meval;     // optional traversal copy: M_0 = m_0, M_k = (k-1)! gamma_(k-1) m_k
     int64_t estride;   // its row stride (even, >= order + 1; pad entries are 0)
     int32_t *parent;   // workspace: parent index per node (-1 at the root)
     int32_t *arrived;  // workspace: finished children per node
@@ -160,19 +161,19 @@ __device__ __forceinline__ void put_moment(const MomArgs &a, int64_t node, int k
 {
     a.moments[node * (a.order + 1) + k] = m;
     if (a.meval) {
-        a.meval[node * a.estride + k] = k == 0 ? m : __dmul_rn(m, c_fact_km1[k]);
+        a.meval[node * a.estride + k] = k == 0 ? m : __dmul_rn(m, c_mev_m[k]);
         if (k == a.order && a.estride > a.order + 1)
             a.meval[node * a.estride + k + 1] = 0.0;
     }
 }
 
 // Store from the raw power sum S_k = sum_j q_j (x_j - c)^k:
-// m_k = S_k / k!, traversal copy (k-1)! m_k = S_k / k.
+// m_k = S_k / k!, traversal copy M_k = gamma_(k-1) S_k / k (dt_farcoef.cuh).
 __device__ __forceinline__ void put_raw_sum(const MomArgs &a, int64_t node, int k, double S)
 {
     a.moments[node * (a.order + 1) + k] = __dmul_rn(S, c_inv_fact[k]);
     if (a.meval) {
-        a.meval[node * a.estride + k] = k == 0 ? S : __dmul_rn(S, c_inv_k[k]);
+        a.meval[node * a.estride + k] = k == 0 ? S : __dmul_rn(S, c_mev_s[k]);
         if (k == a.order && a.estride > a.order + 1)
             a.meval[node * a.estride + k + 1] = 0.0;
     }
