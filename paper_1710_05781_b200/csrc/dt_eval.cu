@@ -351,7 +351,7 @@ __device__ int psel_fast(double big_r, double h, const EvalArgs &a, const float 
 // recurrence of dt_farcoef.cuh, which needs no 1/d and costs four FP64
 // instructions per order (two DMUL off the critical path, the recurrence
 // DFMA, the moment DFMA) against five:
-//   h_k = c_hcoef[k] u h_(k-1) - w h_(k-2),   u = d/s2, w = 1/s2, s2 = d^2 + r_d^2,
+//   h_k = c_k u h_(k-1) - w h_(k-2),   u = d/s2, w = 1/s2, s2 = d^2 + r_d^2,
 // h_1 = r_d^2 / s2^(3/2), h_2 = -3 u h_1, with the traversal moments M_k
 // scaled to match (dt_moments, row stride even, 16-byte aligned, read two at
 // a time).  The sum agrees with the reference's to round-off.  Orders every
@@ -383,7 +383,7 @@ __device__ __forceinline__ double far_field(double d, double rd2, const double2 
     double hm2 = h1, hm1 = h2;
     int k = 3;
 #define DT_FAR_STEP(KK, H2, H1, OUT)                                              \
-    const double OUT = __fma_rn(u * c_hcoef[KK], H1, -(w * H2));
+    const double OUT = __fma_rn(u * c_hcoef[(KK) + 1], H1, -(w * H2));
     if (!WIDE) {
         // unmasked pairs (odd, even): the two recurrence values swap roles
         // every order, so each pair ends with them back in place
@@ -398,8 +398,9 @@ __device__ __forceinline__ double far_field(double d, double rd2, const double2 
             acc = __fma_rn(v1, __ldg(M2 + (kk + 1) / 2).x, acc);
             hm2 = v0;
             hm1 = v1;
-            k = kk + 2;
         }
+        // the pairs above ran for kk = 3, 5, .. while kk + 1 <= min(pmin, 31)
+        k = 3 + 2 * max(0, (min(pmin, 31) - 2) / 2);
     }
     const double *M = reinterpret_cast<const double *>(M2);
 #pragma unroll 1
