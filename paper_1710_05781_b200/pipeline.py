@@ -61,7 +61,7 @@ class TreePipeline:
         self.sign_ws = torch.empty(self.sign_ws_bytes, dtype=torch.uint8, device=self.dev)
         self.cos_t, self.sin_t = contour_tables(self.dev)
         self.side = torch.cuda.Stream(self.dev)
-        self.ev_start, self.ev_scan, self.ev_side = (torch.cuda.Event() for _ in range(3))
+        self.ev_scan, self.ev_side = torch.cuda.Event(), torch.cuda.Event()
         # world > 1: sharded upward pass (one all-gather of cut-level rows)
         self.shard = None
         if world > 1 and self.order + 1 <= 32:  # higher orders: replicated moments
@@ -105,22 +105,21 @@ class TreePipeline:
         cfg = self.config
         ys_part = ys[i0:i1]
         out_part = out[i0:i1]
-        # side stream: (x, q) interleave and, after the scan, the sign term --
-        # both overlap the latency-bound build and upward pass
-        self.ev_start.record(main)
-        self.side.wait_event(self.ev_start)
-        with torch.cuda.stream(self.side):
-            pack_sources(xs, qs, self.xq)
+        # side stream: the (x, q) interleave and the sign term overlap the
+        # latency-bound upward pass.  They start after the build: the build
+        # is a cooperative launch, which waits for co-residency with anything
+        # already running.
         _lib.check(L.dt_prefix_scan(p(qs), p(self.prefix), self.n, p(self.scan_ws),
                                     self.scan_ws_bytes, s), "dt_prefix_scan")
+        self.bufs.launch(xs, cfg.leaf_capacity)
         self.ev_scan.record(main)
         self.side.wait_event(self.ev_scan)
         with torch.cuda.stream(self.side):
+            pack_sources(xs, qs, self.xq)
             _lib.check(L.dt_sign_terms(p(xs), p(self.prefix), self.n, p(ys_part), p(out_part),
                                        i1 - i0, p(self.sign_ws), self.sign_ws_bytes,
                                        _lib.stream_handle()), "dt_sign_terms")
             self.ev_side.record(self.side)
-        self.bufs.launch(xs, cfg.leaf_capacity)
         if self.shard is None:
             launch_moments(self.bufs, xs, qs, self.order, self.moments, self.meval)
         else:  # this rank's subtrees + all-gather of the cut-level rows
