@@ -580,6 +580,27 @@ __device__ __forceinline__ void m2m_form_group8(const MomArgs &a, int64_t P)
     }
 }
 
+// Arrival on a node's counter with acquire-release semantics at GPU scope:
+// the release publishes the rows this warp formed (ordered before it by a
+// __syncwarp), the acquire makes the rows behind earlier arrivals visible to
+// the lane that completes the node (and, after a __syncwarp, to its group).
+// One MEMBAR.ALL.GPU per round instead of two MEMBAR.SC.GPU fences.
+__device__ __forceinline__ int arrive_acq_rel(int32_t *p)
+{
+    int old;
+    asm volatile("atom.add.acq_rel.gpu.s32 %0, [%1], 1;" : "=r"(old) : "l"(p) : "memory");
+    return old;
+}
+
+// A leaf's arrival: its row comes from the P2M launch (ordered by the kernel
+// boundary), so only the acquire is needed.
+__device__ __forceinline__ int arrive_acquire(int32_t *p)
+{
+    int old;
+    asm volatile("atom.add.acquire.gpu.s32 %0, [%1], 1;" : "=r"(old) : "l"(p) : "memory");
+    return old;
+}
+
 // Upward pass without grid barriers (after the P2M kernel, which also wrote
 // parent[] and zeroed arrived[]): every leaf bumps its parent's arrival
 // counter; the warp whose arrival completes a parent forms it and keeps
@@ -612,7 +633,7 @@ __global__ void __launch_bounds__(256) m2m_flow_kernel(MomArgs a)
                 in = __ldg(a.start + mine) >= lo && __ldg(a.end + mine) <= hi;
             if (in) {
                 const int need = (__ldg(a.left + par) >= 0) + (__ldg(a.right + par) >= 0);
-                done = atomicAdd(a.arrived + par, 1) == need - 1;
+                done = arrive_acquire(a.arrived + par) == need - 1;
             }
         }
         // lanes hold the parents they completed; four of them are formed at a
@@ -638,15 +659,15 @@ __global__ void __launch_bounds__(256) m2m_flow_kernel(MomArgs a)
                 if ((lane >> 3) == g)
                     mine_p = pg;
             }
-            __threadfence();  // the other children's rows, published before their arrival
+            __syncwarp();  // the completing lanes' acquires precede the group's loads
             m2m_form_group8(a, mine_p);
-            __threadfence();  // publish the rows before announcing them
+            __syncwarp();  // the group's stores precede the releasing arrivals
             if ((sel >> lane) & 1u) {
                 const int64_t q = __ldcg(a.parent + par);
                 int64_t nxt = -1;
                 if (q >= cut_begin && q >= 0) {
                     const int need = (__ldg(a.left + q) >= 0) + (__ldg(a.right + q) >= 0);
-                    if (atomicAdd(a.arrived + q, 1) == need - 1)
+                    if (arrive_acq_rel(a.arrived + q) == need - 1)
                         nxt = q;
                 }
                 par = nxt;
