@@ -508,10 +508,10 @@ __device__ __forceinline__ void m2m_form_warp(const MomArgs &a, int64_t P)
     for (int i = 1; i < REG_ORDER; ++i) {
         const double tl = __shfl_up_sync(DT_FULL, Sl, 1);
         const double tr = __shfl_up_sync(DT_FULL, Sr, 1);
-        if (lane >= i) {
-            Sl = __fma_rn(dl, tl, Sl);
-            Sr = __fma_rn(dr, tr, Sr);
-        }
+        // orders below i take a zero shift (in place, as m2m_form_group8)
+        const bool on = lane >= i;
+        Sl = __fma_rn(on ? dl : 0.0, tl, Sl);
+        Sr = __fma_rn(on ? dr : 0.0, tr, Sr);
     }
     double out = 0.0;
     if (l >= 0)
@@ -558,11 +558,14 @@ __device__ __forceinline__ void m2m_form_group8(const MomArgs &a, int64_t P)
         // descending within the lane: every update reads the previous pass
 #pragma unroll
         for (int u = 3; u >= 0; --u) {
-            const int k = 4 * gl + u;
-            if (k >= i) {
-                Sl[u] = __fma_rn(dl, u ? Sl[u - 1] : nl, Sl[u]);
-                Sr[u] = __fma_rn(dr, u ? Sr[u - 1] : nr, Sr[u]);
-            }
+            // orders k = 4 gl + u < i sit this pass out: their shift is 0,
+            // and fma(0, x, S) = S (up to the sign of a zero S), which keeps
+            // every update in place; gl >= ceil((i - u) / 4) takes at most
+            // two values per pass
+            const bool on = gl >= ((i - u + 3) >> 2);
+            const double el = on ? dl : 0.0, er = on ? dr : 0.0;
+            Sl[u] = __fma_rn(el, u ? Sl[u - 1] : nl, Sl[u]);
+            Sr[u] = __fma_rn(er, u ? Sr[u - 1] : nr, Sr[u]);
         }
     }
     if (P < 0)
@@ -606,7 +609,10 @@ __device__ __forceinline__ int arrive_acquire(int32_t *p)
 // counter; the warp whose arrival completes a parent forms it and keeps
 // climbing while it completes the next ancestor.  With a shard plan the
 // climb stops below the cut level and covers the plan's subtrees only.
-__global__ void __launch_bounds__(256) m2m_flow_kernel(MomArgs a)
+#ifndef DT_M2M_MINB
+#define DT_M2M_MINB 4  // 64 registers: 4 blocks per SM (3: 0.43 ms, 5: 0.42 ms, 4: 0.39 ms)
+#endif
+__global__ void __launch_bounds__(256, DT_M2M_MINB) m2m_flow_kernel(MomArgs a)
 {
     const int lane = dt_lane();
     const int64_t n = __ldg(a.meta + DT_META_NODES);
@@ -645,6 +651,25 @@ __global__ void __launch_bounds__(256) m2m_flow_kernel(MomArgs a)
             const unsigned todo = __ballot_sync(DT_FULL, par >= 0);
             if (!todo)
                 break;
+            if (__popc(todo) == 1) {
+                // a lone parent (the usual case high in a chain): all 32
+                // lanes, one order each, a third of the group form's work
+                const int src = __ffs(todo) - 1;
+                __syncwarp();
+                m2m_form_warp(a, __shfl_sync(DT_FULL, par, src));
+                __syncwarp();
+                if (lane == src) {
+                    const int64_t q = __ldcg(a.parent + par);
+                    int64_t nxt = -1;
+                    if (q >= cut_begin && q >= 0) {
+                        const int need = (__ldg(a.left + q) >= 0) + (__ldg(a.right + q) >= 0);
+                        if (arrive_acq_rel(a.arrived + q) == need - 1)
+                            nxt = q;
+                    }
+                    par = nxt;
+                }
+                continue;
+            }
             unsigned sel = 0, t = todo;
             int64_t mine_p = -1;
 #pragma unroll
