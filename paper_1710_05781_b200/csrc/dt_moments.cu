@@ -492,7 +492,7 @@ __global__ void __launch_bounds__(256) p2m_group_kernel(MomArgs a)
 // delta^(k-j) S_j is applied in place as 31 passes of S_k += delta S_(k-1)
 // (Pascal's rule; the previous pass's S_(k-1) comes from lane k-1).  Both
 // children run in the same passes.  Same arithmetic, term for term, as the
-// thread-per-node form m2m_level_threads.
+// thread-per-node form m2m_level_threads (skipped orders take a zero shift).
 __device__ __forceinline__ void m2m_form_warp(const MomArgs &a, int64_t P)
 {
     const int lane = dt_lane();
@@ -526,7 +526,9 @@ __device__ __forceinline__ void m2m_form_warp(const MomArgs &a, int64_t P)
 // g), lane l of a group holding orders 4l .. 4l + 3 of both children.  A
 // Pascal pass then needs one neighbour value per lane (the last order of
 // lane l - 1), so a parent costs 8x fewer shuffles than with one order per
-// lane.  Same arithmetic, term for term, as m2m_form_warp / the thread form.
+// lane.  Same arithmetic, term for term, as m2m_form_warp / the thread form
+// (orders a pass skips take a zero shift, fma(0, x, S) = S: equal values, a
+// zero's sign aside).
 __device__ __forceinline__ void m2m_form_group8(const MomArgs &a, int64_t P)
 {
     const int gl = dt_lane() & 7;  // lane within the group
