@@ -346,7 +346,8 @@ def test_sharded_evaluation_is_partition_invariant(dt):
 
 
 @pytest.mark.parametrize("p,adaptive,tol", [(40, False, 1e-10), (45, True, 1e-14),
-                                             (64, False, 1e-10)])
+                                             (64, False, 1e-10), (100, False, 1e-10),
+                                             (127, False, 1e-10)])
 def test_high_order_paths(dt, p, adaptive, tol):
     """Moment orders above 31: the warp-per-leaf dataflow upward pass and the
     wide (rolled) far-field loop.  Interaction lists hash-identical to the
@@ -384,4 +385,14 @@ def test_high_order_paths(dt, p, adaptive, tol):
     np.testing.assert_array_equal(bufs["hash"].cpu().numpy().view(np.uint64), ost.hash)
     np.testing.assert_array_equal(bufs["sum_p"].cpu().numpy(), ost.sum_p)
     assert bufs["sum_p"].sum().item() > 0
-    assert np.max(np.abs(out.cpu().numpy() - phi_o)) <= 1e-12 * np.abs(qs).sum()
+    got = out.cpu().numpy()
+    assert np.isfinite(got).all()
+    if np.isfinite(phi_o).all():
+        assert np.max(np.abs(got - phi_o)) <= 1e-12 * np.abs(qs).sum()
+    else:
+        # the reference's four-term recurrence overflows (k!/rho^k) at the
+        # top orders; the scaled three-term one does not: check against the
+        # direct sum instead (the truncation error is negligible at p = 127)
+        d = t[:, None] - xs[None, :]
+        phi_d = (qs[None, :] * (xs[None, :] - t[:, None]) / np.sqrt(d * d + r_d ** 2)).sum(1)
+        assert np.max(np.abs(got - phi_d)) <= 1e-11 * np.abs(qs).sum()
