@@ -53,7 +53,10 @@ struct BuildArgs {
 // because xs is sorted.  So the lower_bounds of the 2^(K+1) - 1 midpoints of
 // levels 0..K are found by independent searches in one parallel phase
 // instead of K + 1 dependent rounds of DRAM-latency binary searches.
-constexpr int DYADIC_LEVELS = 12;  // levels 0..11
+#ifndef DT_DYADIC_LEVELS
+#define DT_DYADIC_LEVELS 16  // 12: 0.398 ms, 14: 0.383, 16: 0.370, 18: 0.368, 20: 0.408 (configs[2])
+#endif
+constexpr int DYADIC_LEVELS = DT_DYADIC_LEVELS;  // levels 0..DYADIC_LEVELS-1
 constexpr int DYADIC = (1 << DYADIC_LEVELS) - 1;
 
 __device__ __forceinline__ double mid_of(double lo, double hi)
