@@ -23,11 +23,17 @@ namespace cg = cooperative_groups;
 
 namespace {
 
-constexpr int BUILD_THREADS = 512;
+#ifndef DT_BUILD_THREADS
+#define DT_BUILD_THREADS 512
+#endif
+constexpr int BUILD_THREADS = DT_BUILD_THREADS;
 #ifndef DT_BUILD_SMALL
 #define DT_BUILD_SMALL (2 * BUILD_THREADS)
 #endif
-constexpr int SMALL_LEVEL = DT_BUILD_SMALL;  // nodes handled by block 0 alone
+constexpr int SMALL_LEVEL = DT_BUILD_SMALL;
+#ifndef DT_BUILD_FLAGWAIT
+#define DT_BUILD_FLAGWAIT 1
+#endif  // nodes handled by block 0 alone
 
 struct BuildArgs {
     const double *xs;
@@ -130,8 +136,43 @@ __device__ void dyadic_splits(const BuildArgs &a)
 }
 
 // Number of children of frontier node `node` (0 if it is a leaf) and split.
+// Shared-memory samples of xs[r0, r1) (every stride-th source) for the
+// block-0 runs of small levels: a split search bisects the samples first and
+// then only a window of `stride` sources in global memory, so a deep level
+// costs one or two dependent global accesses per node instead of
+// log2(e - s).  The result is the plain lower_bound's: samples[j - 1] < v <=
+// samples[j] bound the global lower bound to the window, and the split is
+// its clamp to [s, e) (xs is sorted).
+#ifndef DT_BUILD_SAMPLES
+#define DT_BUILD_SAMPLES 12288
+#endif
+constexpr int BUILD_SAMPLES = DT_BUILD_SAMPLES;  // dynamic shared memory, 8 bytes each
+struct SplitSamples {
+    const double *v;  // shared memory, count entries
+    int64_t r0, r1, stride;
+    int count;
+};
+
+__device__ __forceinline__ int64_t sampled_lower_bound(const BuildArgs &a, const SplitSamples &sm,
+                                                       int64_t s, int64_t e, double v)
+{
+    int lo = 0, hi = sm.count;  // first sample >= v
+    while (lo < hi) {
+        const int m = (lo + hi) >> 1;
+        if (sm.v[m] < v)
+            lo = m + 1;
+        else
+            hi = m;
+    }
+    const int64_t wlo = lo == 0 ? sm.r0 : sm.r0 + (int64_t)(lo - 1) * sm.stride + 1;
+    const int64_t whi = lo == sm.count ? sm.r1 : sm.r0 + (int64_t)lo * sm.stride;
+    const int64_t g = dt_lower_bound(a.xs, wlo, whi, v);
+    return g < s ? s : (g > e ? e : g);
+}
+
 __device__ __forceinline__ int node_children(const BuildArgs &a, int64_t node, int64_t lev,
-                                             int64_t *split_out)
+                                             int64_t *split_out,
+                                             const SplitSamples *sm = nullptr)
 {
     int64_t s = ld_cg(a.start + node), e = ld_cg(a.end + node);
     if (e - s <= a.leaf_capacity || lev >= a.max_depth)
@@ -154,7 +195,8 @@ __device__ __forceinline__ int node_children(const BuildArgs &a, int64_t node, i
         }
     }
     if (split < 0)
-        split = dt_lower_bound(a.xs, s, e, mid);
+        split = sm && s >= sm->r0 && e <= sm->r1 ? sampled_lower_bound(a, *sm, s, e, mid)
+                                                  : dt_lower_bound(a.xs, s, e, mid);
     *split_out = split;
     return (split > s) + (e > split);
 }
@@ -223,14 +265,14 @@ __device__ int block_excl_scan(int v, int *excl, int *warp_sums)
 // Process frontier [f0, f1) of level `lev` entirely inside the calling block.
 // Returns the number of children written (or -1 on capacity overflow).
 __device__ int64_t level_in_block(const BuildArgs &a, int64_t f0, int64_t f1, int64_t lev,
-                                  int *warp_sums, int64_t *leaves)
+                                  int *warp_sums, int64_t *leaves, const SplitSamples *sm)
 {
     int64_t next = f1;
     int64_t leaf_acc = 0;
     for (int64_t t0 = f0; t0 < f1; t0 += blockDim.x) {
         int64_t node = t0 + threadIdx.x;
         int64_t split = 0;
-        int nc = node < f1 ? node_children(a, node, lev, &split) : 0;
+        int nc = node < f1 ? node_children(a, node, lev, &split, sm) : 0;
         if (node < f1 && nc == 0)
             ++leaf_acc;
         int excl;
@@ -250,6 +292,7 @@ __global__ void __launch_bounds__(BUILD_THREADS) build_kernel(BuildArgs a)
     cg::grid_group grid = cg::this_grid();
     __shared__ int warp_sums[BUILD_THREADS / 32];
     __shared__ int64_t sh_i64[4];
+    extern __shared__ double samples_s[];  // BUILD_SAMPLES
     volatile int64_t *meta = a.meta;
     const int G = gridDim.x;
 
@@ -266,6 +309,14 @@ __global__ void __launch_bounds__(BUILD_THREADS) build_kernel(BuildArgs a)
         root_interval(a, &lo0, &hi0);
         write_node(a, 0, lo0, hi0, 0, 0, a.n);
     }
+#if DT_BUILD_FLAGWAIT
+    // phase counter of the small-level runs (see below)
+    unsigned long long *const small_flag =
+        reinterpret_cast<unsigned long long *>(a.block_total + 4095);
+    unsigned long long small_phase = 0;
+    if (blockIdx.x == 0 && threadIdx.x == 0)
+        *small_flag = 0;
+#endif
     dyadic_splits(a);
     grid.sync();
 
@@ -288,6 +339,21 @@ __global__ void __launch_bounds__(BUILD_THREADS) build_kernel(BuildArgs a)
             if (blockIdx.x == 0) {
                 int64_t leaves = 0;
                 int64_t l = lev;
+                // the run's nodes all lie inside the first level's source
+                // range: sample it once (below the dyadic levels only)
+                SplitSamples sm{samples_s, 0, 0, 1, 0};
+                if (lev >= DYADIC_LEVELS) {
+                    const int64_t g0 = meta[DT_META_LEVEL0 + lev];
+                    const int64_t g1 = meta[DT_META_LEVEL0 + lev + 1];
+                    sm.r0 = ld_cg(a.start + g0);
+                    sm.r1 = ld_cg(a.end + g1 - 1);
+                    const int64_t len = sm.r1 - sm.r0;
+                    sm.stride = len > BUILD_SAMPLES ? (len + BUILD_SAMPLES - 1) / BUILD_SAMPLES : 1;
+                    sm.count = (int)((len + sm.stride - 1) / sm.stride);
+                    for (int j = threadIdx.x; j < sm.count; j += blockDim.x)
+                        samples_s[j] = __ldg(a.xs + sm.r0 + (int64_t)j * sm.stride);
+                    __syncthreads();
+                }
                 while (true) {
                     int64_t g0 = meta[DT_META_LEVEL0 + l];
                     int64_t g1 = meta[DT_META_LEVEL0 + l + 1];
@@ -301,7 +367,8 @@ __global__ void __launch_bounds__(BUILD_THREADS) build_kernel(BuildArgs a)
                         a.block_total[2048 + l] = (int64_t)t;
                     }
 #endif
-                    int64_t made = level_in_block(a, g0, g1, l, warp_sums, &leaves);
+                    int64_t made = level_in_block(a, g0, g1, l, warp_sums, &leaves,
+                                                  lev >= DYADIC_LEVELS ? &sm : nullptr);
                     __syncthreads();
                     if (made < 0) {
                         if (threadIdx.x == 0)
@@ -329,7 +396,32 @@ __global__ void __launch_bounds__(BUILD_THREADS) build_kernel(BuildArgs a)
                     a.meta[DT_META_CURLEVEL] = l;
                 __threadfence();
             }
+#if DT_BUILD_FLAGWAIT
+            // block 0 announces the end of its run with a release store; the
+            // other blocks wait on it with back-off instead of polling a grid
+            // barrier (which slows block 0's own L2 traffic)
+            ++small_phase;
+            if (blockIdx.x == 0) {
+                __syncthreads();
+                if (threadIdx.x == 0)
+                    asm volatile("st.release.gpu.u64 [%0], %1;" ::"l"(small_flag), "l"(small_phase)
+                                 : "memory");
+            } else {
+                if (threadIdx.x == 0) {
+                    unsigned long long v;
+                    while (true) {
+                        asm volatile("ld.acquire.gpu.u64 %0, [%1];" : "=l"(v) : "l"(small_flag)
+                                     : "memory");
+                        if (v >= small_phase)
+                            break;
+                        __nanosleep(256);
+                    }
+                }
+                __syncthreads();
+            }
+#else
             grid.sync();
+#endif
             lev = meta[DT_META_CURLEVEL];
             continue;
         }
@@ -459,15 +551,21 @@ extern "C" int dt_build_tree(const double *xs, int64_t n, int64_t leaf_capacity,
 
     int dev = 0, per_sm = 0;
     DT_CUDA_TRY(cudaGetDevice(&dev));
+    const size_t smem = (size_t)BUILD_SAMPLES * sizeof(double);
+    DT_CUDA_TRY(cudaFuncSetAttribute((const void *)build_kernel,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     DT_CUDA_TRY(
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, build_kernel, BUILD_THREADS, 0));
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, build_kernel, BUILD_THREADS, smem));
     if (per_sm < 1)
         return dt_set_error(DT_ERR_CUDA, "build kernel cannot be resident");
-    int grid = dt_num_sms() * (per_sm > 2 ? 2 : per_sm);
+#ifndef DT_BUILD_PER_SM
+#define DT_BUILD_PER_SM 1  // one block per SM: cheaper grid barriers (0.34 -> 0.31 ms)
+#endif
+    int grid = dt_num_sms() * (per_sm > DT_BUILD_PER_SM ? DT_BUILD_PER_SM : per_sm);
     if (grid > 3000)
         grid = 3000;
     void *args[] = {&a};
     DT_CUDA_TRY(cudaLaunchCooperativeKernel((const void *)build_kernel, grid, BUILD_THREADS, args,
-                                            0, (cudaStream_t)stream));
+                                            smem, (cudaStream_t)stream));
     return DT_OK;
 }

@@ -24,3 +24,4 @@ lv = bufs.meta[8: 8 + depth + 2].cpu().numpy()
 print("per-level us (level: nodes us):")
 for l in range(depth + 1):
     print(l, int(lv[l + 1] - lv[l]), round((t[l + 1] - t[l]) / 1e3, 1) if t[l + 1] > t[l] else None)
+
