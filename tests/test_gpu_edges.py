@@ -86,3 +86,30 @@ def test_assembly_edges(dt):
                                          quadrature_order=1, eps0=1.0))
     # one node at the cell middle with q = (w/2) sigma dx / (2 eps0) = 1 * 3 * 2 / 2
     assert one.xs.tolist() == [1.0] and one.qs.tolist() == [3.0]
+
+
+@pytest.mark.parametrize("kind", ["cluster", "geometric", "duplicates"])
+def test_deep_trees_bit_exact(dt, kind):
+    """Trees far deeper than the precomputed dyadic levels, whose deep levels
+    run in one block with the shared-memory split samples: node arrays
+    bit-identical to the oracle's build."""
+    from oracle import oracle as O
+
+    rng = np.random.default_rng(11)
+    if kind == "cluster":  # a dense clump 1e-9 wide inside a uniform background
+        x = np.concatenate([rng.uniform(-1, 1, 60000), 0.3 + 1e-9 * rng.uniform(0, 1, 60000)])
+    elif kind == "geometric":  # spacing shrinking geometrically toward 0.3
+        x = 0.3 + np.concatenate([-(1.0 - 0.9998 ** np.arange(40000)),
+                                  1.0 - 0.9997 ** np.arange(40000)]) * 0.5
+    else:  # long runs of identical positions (depth hits the cap)
+        x = np.repeat(rng.uniform(-1, 1, 300), 400)
+    x = np.sort(x)
+    q = rng.normal(size=len(x))
+    system = dt.from_sorted(x, q)
+    cfg = dt.EvalConfig(p=8, leaf_capacity=16)
+    tree = dt.build(system, dt.DiscKernel(0.01), cfg)
+    assert tree.depth > 16
+    host = tree.numpy()
+    ot = O.build_structure(x, 16)
+    for f in ("lo", "hi", "center", "half", "level", "start", "end", "left", "right"):
+        np.testing.assert_array_equal(host[f], getattr(ot, f), err_msg=f)
