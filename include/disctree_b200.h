@@ -240,11 +240,13 @@ int dt_pack_tree(const double *centers, const double *halves, const int64_t *sta
                  const int64_t *ends, const int64_t *lefts, const int64_t *rights,
                  int64_t n_nodes, void *packed, void *stream);
 
-/* Task-counter slot of the traversal (the workspace of the *_packed and
- * *_device evaluators must hold at least this many bytes; zeroed by the
- * call, stream-ordered).  Warps take 32-target tasks from per-SM segments
- * of the target range, so neighbouring targets run on the same SM. */
-#define DT_EVAL_COUNTER_BYTES 1024
+/* Traversal workspace slot (the workspace of the *_packed and *_device
+ * evaluators must hold at least this many bytes and be 16-byte aligned):
+ * the task counters (zeroed by the call, stream-ordered; warps take
+ * 32-target tasks from per-SM segments of the target range, so
+ * neighbouring targets run on the same SM), then the adaptive-order tables
+ * each call builds for its tree (breakpoints of the bound scan per level). */
+#define DT_EVAL_COUNTER_BYTES 65536
 
 /* Workspace of dt_tree_phi_sum (packed copies + the counter slot). */
 size_t dt_tree_eval_workspace(int64_t n_nodes, int64_t n_src, int64_t moment_stride);

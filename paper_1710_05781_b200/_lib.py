@@ -26,7 +26,7 @@ DT_META_LEAVES = 2
 DT_META_OVERFLOW = 3
 DT_META_LEVEL0 = 8
 DT_META_WORDS = 72
-DT_EVAL_COUNTER_BYTES = 1024
+DT_EVAL_COUNTER_BYTES = 65536
 DT_MAX_WORLD = 64
 DT_PLAN_CUT = 0
 DT_PLAN_LEVEL_BEGIN = 1

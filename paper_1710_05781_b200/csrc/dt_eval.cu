@@ -97,6 +97,9 @@ struct EvalArgs {
     const int64_t *sign_bracket;
     const int64_t *meta;  // if set: tol_share = tolerance / (3 max(depth, 1)) on device
     double tolerance;
+    // order-selection tables in the workspace slot (built per call), or null
+    const double *pt_bp;
+    const unsigned char *pt_bins;
 };
 
 // tree.py:268-270 _tol_share, evaluated from the device-side tree depth.
@@ -343,6 +346,200 @@ __device__ int psel_fast(double big_r, double h, const EvalArgs &a, const float 
     return min(p, a.p_cap);
 }
 
+// ------------------------------------------------------------ order table
+//
+// For n >= PT_MIN_N the bound value V_n(R) = 1.1 M(R) R (h/R)^(n+1) / (R - h)
+// of a node of half-width h decreases strictly in R: on the reference's
+// 64-point contour d ln M / d ln R <= 5.6 (dense scan of s* = r_d^2/R^2),
+// while the rest falls at least as fast as R^-(n+1), so the slope of ln V_n
+// in ln R is <= -1.4.  "V_n <= tol" is then "R >= b_n", one breakpoint per
+// (level, n): the nodes of level L have the half-width h_L = h0 2^-L up to
+// a relative PT_DH (interval rounding).  In x = log2(R/h) the breakpoints
+// x_n = log2(b_n / h_L) cut a per-level table of bins of width 1/PT_BPU into
+//   clean bins (no x_n within PT_ETA): the order is the bin's constant p;
+//   one-breakpoint bins: p = m or m + 1 by comparing R with b_m in double;
+//   the rest (two breakpoints, or p <= PT_MIN_N possible): psel_fast.
+// PT_ETA covers the float evaluation of x (~3e-7) and the level's spread of
+// h (which moves a breakpoint in x by < 1e-5); the double comparison keeps
+// a relative margin PT_EPS >= (31 + 2) PT_DH / 1.4 (the spread's effect in
+// R) plus the bisection tolerance, else psel_fast decides.
+constexpr int PT_LEVELS = 61;  // levels 0..max_depth
+constexpr int PT_N = 32;       // n = 0..31 (p_cap <= 31)
+constexpr int PT_MIN_N = 6;
+constexpr int PT_BPU = 128;    // bins per unit of log2(R/h)
+constexpr int PT_BINS = 512;   // per level: x in [x0, x0 + 4)
+constexpr double PT_DH = 1e-6;
+constexpr double PT_EPS = 3e-5;
+constexpr double PT_ETA = 5e-5;
+constexpr unsigned char PT_FALLBACK = 0xff, PT_SPLIT = 0x80;
+
+// log V_n(R) in double, the contour maximum over the reference's 64
+// samples (one warp: lane l holds samples l and l + 32, then a max
+// reduction); lh = log h
+struct LaneSamples {
+    double c0, s0, c1, s1;
+};
+
+__device__ double log_bound_value(double R, double h, double lh, int n, double rd2,
+                                  const LaneSamples &q)
+{
+    double m2;  // max |f|^2
+    {
+        const double wr = R * (q.c0 - 1.0), wi = R * q.s0;
+        const double zr = wr * wr - wi * wi + rd2, zi = 2.0 * wr * wi;
+        m2 = (wr * wr + wi * wi) / sqrt(zr * zr + zi * zi);
+    }
+    {
+        const double wr = R * (q.c1 - 1.0), wi = R * q.s1;
+        const double zr = wr * wr - wi * wi + rd2, zi = 2.0 * wr * wi;
+        m2 = fmax(m2, (wr * wr + wi * wi) / sqrt(zr * zr + zi * zi));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+        m2 = fmax(m2, __shfl_xor_sync(DT_FULL, m2, o));
+    const double lr = log(R);
+    return log(1.1) + 0.5 * log(m2) + lr + (double)(n + 1) * (lh - lr) - log(R - h);
+}
+
+// x0: bins start just below log2(1/theta), the smallest R/h of a far pair
+__host__ __device__ inline double pt_x0(double theta)
+{
+    return floor(PT_BPU * log2(1.0 / theta)) / PT_BPU - 1.0 / PT_BPU;
+}
+
+// bp[L][n] = b_n for h_L: the R with V_n(R) = tol_share (h_L / theta if V_n
+// <= tol there already, +inf if never); 0 for n >= p_cap (the reference's
+// loop stops there).  One warp per entry.
+__global__ void psel_breakpoints_kernel(EvalArgs a, double *bp)
+{
+    const int id = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (id >= PT_LEVELS * PT_N)
+        return;
+    const int L = id / PT_N, n = id % PT_N;
+    const double tol = a.meta ? tol_share_of(a) : a.tol_share;
+    const double h = ldexp(__ldg(&a.nodes[0].half), -L);
+    // levels below the tree's depth (when known) hold no nodes
+    const bool used = !a.meta || L <= __ldg(a.meta + DT_META_DEPTH);
+    double b = __longlong_as_double(0x7ff0000000000000LL);  // +inf
+    if (n >= a.p_cap) {
+        b = 0.0;
+    } else if (used && n >= PT_MIN_N && h > 0.0) {
+        // F(u) = ln V_n(e^u) - ln tol falls with slope in [-38, -1.4]:
+        // F(u0) / 1.4 past u0 = ln(h/theta) brackets the root; then
+        // regula falsi with the Illinois modification
+        const double lt = log(tol), lh = log(h);
+        const int l = dt_lane();
+        const LaneSamples q{__ldg(a.cos_tab + l), __ldg(a.sin_tab + l), __ldg(a.cos_tab + l + 32),
+                            __ldg(a.sin_tab + l + 32)};
+        const double rmin = h / a.theta;
+        double ulo = log(rmin);
+        double flo = log_bound_value(rmin, h, lh, n, a.rd2, q) - lt;
+        if (!(flo > 0.0)) {
+            b = rmin;
+        } else if (flo < 1e4) {
+            double uhi = ulo + flo / 1.4;
+            double fhi = log_bound_value(exp(uhi), h, lh, n, a.rd2, q) - lt;
+            int side = 0;
+            for (int it = 0; it < 100 && uhi - ulo > 1e-10; ++it) {
+                double um = (ulo * fhi - uhi * flo) / (fhi - flo);
+                if (!(um > ulo && um < uhi))
+                    um = 0.5 * (ulo + uhi);
+                const double fm =
+                    log_bound_value(exp(um), h, lh, n, a.rd2, q) - lt;
+                if (fm > 0.0) {
+                    ulo = um;
+                    flo = fm;
+                    if (side == 1)
+                        fhi *= 0.5;
+                    side = 1;
+                } else {
+                    uhi = um;
+                    fhi = fm;
+                    if (side == -1)
+                        flo *= 0.5;
+                    side = -1;
+                }
+            }
+            b = exp(uhi) * (1.0 + 1e-12);  // on the V_n <= tol side
+        }
+    }
+    if (dt_lane() == 0) {
+        bp[id] = b;
+        // x_n = log2(b_n / h_L) for the bins (-huge for b_n = 0)
+        bp[PT_LEVELS * PT_N + PT_LEVELS + id] = b > 0.0 ? log2(b / h) : -1e300;
+        if (n == 0)
+            bp[PT_LEVELS * PT_N + L] = h;  // h_L
+    }
+}
+
+// bins[L][j]: the order of bin j, PT_SPLIT | m for a bin holding b_m only,
+// PT_FALLBACK otherwise
+__global__ void psel_bins_kernel(EvalArgs a, const double *bp, unsigned char *bins)
+{
+    const int id = blockIdx.x * blockDim.x + threadIdx.x;
+    if (id >= PT_LEVELS * PT_BINS)
+        return;
+    const int L = id / PT_BINS, j = id % PT_BINS;
+    const double hL = bp[PT_LEVELS * PT_N + L];
+    const double *xs = bp + PT_LEVELS * PT_N + PT_LEVELS + L * PT_N;
+    const double x0 = pt_x0(a.theta);
+    const double xlo = x0 + (double)j / PT_BPU - PT_ETA, xhi = x0 + (double)(j + 1) / PT_BPU + PT_ETA;
+    unsigned char e = PT_FALLBACK;
+    // x_n = log2(b_n / h_L), decreasing in n; p <= PT_MIN_N is possible once
+    // x reaches x_(PT_MIN_N)
+    const double x6 = xs[PT_MIN_N];
+    if (hL > 0.0 && xhi < x6) {
+        int inside = 0, m = -1, p = a.p_cap;
+        for (int n = PT_MIN_N + 1; n < a.p_cap; ++n) {
+            const double xn = xs[n];
+            if (xn >= xlo && xn <= xhi) {
+                ++inside;
+                m = n;
+            } else if (xn < xlo && p == a.p_cap) {
+                p = n;  // first n whose breakpoint lies below the bin
+            }
+        }
+        if (inside == 0)
+            e = (unsigned char)p;
+        else if (inside == 1)
+            e = (unsigned char)(PT_SPLIT | m);
+    }
+    bins[id] = e;
+}
+
+// the workspace slot: task counters, then the tables
+constexpr size_t PT_BP_OFFSET = 1024, PT_BINS_OFFSET = 32768;
+static_assert(PT_BP_OFFSET + sizeof(double) * (2 * PT_LEVELS * PT_N + PT_LEVELS) <= PT_BINS_OFFSET,
+              "breakpoint table overlaps the bins");
+static_assert(PT_BINS_OFFSET + PT_LEVELS * PT_BINS <= DT_EVAL_COUNTER_BYTES,
+              "order tables exceed the workspace slot");
+
+// p from the bins, or -1 (use psel_fast)
+__device__ __forceinline__ int psel_table(double R, double h, const unsigned char *bins,
+                                          const double *hl, const double *bp, float lh0, float x0)
+{
+    const float lh = __log2f(f32_of(h));
+    const int L = __float2int_rn(lh0 - lh);
+    const int j = (int)((__log2f(f32_of(R)) - lh - x0) * (float)PT_BPU);
+    if (!(L >= 0 && L < PT_LEVELS && j >= 0 && j < PT_BINS))
+        return -1;
+    const double hL = hl[L];
+    if (!(fabs(h - hL) <= PT_DH * hL))
+        return -1;
+    const unsigned e = bins[L * PT_BINS + j];
+    if (e < PT_SPLIT)
+        return (int)e;
+    if (e == PT_FALLBACK)
+        return -1;
+    const int m = (int)(e & 0x7f);
+    const double b = __ldg(bp + L * PT_N + m);
+    if (R >= b * (1.0 + PT_EPS))
+        return m;
+    if (R < b * (1.0 - PT_EPS))
+        return m + 1;
+    return -1;
+}
+
 // ------------------------------------------------------------------ far / near
 
 // sum_k Phi^(k)(c, y) m_k, k <= pu (lanes share pmax = max pu over the warp).
@@ -539,6 +736,20 @@ __global__ void __launch_bounds__(EVAL_THREADS, DT_EVAL_MINB) tree_eval_kernel(E
         fconst_s[0] = f32_of(a.rd2);
         fconst_s[1] = f32_of(log2(CONTOUR_SAFETY / a.tol_share));
     }
+    // order-selection bins and level half-widths (psel_table)
+    __shared__ __align__(16) unsigned char pbins_s[PT_LEVELS * PT_BINS];
+    __shared__ double phl_s[PT_LEVELS];
+    const bool table_ok = ADAPTIVE && a.pt_bins != nullptr;
+    if (table_ok) {
+        const uint4 *src = reinterpret_cast<const uint4 *>(a.pt_bins);
+        uint4 *dst = reinterpret_cast<uint4 *>(pbins_s);
+        for (int i = threadIdx.x; i < PT_LEVELS * PT_BINS / 16; i += blockDim.x)
+            dst[i] = src[i];
+        for (int i = threadIdx.x; i < PT_LEVELS; i += blockDim.x)
+            phl_s[i] = a.pt_bp[PT_LEVELS * PT_N + i];
+    }
+    const float plh0 = __log2f(f32_of(__ldg(&a.nodes[0].half)));
+    const float px0 = (float)pt_x0(a.theta);
     __syncthreads();
 
 #if DT_EVAL_SEGMENTS
@@ -622,7 +833,13 @@ __global__ void __launch_bounds__(EVAL_THREADS, DT_EVAL_MINB) tree_eval_kernel(E
                 int pu = -1;
                 if (far) {
                     if (ADAPTIVE) {
-                        int r = fast_ok ? psel_fast(big_r, half, a, isig_s, fconst_s[0],
+                        int r = table_ok ? psel_table(big_r, half, pbins_s, phl_s, a.pt_bp,
+                                                      plh0, px0)
+                                         : -1;
+                        UTIL_ADD(10, 1);
+                        UTIL_ADD(11, r < 0);
+                        if (r < 0)
+                            r = fast_ok ? psel_fast(big_r, half, a, isig_s, fconst_s[0],
                                                     fconst_s[1])
                                         : -1;
                         if (r < 0) {
@@ -874,7 +1091,19 @@ int launch_fused(EvalArgs &a, bool adaptive, bool stats, cudaStream_t s, int64_t
 // caller's workspace (zeroed here, stream-ordered).
 int launch_eval(EvalArgs &a, bool adaptive, bool stats, cudaStream_t s)
 {
-    DT_CUDA_TRY(cudaMemsetAsync(a.counter, 0, DT_EVAL_COUNTER_BYTES, s));
+    DT_CUDA_TRY(cudaMemsetAsync(a.counter, 0, PT_BP_OFFSET, s));
+    a.pt_bp = nullptr;
+    a.pt_bins = nullptr;
+    if (adaptive && a.n_samples == 64 && a.psel_mode == DT_PSEL_FAST && a.p_cap <= PT_N - 1 &&
+        a.theta <= 0.5) {
+        double *bp = reinterpret_cast<double *>(reinterpret_cast<char *>(a.counter) + PT_BP_OFFSET);
+        unsigned char *bins = reinterpret_cast<unsigned char *>(a.counter) + PT_BINS_OFFSET;
+        psel_breakpoints_kernel<<<(PT_LEVELS * PT_N * 32 + 255) / 256, 256, 0, s>>>(a, bp);
+        psel_bins_kernel<<<(PT_LEVELS * PT_BINS + 255) / 256, 256, 0, s>>>(a, bp, bins);
+        DT_CUDA_TRY(cudaGetLastError());
+        a.pt_bp = bp;
+        a.pt_bins = bins;
+    }
     return launch_fused(a, adaptive, stats, s, 0);
 }
 
@@ -977,6 +1206,7 @@ extern "C" int dt_tree_phi_sum_packed(const void *packed_nodes, int64_t n_nodes,
     DT_CHECK_ARG((moment_stride & 1) == 0, "moment_stride must be even (16-byte rows)");
     if (!workspace || workspace_bytes < DT_EVAL_COUNTER_BYTES)
         return dt_set_error(DT_ERR_WORKSPACE, "eval workspace too small");
+    DT_CHECK_ARG(((uintptr_t)workspace & 15) == 0, "eval workspace must be 16-byte aligned");
     EvalArgs a{};
     a.nodes = (const dt_node *)packed_nodes;
     a.n_nodes = n_nodes;
@@ -1036,6 +1266,7 @@ extern "C" int dt_tree_field_packed(const void *packed_nodes, int64_t n_nodes,
     DT_CHECK_ARG((moment_stride & 1) == 0, "moment_stride must be even (16-byte rows)");
     if (!workspace || workspace_bytes < DT_EVAL_COUNTER_BYTES)
         return dt_set_error(DT_ERR_WORKSPACE, "eval workspace too small");
+    DT_CHECK_ARG(((uintptr_t)workspace & 15) == 0, "eval workspace must be 16-byte aligned");
     for (const void *ptr : {(const void *)ys, (const void *)out}) {
         cudaPointerAttributes at;
         DT_CUDA_TRY(cudaPointerGetAttributes(&at, ptr));
@@ -1105,6 +1336,7 @@ extern "C" int dt_tree_eval_device(const void *packed_nodes, const int64_t *meta
     DT_CHECK_ARG((moment_stride & 1) == 0, "moment_stride must be even (16-byte rows)");
     if (!workspace || workspace_bytes < DT_EVAL_COUNTER_BYTES)
         return dt_set_error(DT_ERR_WORKSPACE, "eval workspace too small");
+    DT_CHECK_ARG(((uintptr_t)workspace & 15) == 0, "eval workspace must be 16-byte aligned");
     EvalArgs a{};
     a.nodes = (const dt_node *)packed_nodes;
     a.n_nodes = node_capacity;

@@ -396,3 +396,42 @@ def test_high_order_paths(dt, p, adaptive, tol):
         d = t[:, None] - xs[None, :]
         phi_d = (qs[None, :] * (xs[None, :] - t[:, None]) / np.sqrt(d * d + r_d ** 2)).sum(1)
         assert np.max(np.abs(got - phi_d)) <= 1e-11 * np.abs(qs).sum()
+
+
+@pytest.mark.parametrize("case", ["cfg2s", "rand_adaptive", "cfg1s", "graded_2e20"])
+def test_order_tables_vs_exact_replica(dt, case):
+    """The traversal's adaptive orders through the per-level breakpoint
+    tables (DT_PSEL_FAST) equal the exact replica's (DT_PSEL_EXACT, all 64
+    samples for every pair): per-target interaction hashes and order sums."""
+    from paper_1710_05781_b200 import _lib
+    from paper_1710_05781_b200 import workloads as W
+    from paper_1710_05781_b200.tree import tree_phi_sum
+
+    if case == "graded_2e20":
+        w = W.cfg2(cells=1 << 18)
+        system = dt.from_sorted(w.xs, w.qs)
+        kernel = dt.DiscKernel(w.r_d)
+        cfg = dt.EvalConfig(p=w.p, theta=w.theta, leaf_capacity=w.leaf_capacity,
+                            adaptive=True, tolerance=w.tolerance)
+        ys = torch.from_numpy(w.targets[::7].copy()).cuda()
+    else:
+        g = load_case(case)
+        system = _system(dt, g)
+        kernel = dt.DiscKernel(float(g["r_d"]))
+        cfg = dt.EvalConfig(p=int(g["p"]), theta=float(g["theta"]),
+                            leaf_capacity=int(g["leaf_capacity"]), adaptive=True,
+                            tolerance=float(g["tolerance"]) if bool(g["adaptive"]) else 1e-10)
+        ys = torch.from_numpy(np.sort(g["targets"])).cuda()
+    tree = dt.build(system, kernel, cfg)
+    res = {}
+    for mode in (_lib.DT_PSEL_FAST, _lib.DT_PSEL_EXACT):
+        names = ("hash", "near_pairs", "n_far", "sum_p", "n_p0", "n_exact")
+        bufs = {k: torch.zeros(len(ys), dtype=torch.int64, device="cuda") for k in names}
+        st = _lib.EvalStats(*[bufs[k].data_ptr() for k in names])
+        out = torch.zeros_like(ys)
+        tree_phi_sum(tree, kernel, cfg, ys, out, accumulate=False, stats=st, psel_mode=mode)
+        res[mode] = {k: v.cpu().numpy() for k, v in bufs.items()}
+    f, e = res[_lib.DT_PSEL_FAST], res[_lib.DT_PSEL_EXACT]
+    np.testing.assert_array_equal(f["hash"], e["hash"])
+    np.testing.assert_array_equal(f["sum_p"], e["sum_p"])
+    assert f["sum_p"].sum() > 0
