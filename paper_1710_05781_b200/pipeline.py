@@ -33,8 +33,11 @@ from .tree import (
     pack_sources,
 )
 
-# kernels launched per step (memset of the work counter not counted)
-LAUNCHES_PER_STEP = 3 + 2 + 1 + 2 + 1 + 1  # scan(3) sign(2) build moments(2) pack eval
+# kernels launched per step (memset of the work counter not counted):
+# scan(3) sign(2) build moments(2) pack eval, plus the two order-table
+# kernels ahead of an adaptive evaluation with moment order <= 31, theta <= 1/2
+LAUNCHES_PER_STEP = 3 + 2 + 1 + 2 + 1 + 1
+ORDER_TABLE_LAUNCHES = 2
 
 
 class TreePipeline:
@@ -70,8 +73,9 @@ class TreePipeline:
             self.shard = ShardedMoments(self.bufs, self.order, self.moments, self.meval,
                                         self.estride, config.theta, world, rank, group,
                                         cut_level)
+        tables = bool(config.adaptive) and self.order <= 31 and config.theta <= 0.5
         self.launches_per_step = LAUNCHES_PER_STEP + (
-            self.shard.LAUNCHES - 2 if self.shard else 0)
+            self.shard.LAUNCHES - 2 if self.shard else 0) + (ORDER_TABLE_LAUNCHES if tables else 0)
 
     @classmethod
     def planned(cls, xs: torch.Tensor, n_targets: int, kernel: DiscKernel,
