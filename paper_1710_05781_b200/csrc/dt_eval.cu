@@ -354,20 +354,26 @@ __device__ int psel_fast(double big_r, double h, const EvalArgs &a, const float 
 // while the rest falls at least as fast as R^-(n+1), so the slope of ln V_n
 // in ln R is <= -1.4.  "V_n <= tol" is then "R >= b_n", one breakpoint per
 // (level, n): the nodes of level L have the half-width h_L = h0 2^-L up to
-// a relative PT_DH (interval rounding).  In x = log2(R/h) the breakpoints
-// x_n = log2(b_n / h_L) cut a per-level table of bins of width 1/PT_BPU into
-//   clean bins (no x_n within PT_ETA): the order is the bin's constant p;
-//   one-breakpoint bins: p = m or m + 1 by comparing R with b_m in double;
-//   the rest (two breakpoints, or p <= PT_MIN_N possible): psel_fast.
-// PT_ETA covers the float evaluation of x (~3e-7) and the level's spread of
-// h (which moves a breakpoint in x by < 1e-5); the double comparison keeps
-// a relative margin PT_EPS >= (31 + 2) PT_DH / 1.4 (the spread's effect in
-// R) plus the bisection tolerance, else psel_fast decides.
+// a relative PT_DH (interval rounding).  The bins partition R per level by
+// the bits of R itself: bin j holds the R whose high word lies in
+// [hi(h_L) + (j + jbase) 2^13, hi(h_L) + (j + jbase + 1) 2^13) -- 128 bins
+// per binade, a monotone, integer-only function of R (no logarithms in the
+// traversal).  With x = log2(R/h_L), the breakpoints x_n = log2(b_n / h_L)
+// make each bin
+//   clean (no x_n within PT_ETA of the bin's x-range): the bin's constant p;
+//   one-breakpoint: p = m or m + 1 by comparing R with b_m in double;
+//   anything else (two breakpoints, p <= PT_MIN_N possible): psel_fast.
+// A node's level comes from the bits of its h as well,
+// L = (hi(h0) - hi(h) + 2^19) >> 20, and a level whose nodes do not all have
+// |h - h_L| <= PT_DH h_L (scanned when the tables are built) gets no table.
+// PT_ETA covers the level's spread of h (which moves a breakpoint in x by
+// < 1e-5); the double comparison keeps a relative margin PT_EPS >=
+// (31 + 2) PT_DH / 1.4 (the spread's effect in R) plus the bisection
+// tolerance, else psel_fast decides.
 constexpr int PT_LEVELS = 61;  // levels 0..max_depth
 constexpr int PT_N = 32;       // n = 0..31 (p_cap <= 31)
 constexpr int PT_MIN_N = 6;
-constexpr int PT_BPU = 128;    // bins per unit of log2(R/h)
-constexpr int PT_BINS = 512;   // per level: x in [x0, x0 + 4)
+constexpr int PT_BINS = 512;   // per level: four binades of R from just below h_L / theta
 constexpr double PT_DH = 1e-6;
 constexpr double PT_EPS = 3e-5;
 constexpr double PT_ETA = 5e-5;
@@ -401,17 +407,43 @@ __device__ double log_bound_value(double R, double h, double lh, int n, double r
     return log(1.1) + 0.5 * log(m2) + lr + (double)(n + 1) * (lh - lr) - log(R - h);
 }
 
-// x0: bins start just below log2(1/theta), the smallest R/h of a far pair
-__host__ __device__ inline double pt_x0(double theta)
+// jbase: bin 0 starts below every far R of a level.  With blog(v) = e + m - 1
+// for v = 2^e m (1 <= m < 2), log2(v) - 0.0861 <= blog(v) <= log2(v), so
+// (hi(R) - hi(h_L)) / 2^20 = blog(R) - blog(h_L) >= log2(R / h_L) - 0.0861 and
+// R >= h / theta >= h_L (1 - PT_DH) / theta.
+__host__ __device__ inline int pt_jbase(double theta)
 {
-    return floor(PT_BPU * log2(1.0 / theta)) / PT_BPU - 1.0 / PT_BPU;
+    return (int)floor(128.0 * (log2(1.0 / theta) - 0.0862)) - 1;
+}
+
+// the level of a node of half-width h from the bits of h (h0: the root's)
+__device__ __forceinline__ int pt_level(int hi0, double h)
+{
+    return (hi0 - __double2hiint(h) + 0x80000) >> 20;
 }
 
 // bp[L][n] = b_n for h_L: the R with V_n(R) = tol_share (h_L / theta if V_n
 // <= tol there already, +inf if never); 0 for n >= p_cap (the reference's
-// loop stops there).  One warp per entry.
-__global__ void psel_breakpoints_kernel(EvalArgs a, double *bp)
+// loop stops there).  One warp per entry.  First, a grid-stride scan of the
+// nodes sets bad[L] for every level L = pt_level(h) holding a node with
+// |h - h_L| > PT_DH h_L (or lying below the tree's depth, where no
+// breakpoints are computed); bad[] is zeroed by the caller.
+__global__ void psel_breakpoints_kernel(EvalArgs a, double *bp, unsigned *bad)
 {
+    {
+        const double h0 = __ldg(&a.nodes[0].half);
+        const int hi0 = __double2hiint(h0);
+        const int64_t nn = a.meta ? __ldg(a.meta + DT_META_NODES) : a.n_nodes;
+        const int64_t dep = a.meta ? __ldg(a.meta + DT_META_DEPTH) : PT_LEVELS - 1;
+        for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nn;
+             i += (int64_t)gridDim.x * blockDim.x) {
+            const double h = __ldg(&a.nodes[i].half);
+            const int L = pt_level(hi0, h);
+            if ((unsigned)L < (unsigned)PT_LEVELS &&
+                (L > dep || !(fabs(h - ldexp(h0, -L)) <= PT_DH * ldexp(h0, -L))))
+                atomicOr(bad + L, 1u);
+        }
+    }
     const int id = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     if (id >= PT_LEVELS * PT_N)
         return;
@@ -474,7 +506,8 @@ __global__ void psel_breakpoints_kernel(EvalArgs a, double *bp)
 
 // bins[L][j]: the order of bin j, PT_SPLIT | m for a bin holding b_m only,
 // PT_FALLBACK otherwise
-__global__ void psel_bins_kernel(EvalArgs a, const double *bp, unsigned char *bins)
+__global__ void psel_bins_kernel(EvalArgs a, const double *bp, const unsigned *bad,
+                                 unsigned char *bins)
 {
     const int id = blockIdx.x * blockDim.x + threadIdx.x;
     if (id >= PT_LEVELS * PT_BINS)
@@ -482,13 +515,22 @@ __global__ void psel_bins_kernel(EvalArgs a, const double *bp, unsigned char *bi
     const int L = id / PT_BINS, j = id % PT_BINS;
     const double hL = bp[PT_LEVELS * PT_N + L];
     const double *xs = bp + PT_LEVELS * PT_N + PT_LEVELS + L * PT_N;
-    const double x0 = pt_x0(a.theta);
-    const double xlo = x0 + (double)j / PT_BPU - PT_ETA, xhi = x0 + (double)(j + 1) / PT_BPU + PT_ETA;
+    // the bin's R-range: high words hiL + (j + jbase) 2^13 .. + 2^13 (exact
+    // doubles); the traversal's hiL = hi(h0) - (L << 20) must be hL's high
+    // word (no subnormals) and hL must share h0's low word
+    const double h0 = __ldg(&a.nodes[0].half);
+    const int hiL = __double2hiint(h0) - (L << 20);
+    const int jb = pt_jbase(a.theta) + j;
+    const bool exact_level = hL > 0.0 && __double2hiint(hL) == hiL &&
+                             __double2loint(hL) == __double2loint(h0) && bad[L] == 0;
+    const double rlo = __hiloint2double(hiL + (jb << 13), 0);
+    const double rhi = __hiloint2double(hiL + ((jb + 1) << 13), 0);
+    const double xlo = log2(rlo / hL) - PT_ETA, xhi = log2(rhi / hL) + PT_ETA;
     unsigned char e = PT_FALLBACK;
     // x_n = log2(b_n / h_L), decreasing in n; p <= PT_MIN_N is possible once
     // x reaches x_(PT_MIN_N)
     const double x6 = xs[PT_MIN_N];
-    if (hL > 0.0 && xhi < x6) {
+    if (exact_level && xhi < x6) {
         int inside = 0, m = -1, p = a.p_cap;
         for (int n = PT_MIN_N + 1; n < a.p_cap; ++n) {
             const double xn = xs[n];
@@ -507,24 +549,25 @@ __global__ void psel_bins_kernel(EvalArgs a, const double *bp, unsigned char *bi
     bins[id] = e;
 }
 
-// the workspace slot: task counters, then the tables
-constexpr size_t PT_BP_OFFSET = 1024, PT_BINS_OFFSET = 32768;
+// the workspace slot: task counters and the bad-level flags (zeroed per
+// call), then the tables
+constexpr size_t PT_BAD_OFFSET = 768, PT_BP_OFFSET = 1024, PT_BINS_OFFSET = 32768;
+static_assert(DT_EVAL_SEGMENTS * 4 <= PT_BAD_OFFSET && PT_BAD_OFFSET + 4 * PT_LEVELS <= PT_BP_OFFSET,
+              "counter slot layout");
 static_assert(PT_BP_OFFSET + sizeof(double) * (2 * PT_LEVELS * PT_N + PT_LEVELS) <= PT_BINS_OFFSET,
               "breakpoint table overlaps the bins");
 static_assert(PT_BINS_OFFSET + PT_LEVELS * PT_BINS <= DT_EVAL_COUNTER_BYTES,
               "order tables exceed the workspace slot");
 
-// p from the bins, or -1 (use psel_fast)
+// p from the bins, or -1 (use psel_fast): integer arithmetic on the high
+// words of R and h (hi0 = hi(h0), jbase = pt_jbase(theta)), one shared-memory
+// byte, at most one double comparison
 __device__ __forceinline__ int psel_table(double R, double h, const unsigned char *bins,
-                                          const double *hl, const double *bp, float lh0, float x0)
+                                          const double *bp, int hi0, int jbase)
 {
-    const float lh = __log2f(f32_of(h));
-    const int L = __float2int_rn(lh0 - lh);
-    const int j = (int)((__log2f(f32_of(R)) - lh - x0) * (float)PT_BPU);
-    if (!(L >= 0 && L < PT_LEVELS && j >= 0 && j < PT_BINS))
-        return -1;
-    const double hL = hl[L];
-    if (!(fabs(h - hL) <= PT_DH * hL))
+    const int L = pt_level(hi0, h);
+    const int j = ((__double2hiint(R) - (hi0 - (L << 20))) >> 13) - jbase;
+    if (!((unsigned)L < (unsigned)PT_LEVELS && (unsigned)j < (unsigned)PT_BINS))
         return -1;
     const unsigned e = bins[L * PT_BINS + j];
     if (e < PT_SPLIT)
@@ -738,18 +781,15 @@ __global__ void __launch_bounds__(EVAL_THREADS, DT_EVAL_MINB) tree_eval_kernel(E
     }
     // order-selection bins and level half-widths (psel_table)
     __shared__ __align__(16) unsigned char pbins_s[PT_LEVELS * PT_BINS];
-    __shared__ double phl_s[PT_LEVELS];
     const bool table_ok = ADAPTIVE && a.pt_bins != nullptr;
     if (table_ok) {
         const uint4 *src = reinterpret_cast<const uint4 *>(a.pt_bins);
         uint4 *dst = reinterpret_cast<uint4 *>(pbins_s);
         for (int i = threadIdx.x; i < PT_LEVELS * PT_BINS / 16; i += blockDim.x)
             dst[i] = src[i];
-        for (int i = threadIdx.x; i < PT_LEVELS; i += blockDim.x)
-            phl_s[i] = a.pt_bp[PT_LEVELS * PT_N + i];
     }
-    const float plh0 = __log2f(f32_of(__ldg(&a.nodes[0].half)));
-    const float px0 = (float)pt_x0(a.theta);
+    const int phi0 = __double2hiint(__ldg(&a.nodes[0].half));
+    const int pjb = pt_jbase(a.theta);
     __syncthreads();
 
 #if DT_EVAL_SEGMENTS
@@ -833,8 +873,7 @@ __global__ void __launch_bounds__(EVAL_THREADS, DT_EVAL_MINB) tree_eval_kernel(E
                 int pu = -1;
                 if (far) {
                     if (ADAPTIVE) {
-                        int r = table_ok ? psel_table(big_r, half, pbins_s, phl_s, a.pt_bp,
-                                                      plh0, px0)
+                        int r = table_ok ? psel_table(big_r, half, pbins_s, a.pt_bp, phi0, pjb)
                                          : -1;
                         UTIL_ADD(10, 1);
                         UTIL_ADD(11, r < 0);
@@ -1098,8 +1137,9 @@ int launch_eval(EvalArgs &a, bool adaptive, bool stats, cudaStream_t s)
         a.theta <= 0.5) {
         double *bp = reinterpret_cast<double *>(reinterpret_cast<char *>(a.counter) + PT_BP_OFFSET);
         unsigned char *bins = reinterpret_cast<unsigned char *>(a.counter) + PT_BINS_OFFSET;
-        psel_breakpoints_kernel<<<(PT_LEVELS * PT_N * 32 + 255) / 256, 256, 0, s>>>(a, bp);
-        psel_bins_kernel<<<(PT_LEVELS * PT_BINS + 255) / 256, 256, 0, s>>>(a, bp, bins);
+        unsigned *bad = reinterpret_cast<unsigned *>(reinterpret_cast<char *>(a.counter) + PT_BAD_OFFSET);
+        psel_breakpoints_kernel<<<(PT_LEVELS * PT_N * 32 + 255) / 256, 256, 0, s>>>(a, bp, bad);
+        psel_bins_kernel<<<(PT_LEVELS * PT_BINS + 255) / 256, 256, 0, s>>>(a, bp, bad, bins);
         DT_CUDA_TRY(cudaGetLastError());
         a.pt_bp = bp;
         a.pt_bins = bins;
