@@ -562,11 +562,11 @@ static_assert(PT_BINS_OFFSET + PT_LEVELS * PT_BINS <= DT_EVAL_COUNTER_BYTES,
 // p from the bins, or -1 (use psel_fast): integer arithmetic on the high
 // words of R and h (hi0 = hi(h0), jbase = pt_jbase(theta)), one shared-memory
 // byte, at most one double comparison
-__device__ __forceinline__ int psel_table(double R, double h, const unsigned char *bins,
+__device__ __forceinline__ int psel_table(double R, int hiR, double h, const unsigned char *bins,
                                           const double *bp, int hi0, int jbase)
 {
     const int L = pt_level(hi0, h);
-    const int j = ((__double2hiint(R) - (hi0 - (L << 20))) >> 13) - jbase;
+    const int j = ((hiR - (hi0 - (L << 20))) >> 13) - jbase;
     if (!((unsigned)L < (unsigned)PT_LEVELS && (unsigned)j < (unsigned)PT_BINS))
         return -1;
     const unsigned e = bins[L * PT_BINS + j];
@@ -873,7 +873,8 @@ __global__ void __launch_bounds__(EVAL_THREADS, DT_EVAL_MINB) tree_eval_kernel(E
                 int pu = -1;
                 if (far) {
                     if (ADAPTIVE) {
-                        int r = table_ok ? psel_table(big_r, half, pbins_s, a.pt_bp, phi0, pjb)
+                        int r = table_ok ? psel_table(big_r, __double2hiint(d) & 0x7fffffff, half, pbins_s,
+                                                      a.pt_bp, phi0, pjb)
                                          : -1;
                         UTIL_ADD(10, 1);
                         UTIL_ADD(11, r < 0);
@@ -904,7 +905,8 @@ __global__ void __launch_bounds__(EVAL_THREADS, DT_EVAL_MINB) tree_eval_kernel(E
                 if (far) {
                     acc += far_field<WIDE>(
                         d, a.rd2,
-                        reinterpret_cast<const double2 *>(a.moments + (int64_t)node * a.stride),
+                        reinterpret_cast<const double2 *>(a.moments) +
+                            (unsigned)node * (unsigned)(a.stride >> 1),
                         pu, pmin, pmax);
                     if (STATS) {
                         hh += mix64((uint64_t)node * 256u + (uint64_t)pu);
@@ -1212,6 +1214,8 @@ static int check_eval_args(int64_t n_nodes, int64_t n_src, int64_t p, int adapti
     DT_CHECK_ARG(n_src >= 0 && n_src < (int64_t)1 << 31, "bad source count");
     DT_CHECK_ARG(i0 >= 0 && i1 >= i0, "bad target range");
     DT_CHECK_ARG(p >= 0 && p < stride, "p must be >= 0 and < moment_stride");
+    // the traversal indexes moment rows in 32 bits (16-byte units)
+    DT_CHECK_ARG(n_nodes * ((stride + 1) / 2) < ((int64_t)1 << 32), "moment array too large");
     DT_CHECK_ARG(rd2 > 0.0, "rd2 must be > 0");
     DT_CHECK_ARG(theta > 0.0 && theta < 1.0, "theta must lie in (0, 1)");
     if (adaptive) {
