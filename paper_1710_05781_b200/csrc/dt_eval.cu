@@ -504,6 +504,45 @@ __global__ void psel_breakpoints_kernel(EvalArgs a, double *bp, unsigned *bad)
     }
 }
 
+// A bin's order without any monotonicity in R (used where p <= PT_MIN_N is
+// possible): the reference's p is the smallest n < p_cap with V_n(R) <= tol
+// (else p_cap), and V_n(R) = V_0(R) (h/R)^n falls with n, so p is constant
+// on [rlo, rhi] if V_p <= tol and V_(p-1) > tol hold on the whole bin.  Bounds
+// of ln V_n = ln 1.1 + ln M(R) + (n+1) ln h - n ln R - ln(R - h) over the bin
+// (h within PT_DH of h_L): ln M at the bin's centre +- PT_LIPM times the
+// half-width in ln R (|d ln M / d ln R| <= 5.61 on the 64-point contour over
+// 14 decades of R / r_d), the other terms at the bin's ends.  A margin of 1e-9
+// covers round-off in the reference's value.  PT_FALLBACK if undecided.
+constexpr double PT_LIPM = 7.0;
+__device__ unsigned char psel_bin_interval(const EvalArgs &a, double rlo, double rhi, double hL)
+{
+    const double hmin = hL * (1.0 - PT_DH), hmax = hL * (1.0 + PT_DH);
+    if (!(rlo > 2.0 * hmax))
+        return PT_FALLBACK;
+    const double rc = sqrt(rlo * rhi);
+    double m2 = 0.0;
+    for (int t = 0; t < 64; ++t) {
+        const double wr = rc * (__ldg(a.cos_tab + t) - 1.0), wi = rc * __ldg(a.sin_tab + t);
+        const double zr = wr * wr - wi * wi + a.rd2, zi = 2.0 * wr * wi;
+        m2 = fmax(m2, (wr * wr + wi * wi) / sqrt(zr * zr + zi * zi));
+    }
+    const double lrlo = log(rlo), lrhi = log(rhi);
+    const double slack = PT_LIPM * 0.5 * (lrhi - lrlo) + 1e-12;
+    const double lm = 0.5 * log(m2);
+    const double lt = log(a.meta ? tol_share_of(a) : a.tol_share), c = log(1.1), mg = 1e-9;
+    // upper / lower bounds of ln V_n - ln tol, n = 0, 1, ...
+    const double up0 = c + lm + slack + log(hmax) - log(rlo - hmax) - lt;
+    const double lo0 = c + lm - slack + log(hmin) - log(rhi - hmin) - lt;
+    const double dup = log(hmax) - lrlo, dlo = log(hmin) - lrhi;  // d/dn, both < 0
+    for (int n = 0; n < a.p_cap; ++n) {
+        if (up0 + n * dup < -mg)  // V_n <= tol on the whole bin
+            return (n == 0 || lo0 + (n - 1) * dlo > mg) ? (unsigned char)n : PT_FALLBACK;
+        if (!(lo0 + n * dlo > mg))  // V_n may fall to tol inside the bin
+            return PT_FALLBACK;
+    }
+    return (unsigned char)a.p_cap;  // V_n > tol for every n < p_cap
+}
+
 // bins[L][j]: the order of bin j, PT_SPLIT | m for a bin holding b_m only,
 // PT_FALLBACK otherwise
 __global__ void psel_bins_kernel(EvalArgs a, const double *bp, const unsigned *bad,
@@ -546,6 +585,8 @@ __global__ void psel_bins_kernel(EvalArgs a, const double *bp, const unsigned *b
         else if (inside == 1)
             e = (unsigned char)(PT_SPLIT | m);
     }
+    if (e == PT_FALLBACK && exact_level && a.n_samples == 64)
+        e = psel_bin_interval(a, rlo, rhi, hL);
     bins[id] = e;
 }
 

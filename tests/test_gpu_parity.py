@@ -435,3 +435,35 @@ def test_order_tables_vs_exact_replica(dt, case):
     np.testing.assert_array_equal(f["hash"], e["hash"])
     np.testing.assert_array_equal(f["sum_p"], e["sum_p"])
     assert f["sum_p"].sum() > 0
+
+
+@pytest.mark.parametrize("r_d", [1e-4, 5e-3, 1e-1])
+@pytest.mark.parametrize("tol", [1e-4, 1e-8, 1e-12])
+def test_order_tables_geometry_sweep(dt, r_d, tol):
+    """Adaptive orders through the tables (breakpoint bins, and the interval
+    bins of the low-order regime R << r_d on deep levels) equal the exact
+    replica's over a sweep of r_d and tolerance on a graded mesh (depth ~24):
+    per-target interaction hashes, order sums and counts of order-0 pairs."""
+    from paper_1710_05781_b200 import _lib
+    from paper_1710_05781_b200 import workloads as W
+    from paper_1710_05781_b200.tree import tree_phi_sum
+
+    w = W.cfg2(cells=1 << 16)
+    system = dt.from_sorted(w.xs, w.qs)
+    kernel = dt.DiscKernel(r_d)
+    cfg = dt.EvalConfig(p=8, leaf_capacity=w.leaf_capacity, adaptive=True, tolerance=tol)
+    ys = torch.from_numpy(w.targets[::5].copy()).cuda()
+    tree = dt.build(system, kernel, cfg)
+    res = {}
+    for mode in (_lib.DT_PSEL_FAST, _lib.DT_PSEL_EXACT):
+        names = ("hash", "near_pairs", "n_far", "sum_p", "n_p0", "n_exact")
+        bufs = {k: torch.zeros(len(ys), dtype=torch.int64, device="cuda") for k in names}
+        st = _lib.EvalStats(*[bufs[k].data_ptr() for k in names])
+        out = torch.zeros_like(ys)
+        tree_phi_sum(tree, kernel, cfg, ys, out, accumulate=False, stats=st, psel_mode=mode)
+        res[mode] = {k: v.cpu().numpy() for k, v in bufs.items()}
+    f, e = res[_lib.DT_PSEL_FAST], res[_lib.DT_PSEL_EXACT]
+    np.testing.assert_array_equal(f["hash"], e["hash"])
+    np.testing.assert_array_equal(f["sum_p"], e["sum_p"])
+    np.testing.assert_array_equal(f["n_p0"], e["n_p0"])
+    assert f["n_far"].sum() > 0
