@@ -40,5 +40,4 @@ print("far order util (sum pu+1 / 32*(pmax+1)): %.3f" % ((u[4] + u[2]) / (32 * (
 print("mean pmax %.2f, mean pmin %.2f, mean pu %.2f" % (u[3] / u[1], u[5] / u[1], u[4] / u[2]))
 print("near lane util: %.3f" % (u[7] / (32 * u[6])))
 print("far events/target %.2f near pairs/target (executed lanes) %.1f" % (u[2] / T, u[8] * 32 / T))
-print("table calls (warp) %d, fallback lanes-any %d" % (u[10], u[11]))
-print("fallback lanes: range %d, fallback bin %d, split margin %d" % (u[12], u[13], u[14]))
+print("table calls (lane 0) %d, table misses (lane 0) %d" % (u[10], u[11]))
