@@ -329,6 +329,16 @@ int dt_phi_sum_direct(const double *xs, const double *qs, int64_t n, const doubl
                       double rd2, double *out, int64_t i0, int64_t i1, int mode, int accumulate,
                       void *stream);
 
+/* Replaces _kernels.phi_sum_symmetric (_kernels.py:107-142), the path
+ * evaluate_direct takes when targets == sources (direct.py:80): out[i] (+)=
+ * sum_j q_j (x_j - x_i) / sqrt((x_j - x_i)^2 + rd2) for i < n, every pair
+ * evaluated once and applied to both of its targets; a fixed summation order
+ * (deterministic).  workspace: dt_phi_sum_symmetric_workspace(n) bytes
+ * (~4 n^2 / 2048 bytes: the packed column partials). */
+size_t dt_phi_sum_symmetric_workspace(int64_t n);
+int dt_phi_sum_symmetric(const double *xs, const double *qs, int64_t n, double rd2, double *out,
+                         int accumulate, void *workspace, size_t workspace_bytes, void *stream);
+
 /* ---------------------------------------------------------------- diagnostics */
 
 /* FP64 FMA throughput probe for the roofline denominator: `blocks` x 256

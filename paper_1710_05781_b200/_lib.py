@@ -124,6 +124,8 @@ SIGNATURES = {
     "dt_phi_sum_direct": (
         C.c_int, [_P, _P, _I64, _P, _D, _P, _I64, _I64, C.c_int, C.c_int, _P],
     ),
+    "dt_phi_sum_symmetric_workspace": (_SZ, [_I64]),
+    "dt_phi_sum_symmetric": (C.c_int, [_P, _P, _I64, _D, _P, C.c_int, _P, _SZ, _P]),
 }
 
 _lib = None

@@ -48,6 +48,30 @@ def phi_sum_direct(xs: torch.Tensor, qs: torch.Tensor, ys: torch.Tensor, rd2: fl
     )
 
 
+def phi_sum_symmetric(xs: torch.Tensor, qs: torch.Tensor, rd2: float, out: torch.Tensor,
+                      accumulate: bool = True) -> bool:
+    """out[i] (+)= sum_j q_j (x_j - x_i)/sqrt((x_j - x_i)^2 + rd2) for targets ==
+    sources, each pair evaluated once (_kernels.phi_sum_symmetric,
+    _kernels.py:107-142).  Returns False (nothing done) when the column
+    partials would not fit in a quarter of the free device memory."""
+    n = xs.numel()
+    if n == 0:
+        return True
+    L = _lib.load()
+    need = int(L.dt_phi_sum_symmetric_workspace(n))
+    free, _ = torch.cuda.mem_get_info(xs.device)
+    if need > free // 4:
+        return False
+    ws = torch.empty(need, dtype=torch.uint8, device=xs.device)
+    p = _lib.ptr
+    _lib.check(
+        L.dt_phi_sum_symmetric(p(xs), p(qs), n, float(rd2), p(out), int(bool(accumulate)),
+                               p(ws), need, _lib.stream_handle()),
+        "dt_phi_sum_symmetric",
+    )
+    return True
+
+
 def evaluate_direct(system, kernel, targets, threads: int | None = 1,
                     compensated: bool = False, *, precision: str = "fp64"):
     """Field at every target by direct summation (direct.py:52-88).
@@ -68,7 +92,13 @@ def evaluate_direct(system, kernel, targets, threads: int | None = 1,
     values = _sign_terms(system, t)
     mode = _lib.DT_DIRECT_KAHAN if compensated else (
         _lib.DT_DIRECT_FP32 if precision == "fp32" else _lib.DT_DIRECT_FP64)
-    phi_sum_direct(system.xs, system.qs, t, kernel.r_d * kernel.r_d, values, mode)
+    rd2 = kernel.r_d * kernel.r_d
+    # targets == sources: each pair once (direct.py:80 -> phi_sum_symmetric)
+    done = (mode == _lib.DT_DIRECT_FP64 and t.numel() == system.xs.numel()
+            and bool(torch.equal(t, system.xs))
+            and phi_sum_symmetric(system.xs, system.qs, rd2, values))
+    if not done:
+        phi_sum_direct(system.xs, system.qs, t, rd2, values, mode)
     torch.cuda.synchronize(dev)
     elapsed = time.perf_counter() - start
     return FieldResult(values=back(values), build_time=0.0, eval_time=elapsed, method="direct")
