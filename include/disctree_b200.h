@@ -215,7 +215,8 @@ int dt_shard_finish(const int64_t *plan, int world, int64_t cut_level, const dou
 /* ---------------------------------------------------------------- (d)+(e) */
 
 typedef struct dt_eval_stats {
-    uint64_t *hash;      /* sum of splitmix64(event code) over interaction events */
+    uint64_t *hash;      /* ordered hash of the interaction events: h <- splitmix64(h ^ code)
+                          * in the target's depth-first visit order (oracle.c) */
     int64_t *near_pairs; /* near-field (source, target) pairs                    */
     int64_t *n_far;      /* accepted far nodes                                   */
     int64_t *sum_p;      /* sum of truncation orders over accepted far nodes     */
@@ -256,7 +257,9 @@ size_t dt_tree_eval_workspace(int64_t n_nodes, int64_t n_src, int64_t moment_str
  * (out[i] += phi if accumulate != 0).  The MAC and the adaptive truncation
  * order are bit-identical to the compiled reference; cos_tab/sin_tab are the
  * n_samples contour tables (tree.py:342, from host numpy).  Targets may be
- * in any order; sorted targets traverse coherently (fast). */
+ * in any order; sorted targets traverse coherently (fast).  Orders are
+ * limited to 127 as in dt_moments: p, p_cap <= 127 and moment_stride <= 128
+ * (DT_ERR_ARG otherwise; the recurrence tables end there). */
 int dt_tree_phi_sum(const double *centers, const double *halves, const int64_t *starts,
                     const int64_t *ends, const int64_t *lefts, const int64_t *rights,
                     const double *moments, int64_t moment_stride, int64_t n_nodes,
@@ -334,7 +337,9 @@ int dt_phi_sum_direct(const double *xs, const double *qs, int64_t n, const doubl
  * sum_j q_j (x_j - x_i) / sqrt((x_j - x_i)^2 + rd2) for i < n, every pair
  * evaluated once and applied to both of its targets; a fixed summation order
  * (deterministic).  workspace: dt_phi_sum_symmetric_workspace(n) bytes
- * (~4 n^2 / 2048 bytes: the packed column partials). */
+ * (~4 n^2 / 2048 bytes: the packed column partials; 2 GB at n = 2^20,
+ * 8 GB at 2^21, quadratic beyond).  The Python layer caps it
+ * (direct.SYM_MAX_WORKSPACE = 8 GiB) and uses dt_phi_sum_direct above. */
 size_t dt_phi_sum_symmetric_workspace(int64_t n);
 int dt_phi_sum_symmetric(const double *xs, const double *qs, int64_t n, double rd2, double *out,
                          int accumulate, void *workspace, size_t workspace_bytes, void *stream);

@@ -343,10 +343,11 @@ void or_phi_derivatives(double d, double rd2, int64_t p, double *deriv)
     }
 }
 
-/* Interaction-set hash: sum over events of splitmix64(code), code =
- * node*256 + p_use (far) or node*256 + 255 (near).  Order-independent, so a
- * GPU path that evaluates far and near interactions in separate passes can
- * be compared event set for event set. */
+/* Interaction-list hash, ordered: h <- splitmix64(h ^ code) for every event
+ * in the target's depth-first visit order (_kernels.py:204-264: pop, accept
+ * -> far, else leaf -> near, else push right then left), code = node*256 +
+ * p_use (far) or node*256 + 255 (near).  Two lists hash equal only if they
+ * hold the same events in the same order (up to 64-bit collisions). */
 static inline uint64_t mix64(uint64_t z)
 {
     z += 0x9e3779b97f4a7c15ULL;
@@ -358,8 +359,8 @@ static inline uint64_t mix64(uint64_t z)
 /*
  * _kernels.py:163-266 (tree_phi_sum) for targets [i0, i1).  Optional
  * instrumentation (any pointer may be NULL):
- *   hash[i]      sum of mix64(code) over the target's interaction events:
- *                far node -> node*256 + p_use, near leaf -> node*256 + 255
+ *   hash[i]      ordered hash of the target's interaction events (visit
+ *                order): far node -> node*256 + p_use, near leaf -> node*256 + 255
  *   near[i]      number of near-field (source, target) pairs
  *   nfar[i]      number of accepted far nodes
  *   sump[i]      sum of p_use over accepted far nodes
@@ -401,7 +402,7 @@ void or_tree_phi_sum(const double *centers, const double *halves, const int64_t 
                     const double *mrow = moments + node * moment_stride;
                     for (int64_t k = 0; k <= p_use; ++k)
                         acc += deriv[k] * mrow[k];
-                    hh += mix64((uint64_t)node * 256u + (uint64_t)p_use);
+                    hh = mix64(hh ^ ((uint64_t)node * 256u + (uint64_t)p_use));
                     ++c_far;
                     c_sump += p_use;
                     if (p_use == 0)
@@ -411,7 +412,7 @@ void or_tree_phi_sum(const double *centers, const double *halves, const int64_t 
                         double dd = xs[j] - y;
                         acc += qs[j] * dd / sqrt(dd * dd + rd2);
                     }
-                    hh += mix64((uint64_t)node * 256u + 255u);
+                    hh = mix64(hh ^ ((uint64_t)node * 256u + 255u));
                     c_near += ends[node] - starts[node];
                 } else {
                     if (rights[node] >= 0)

@@ -774,7 +774,8 @@ __device__ double audit_bound(const EvalArgs &a, double R, double h, int p, int 
     return value * qa;
 }
 
-// interaction-set hash (see oracle.c): sum of splitmix64 over event codes
+// ordered interaction-list hash (see oracle.c): h <- splitmix64(h ^ code)
+// per event in the lane's own depth-first visit order
 __device__ __forceinline__ uint64_t mix64(uint64_t z)
 {
     z += 0x9e3779b97f4a7c15ULL;
@@ -950,7 +951,7 @@ __global__ void __launch_bounds__(EVAL_THREADS, DT_EVAL_MINB) tree_eval_kernel(E
                             (unsigned)node * (unsigned)(a.stride >> 1),
                         pu, pmin, pmax);
                     if (STATS) {
-                        hh += mix64((uint64_t)node * 256u + (uint64_t)pu);
+                        hh = mix64(hh ^ ((uint64_t)node * 256u + (uint64_t)pu));
                         ++c_far;
                         c_sump += pu;
                         c_p0 += pu == 0;
@@ -968,7 +969,7 @@ __global__ void __launch_bounds__(EVAL_THREADS, DT_EVAL_MINB) tree_eval_kernel(E
                     if ((rest >> lane) & 1u) {
                         acc += near_field(a.xq, se.x, se.y, y, a.rd2);
                         if (STATS) {
-                            hh += mix64((uint64_t)node * 256u + 255u);
+                            hh = mix64(hh ^ ((uint64_t)node * 256u + 255u));
                             c_near += se.y - se.x;
                         }
                     }
@@ -1255,13 +1256,17 @@ static int check_eval_args(int64_t n_nodes, int64_t n_src, int64_t p, int adapti
     DT_CHECK_ARG(n_src >= 0 && n_src < (int64_t)1 << 31, "bad source count");
     DT_CHECK_ARG(i0 >= 0 && i1 >= i0, "bad target range");
     DT_CHECK_ARG(p >= 0 && p < stride, "p must be >= 0 and < moment_stride");
+    // the recurrence and moment-scaling tables (dt_farcoef.cuh) cover orders
+    // 0..127, as dt_moments does
+    DT_CHECK_ARG(stride <= 128 && p <= 127, "moment_stride must be <= 128 and p <= 127");
     // the traversal indexes moment rows in 32 bits (16-byte units)
     DT_CHECK_ARG(n_nodes * ((stride + 1) / 2) < ((int64_t)1 << 32), "moment array too large");
     DT_CHECK_ARG(rd2 > 0.0, "rd2 must be > 0");
     DT_CHECK_ARG(theta > 0.0 && theta < 1.0, "theta must lie in (0, 1)");
     if (adaptive) {
         DT_CHECK_ARG(tol_share > 0.0, "tol_share must be > 0");
-        DT_CHECK_ARG(p_cap >= 0 && p_cap < stride, "p_cap must be < moment_stride");
+        DT_CHECK_ARG(p_cap >= 0 && p_cap < stride && p_cap <= 127,
+                     "p_cap must be < moment_stride and <= 127");
         DT_CHECK_ARG(n_samples >= 1, "n_samples must be >= 1");
     }
     return DT_OK;

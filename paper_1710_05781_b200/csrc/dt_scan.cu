@@ -182,7 +182,9 @@ __global__ void __launch_bounds__(SIGN_THREADS) sign_terms_kernel(
     for (int k = 0; k < SIGN_PER_THREAD; ++k) {
         const int64_t i = t0 + (int64_t)k * SIGN_THREADS + threadIdx.x;
         y[k] = i < t1 ? __ldg(ys + i) : 0.0;
-        if (i + 1 < t1 && !(y[k] <= __ldg(ys + i + 1)))
+        // across the tile boundary too: the next tile's first target bounds
+        // this tile's search range from above only if it is not below ours
+        if (i < t1 && i + 1 < t && !(y[k] <= __ldg(ys + i + 1)))
             ok = false;
     }
     const bool sorted = __syncthreads_and(ok);

@@ -48,19 +48,26 @@ def phi_sum_direct(xs: torch.Tensor, qs: torch.Tensor, ys: torch.Tensor, rd2: fl
     )
 
 
+# Upper bound on the symmetric path's partial-sum workspace (bytes); above it
+# evaluate_direct takes the plain kernel (same values to round-off).
+SYM_MAX_WORKSPACE = 8 << 30
+
+
 def phi_sum_symmetric(xs: torch.Tensor, qs: torch.Tensor, rd2: float, out: torch.Tensor,
                       accumulate: bool = True) -> bool:
     """out[i] (+)= sum_j q_j (x_j - x_i)/sqrt((x_j - x_i)^2 + rd2) for targets ==
     sources, each pair evaluated once (_kernels.phi_sum_symmetric,
-    _kernels.py:107-142).  Returns False (nothing done) when the column
-    partials would not fit in a quarter of the free device memory."""
+    _kernels.py:107-142).  Returns False (nothing done) when the partial
+    sums (~4 n^2 / 2048 bytes: 2 GB at n = 2^20, 8 GB at 2^21) would exceed
+    SYM_MAX_WORKSPACE or a quarter of the free device memory; the caller
+    then uses the plain kernel."""
     n = xs.numel()
     if n == 0:
         return True
     L = _lib.load()
     need = int(L.dt_phi_sum_symmetric_workspace(n))
     free, _ = torch.cuda.mem_get_info(xs.device)
-    if need > free // 4:
+    if need > min(free // 4, SYM_MAX_WORKSPACE):
         return False
     ws = torch.empty(need, dtype=torch.uint8, device=xs.device)
     p = _lib.ptr

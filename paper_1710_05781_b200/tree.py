@@ -408,14 +408,13 @@ def _evaluate_host_pipelined(tree: Tree, kernel: DiscKernel, config: EvalConfig,
     chunks = [(i, min(T, i + PIPELINE_CHUNK)) for i in range(0, T, PIPELINE_CHUNK)]
     L = _lib.load()
     p = _lib.ptr
-    sign_bytes = int(L.dt_sign_terms_workspace(PIPELINE_CHUNK))
+    ws_bytes = int(L.dt_tree_field_workspace(PIPELINE_CHUNK))
+    cos_t, sin_t = contour_tables(dev)
     # two compute streams in turn: chunk i+1's traversal fills the SMs that
     # chunk i's tail leaves idle (own workspaces per stream)
     main = torch.cuda.current_stream(dev)
     comps = [main, torch.cuda.Stream(dev)]
-    sign_ws = [torch.empty(sign_bytes, dtype=torch.uint8, device=dev) for _ in comps]
-    eval_ws = [torch.empty(_lib.DT_EVAL_COUNTER_BYTES, dtype=torch.uint8, device=dev)
-               for _ in comps]
+    eval_ws = [torch.empty(ws_bytes, dtype=torch.uint8, device=dev) for _ in comps]
     s_in, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
     ready = torch.cuda.Event()
     ready.record(main)
@@ -437,15 +436,19 @@ def _evaluate_host_pipelined(tree: Tree, kernel: DiscKernel, config: EvalConfig,
             arrived.record(s_in)
         comp.wait_event(arrived)
         with torch.cuda.stream(comp):
-            # finiteness and order, including the step into this chunk
-            lo = i0 - 1 if i0 else 0
-            _lib.check(L.dt_check_values(p(d_t[lo:i1]), i1 - lo, p(flags),
-                                         _lib.stream_handle()), "dt_check_values")
-            _lib.check(L.dt_sign_terms(p(system.xs), p(system.prefix), len(system),
-                                       p(d_t[i0:i1]), p(d_o[i0:i1]), i1 - i0, p(sign_ws[k]),
-                                       sign_bytes, _lib.stream_handle()), "dt_sign_terms")
-            tree_phi_sum(tree, kernel, config, d_t, d_o, i0=i0, i1=i1, accumulate=True,
-                         workspace=eval_ws[k])
+            # sign term + traversal in one kernel; non-finite targets are
+            # counted in flags[0] and not traversed (no O(N) walk per NaN)
+            _lib.check(
+                L.dt_tree_field_packed(
+                    p(tree.packed), len(tree), p(tree.meval), tree.meval.shape[1], p(tree.xq),
+                    p(system.xs), p(system.prefix), len(system), kernel.r_d * kernel.r_d,
+                    float(config.theta), int(config.p), int(bool(config.adaptive)),
+                    _tol_share(tree, config), int(tree.moment_order), p(cos_t), p(sin_t),
+                    cos_t.numel(), p(d_t), p(d_o), i0, i1, p(flags), p(eval_ws[k]), ws_bytes,
+                    _lib.stream_handle(),
+                ),
+                "dt_tree_field_packed",
+            )
             done = torch.cuda.Event()
             done.record(comp)
         s_out.wait_event(done)

@@ -68,6 +68,25 @@ def test_version_and_errors_without_gpu():
     assert lib.dt_shard_rows_bytes(4, 30, 32) == 16 * 63 * 8
 
 
+def test_order_limits_checked_before_device_work():
+    """The far-field tables cover orders 0..127: larger p, p_cap or moment
+    strides are rejected (DT_ERR_ARG) instead of reading past them."""
+    from paper_1710_05781_b200 import _lib
+
+    lib = _lib.load()
+
+    def call(p, p_cap, stride, adaptive=1):
+        return lib.dt_tree_phi_sum(1, 1, 1, 1, 1, 1, 1, stride, 3, 1, 1, 4, 1e-4, 1 / 3, p,
+                                   adaptive, 1e-10, p_cap, 1, 1, 64, 1, 1, 0, 0, 0, None, 0,
+                                   None)
+
+    assert call(128, 30, 256) == -1 and b"<= 127" in lib.dt_last_error()
+    assert call(8, 128, 256) == -1 and b"<= 127" in lib.dt_last_error()
+    assert call(8, 30, 130, adaptive=0) == -1 and b"<= 128" in lib.dt_last_error()
+    # in range: the argument checks pass and the empty target range returns OK
+    assert call(127, 127, 128) == 0
+
+
 def test_no_gpu_fails_loudly():
     torch = pytest.importorskip("torch")
     if torch.cuda.is_available():

@@ -113,3 +113,33 @@ def test_deep_trees_bit_exact(dt, kind):
     ot = O.build_structure(x, 16)
     for f in ("lo", "hi", "center", "half", "level", "start", "end", "left", "right"):
         np.testing.assert_array_equal(host[f], getattr(ot, f), err_msg=f)
+
+
+def test_sign_terms_tile_aligned_sorted_runs(dt):
+    """Targets made of sorted runs whose length is a multiple of the sign
+    kernel's 2048-target tile: each tile is sorted on its own but the next
+    tile starts lower, so its bracket must not bound this tile's search
+    (dt_sign_terms, charges.py:183-187 semantics for any target order)."""
+    from oracle import oracle as O
+
+    rng = np.random.default_rng(21)
+    x = np.sort(rng.uniform(-1, 1, 5000))
+    q = rng.normal(size=5000)
+    s = dt.from_sorted(x, q)
+    g = np.sort(rng.uniform(-1.2, 1.2, 4096))
+    t = np.concatenate([g, g, g[::-1][:2048], g])
+    from paper_1710_05781_b200.charges import _sign_terms
+
+    got = _sign_terms(s, torch.from_numpy(t).cuda()).cpu().numpy()
+    pre = O.prefix(q)
+    want = O.sign_terms(x, pre, float(pre[-1]), t)
+    assert np.max(np.abs(got - want)) <= 1e-13 * np.abs(q).sum()
+    # and through the field paths, against the oracle's tree and direct sums
+    k = dt.DiscKernel(0.01)
+    cfg = dt.EvalConfig(p=8, leaf_capacity=32)
+    tree = dt.build(s, k, cfg)
+    f = dt.evaluate_all(tree, k, cfg, s, t).values
+    fw, _ = O.evaluate_tree(x, q, 0.01, 8, cfg.theta, 32, False, 1e-9, t)
+    assert np.max(np.abs(f - fw)) <= 1e-12 * np.abs(q).sum()
+    d = dt.evaluate_direct(s, k, t).values
+    assert np.max(np.abs(d - O.evaluate_direct(x, q, 0.01, t))) <= 1e-13 * np.abs(q).sum()

@@ -1,7 +1,8 @@
 """targets == sources direct sums, each pair once (dt_phi_sum_symmetric,
 mirror of _kernels.phi_sum_symmetric, _kernels.py:107-142): against the plain
 GPU kernel and the C oracle, across band boundaries (2048 rows per band),
-determinism and accumulate mode."""
+determinism and accumulate mode.  n = 70001 and 100003 span 3 and 4 column
+chunks of 32768 (several row partials per target, the combine's chunk loop)."""
 import numpy as np
 import pytest
 import torch
@@ -20,7 +21,7 @@ def _instance(n, seed):
     return xs, qs
 
 
-@pytest.mark.parametrize("n", [1, 2, 100, 2047, 2048, 2049, 4096, 5000, 20011])
+@pytest.mark.parametrize("n", [1, 2, 100, 2047, 2048, 2049, 4096, 5000, 20011, 70001, 100003])
 def test_symmetric_matches_plain_and_oracle(n):
     from oracle import oracle as O
     from paper_1710_05781_b200.direct import phi_sum_direct, phi_sum_symmetric
