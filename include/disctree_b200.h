@@ -134,23 +134,30 @@ int dt_build_tree(const double *xs, int64_t n, int64_t leaf_capacity, int64_t ma
 
 /* ---------------------------------------------------------------- (c) */
 
-/* Node moments m_k = sum_j q_j (x_j - c)^k / k!, k = 0..order, row-major
- * [n_nodes][order + 1] (tree.py:224-238): P2M at every leaf from its sources,
- * then M2M (binomial shift) bottom-up as a dataflow without grid barriers
- * (the warp completing a node's last child forms the node).  Reads the tree
- * produced by
- * dt_build_tree (meta gives n_nodes); node_capacity bounds the node arrays.
- * moments_eval (optional) receives the traversal layout used by the *_packed
- * and *_device evaluators: M_0 = m_0, M_k = (k-1)! gamma_(k-1) m_k with
- * gamma_0 = gamma_1 = 1, gamma_n = (n+1)/n gamma_(n-2) (the scaling of the
- * three-term far-field recurrence, csrc/dt_farcoef.cuh), row stride
- * eval_stride (even, >= order + 1; padding zeroed). */
-size_t dt_moments_workspace(int64_t node_capacity);
+/* Node moments m_k = sum_j q_j (x_j - c)^k / k!, k = 0..order (tree.py:224-238):
+ * P2M at every leaf from its sources, then M2M (binomial shift) bottom-up
+ * as a dataflow without grid barriers (the warp completing a node's last
+ * child forms the node), fused into one kernel for order <= 31.  Reads the
+ * tree produced by dt_build_tree (meta gives n_nodes); node_capacity bounds
+ * the node arrays.  Two layouts:
+ *   moments_eval: the traversal layout read by the *_packed and *_device
+ *     evaluators, M_0 = m_0, M_k = (k-1)! gamma_(k-1) m_k with gamma_0 =
+ *     gamma_1 = 1, gamma_n = (n+1)/n gamma_(n-2) (the scaling of the
+ *     three-term far-field recurrence, csrc/dt_farcoef.cuh), row stride
+ *     eval_stride (even, >= order + 1; padding zeroed; 16-byte aligned).
+ *     Required for order <= 31, where the pass works on these rows only.
+ *   moments: the reference layout, row-major [n_nodes][order + 1]; optional
+ *     for order <= 31 (then derived from moments_eval at the end, as
+ *     dt_moments_from_eval does), required above. */size_t dt_moments_workspace(int64_t node_capacity);
 int dt_moments(const double *xs, const double *qs, const double *center, const int64_t *start,
                const int64_t *end, const int64_t *left, const int64_t *right,
                const int64_t *meta, int64_t order, double *moments, double *moments_eval,
                int64_t eval_stride, int64_t node_capacity, void *workspace,
                size_t workspace_bytes, void *stream);
+/* Reference-layout moments[n_nodes][order + 1] from traversal rows:
+ * m_k = M_k / ((k-1)! gamma_(k-1)) (one rounding per entry). */
+int dt_moments_from_eval(const double *moments_eval, int64_t eval_stride, int64_t n_nodes,
+                         int64_t order, double *moments, void *stream);
 
 /* ---------------------------------------------------------------- (c) sharded */
 
@@ -188,12 +195,12 @@ int dt_shard_plan(const double *center, const double *half, const int64_t *start
                   const int64_t *end, const int64_t *meta, int64_t n_src, const double *ys,
                   int64_t n_targets, int targets_sorted, double theta, int64_t cut_level,
                   int world, int rank, int64_t *plan, void *stream);
-/* Per-rank slot of the gather buffer: 2^cut_level rows of (order + 1) moments
- * followed by eval_stride traversal moments (cut_level <= 20; 0 on bad
- * arguments). */
+/* Per-rank slot of the gather buffer: 2^cut_level traversal rows of
+ * eval_stride doubles (cut_level <= 20; 0 on bad arguments). */
 size_t dt_shard_rows_bytes(int64_t cut_level, int64_t order, int64_t eval_stride);
 /* dt_moments restricted to the plan: leaves above level l, and every node at
- * levels >= l whose sources lie in [src_lo, src_hi).  order <= 31; the
+ * levels >= l whose sources lie in [src_lo, src_hi).  order <= 31; writes
+ * moments_eval only (moments is ignored: dt_shard_finish derives it); the
  * workspace is dt_moments_workspace(node_capacity) bytes. */
 int dt_moments_partial(const double *xs, const double *qs, const double *center,
                        const int64_t *start, const int64_t *end, const int64_t *left,
@@ -206,7 +213,8 @@ int dt_shard_pack(const int64_t *plan, int rank, int64_t cut_level, int64_t orde
                   const double *moments, const double *moments_eval, int64_t eval_stride,
                   double *send, void *stream);
 /* After the all-gather (recv = world slots, rank order): write every owner's
- * level-l rows, then form levels < l (M2M), in one kernel. */
+ * level-l rows, then form levels < l (M2M), in one kernel; if moments is not
+ * NULL the reference layout of every node is derived as well. */
 int dt_shard_finish(const int64_t *plan, int world, int64_t cut_level, const double *recv,
                     const double *center, const int64_t *left, const int64_t *right,
                     const int64_t *meta, int64_t order, double *moments, double *moments_eval,

@@ -235,6 +235,69 @@ void or_moments(const double *xs, const double *qs, int64_t n_nodes, const doubl
     }
 }
 
+/*
+ * The same per-source terms as or_moments (term *= t / k, tree.py:235-237),
+ * summed with cascade (pairwise) summation instead of the reference's
+ * sequential np.add.reduceat: blocks of 64 terms are summed in order and the
+ * block sums merged like a binary counter, so the summation error is
+ * ~(64 + log2 n) eps instead of ~sqrt(n) eps (random walk) for a node of n
+ * sources.  A more accurate yardstick than the reference's own sums for the
+ * GPU's moments of large nodes (the root of configs[3] has 2^27 sources).
+ */
+#define OR_CASCADE_BLOCK 64
+#define OR_CASCADE_LEVELS 48
+void or_moments_cascade(const double *xs, const double *qs, int64_t n_nodes,
+                        const double *center, const int64_t *start, const int64_t *end,
+                        int64_t order, double *moments)
+{
+    const int64_t o1 = order + 1;
+#pragma omp parallel
+    {
+        double *stack = (double *)calloc((size_t)(OR_CASCADE_LEVELS * o1), sizeof(double));
+        double *blk = (double *)malloc(sizeof(double) * (size_t)o1);
+#pragma omp for schedule(dynamic, 16)
+        for (int64_t node = 0; node < n_nodes; ++node) {
+            double *row = moments + node * o1;
+            const double c = center[node];
+            uint64_t count = 0; /* full blocks pushed so far: bit l set <=> stack[l] holds a sum */
+            for (int64_t j0 = start[node]; j0 < end[node]; j0 += OR_CASCADE_BLOCK) {
+                int64_t j1 = j0 + OR_CASCADE_BLOCK < end[node] ? j0 + OR_CASCADE_BLOCK : end[node];
+                for (int64_t k = 0; k < o1; ++k)
+                    blk[k] = 0.0;
+                for (int64_t j = j0; j < j1; ++j) {
+                    double t = xs[j] - c;
+                    double term = qs[j];
+                    blk[0] += term;
+                    for (int64_t k = 1; k < o1; ++k) {
+                        term *= t / (double)k;
+                        blk[k] += term;
+                    }
+                }
+                /* binary-counter merge: carry while the level is occupied */
+                int lev = 0;
+                while (count & ((uint64_t)1 << lev)) {
+                    double *s = stack + (size_t)lev * o1;
+                    for (int64_t k = 0; k < o1; ++k)
+                        blk[k] = s[k] + blk[k];
+                    ++lev;
+                }
+                memcpy(stack + (size_t)lev * o1, blk, sizeof(double) * (size_t)o1);
+                ++count;
+            }
+            for (int64_t k = 0; k < o1; ++k)
+                row[k] = 0.0;
+            for (int lev = 0; lev < OR_CASCADE_LEVELS; ++lev)
+                if (count & ((uint64_t)1 << lev)) {
+                    const double *s = stack + (size_t)lev * o1;
+                    for (int64_t k = 0; k < o1; ++k)
+                        row[k] += s[k];
+                }
+        }
+        free(blk);
+        free(stack);
+    }
+}
+
 /* ---------------------------------------------------------------- (d) */
 
 /* numba cmathimpl.sqrt_impl (numpy npy_csqrt, CACM algorithm 312) for the

@@ -63,6 +63,7 @@ def lib():
         L.or_build.restype = C.c_int
         L.or_tree_free.argtypes = [C.POINTER(_Tree)]
         L.or_moments.argtypes = [_D, _D, C.c_int64, _D, _I, _I, C.c_int64, _D]
+        L.or_moments_cascade.argtypes = L.or_moments.argtypes
         L.or_adaptive_value.argtypes = [C.c_double, C.c_double, C.c_double, _D, _D, C.c_int64, _D]
         L.or_adaptive_value.restype = C.c_double
         L.or_choose_p.argtypes = [
@@ -170,6 +171,18 @@ def moments(xs, qs, tree: OracleTree, order: int) -> np.ndarray:
     xs, qs = _f64(xs), _f64(qs)
     out = np.empty((len(tree), order + 1))
     lib().or_moments(
+        _d(xs), _d(qs), len(tree), _d(tree.center), _i(tree.start), _i(tree.end), int(order),
+        _d(out),
+    )
+    return out
+
+
+def moments_cascade(xs, qs, tree: OracleTree, order: int) -> np.ndarray:
+    """The reference's per-source terms (tree.py:235-237) with cascade
+    summation: a more accurate yardstick than its sequential sums."""
+    xs, qs = _f64(xs), _f64(qs)
+    out = np.empty((len(tree), order + 1))
+    lib().or_moments_cascade(
         _d(xs), _d(qs), len(tree), _d(tree.center), _i(tree.start), _i(tree.end), int(order),
         _d(out),
     )

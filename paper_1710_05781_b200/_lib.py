@@ -81,6 +81,7 @@ SIGNATURES = {
     "dt_moments": (
         C.c_int, [_P, _P, _P, _P, _P, _P, _P, _P, _I64, _P, _P, _I64, _I64, _P, _SZ, _P],
     ),
+    "dt_moments_from_eval": (C.c_int, [_P, _I64, _I64, _I64, _P, _P]),
     "dt_shard_plan": (
         C.c_int,
         [_P, _P, _P, _P, _P, _I64, _P, _I64, C.c_int, _D, _I64, C.c_int, C.c_int, _P, _P],

@@ -7,21 +7,27 @@
 // sum of its children shifted to its center,
 //     m_k(parent) = sum_{j<=k} m_j(child) * delta^(k-j) / (k-j)!,
 //     delta = c_child - c_parent,
-// computed on raw power sums S_k = k! m_k, where the shift is the binomial
-// transform S'_k = sum_j C(k,j) delta^(k-j) S_j, applied in place as 31
-// passes of Pascal's rule S_k += delta S_(k-1).
-//   order + 1 <= 32: P2M with 2 lanes per leaf (p2m_group_kernel), then a
-//     barrier-free dataflow (m2m_flow_kernel): every leaf bumps its parent's
-//     arrival counter; the lane whose arrival completes a parent keeps it,
-//     and the warp forms four kept parents at a time (8 lanes each, 4 orders
-//     per lane) before those lanes climb on.  The shard plan (multi-GPU) restricts
-//     both to one rank's subtrees; shard_finish_kernel forms the levels above
-//     the cut with the same arithmetic, thread per node.
-//   higher orders: warp per leaf + the same dataflow with a Toeplitz shift.
+// the binomial transform of the raw power sums S_k = k! m_k, applied in
+// place as 31 passes of Pascal's rule S_k += delta S_(k-1).
+//   order + 1 <= 32 (upward_kernel): one fused kernel on the traversal-layout
+//     rows M_k = c_k S_k only (the reference layout is derived on request):
+//     warps take 32 node slots at a time, deepest first, form the leaves
+//     among them (P2M with split powers, 2 lanes per leaf), and every formed
+//     leaf bumps its parent's arrival counter; the lane whose arrival
+//     completes a parent keeps it, and the warp forms kept parents (four at
+//     a time, 8 lanes and 4 orders per lane, or a lone one on 32 lanes)
+//     before those lanes climb on.  The M2M chains thus run while other
+//     warps are still in P2M.  The shard plan (multi-GPU) restricts it to
+//     one rank's subtrees; shard_finish_kernel forms the levels above the
+//     cut with the same arithmetic, thread per node.
+//   higher orders: warp per leaf + the same dataflow with a Toeplitz shift,
+//     both layouts written.
 // The shift is exact algebra; round-off differs from the reference's direct
 // sums at the 1e-16 level of sum|q| r^k / k!.
 // Algorithmic HBM bytes: P2M 16 N + 8 (order+1) leaves; M2M 24 (order+1)
 // per internal node (two child rows read, one row written).
+
+#include <algorithm>
 
 #include "dt_common.cuh"
 #include "dt_farcoef.cuh"
@@ -84,75 +90,6 @@ __constant__ double c_inv_k[MAX_ORDER1] = {  // 1/k rounded to nearest (k >= 1)
     0x1.0842108421084p-7, 0x1.0624dd2f1a9fcp-7, 0x1.0410410410410p-7, 0x1.0204081020408p-7,
 };
 
-__constant__ double c_fact_km1[MAX_ORDER1] = {  // (k-1)! rounded (k >= 1)
-    0.0, 0x1.0000000000000p+0, 0x1.0000000000000p+0, 0x1.0000000000000p+1,
-    0x1.8000000000000p+2, 0x1.8000000000000p+4, 0x1.e000000000000p+6, 0x1.6800000000000p+9,
-    0x1.3b00000000000p+12, 0x1.3b00000000000p+15, 0x1.6260000000000p+18, 0x1.baf8000000000p+21,
-    0x1.308a800000000p+25, 0x1.c8cfc00000000p+28, 0x1.7328cc0000000p+32, 0x1.44c3b28000000p+36,
-    0x1.3077775800000p+40, 0x1.3077775800000p+44, 0x1.437eeecd80000p+48, 0x1.6beecca730000p+52,
-    0x1.b02b930689000p+56, 0x1.0e1b3be415a00p+61, 0x1.6283be9b5c620p+65, 0x1.e77526159f06cp+69,
-    0x1.5e5c335f8a4cep+74, 0x1.06c52687a7b9ap+79, 0x1.9a940c33f6121p+83, 0x1.4d9849ea37eebp+88,
-    0x1.19787e5d9f316p+93, 0x1.ec92dd23d6967p+97, 0x1.be6518687a785p+102, 0x1.a27ec6e1f2d0dp+107,
-    0x1.956ad0aae33a4p+112, 0x1.956ad0aae33a4p+117, 0x1.a21627303a541p+122, 0x1.bc3789a33df96p+127,
-    0x1.e5dcbe8a8bc8cp+132, 0x1.114c2b2deea0fp+138, 0x1.3c0011ed1bea1p+143, 0x1.774015499125fp+148,
-    0x1.c95619f1a8e64p+153, 0x1.1dd5d037098fep+159, 0x1.6e39f2c684406p+164, 0x1.e0ac0ea48d948p+169,
-    0x1.42f399d68f1fcp+175, 0x1.bc0ef38704cbbp+180, 0x1.383a833aef5f3p+186, 0x1.c0d41ca4b818ep+191,
-    0x1.499bc508f7324p+197, 0x1.ee69a78d72cb6p+202, 0x1.7a88e4484be3bp+208, 0x1.27baf2587b49ep+214,
-    0x1.d751f23d047dcp+219, 0x1.7ef294d193a63p+225, 0x1.3d20e33d8e45ap+231, 0x1.0b93bfbbf00acp+237,
-    0x1.cbe5f18b04928p+242, 0x1.92693359a4003p+248, 0x1.6665b1bbd6102p+254, 0x1.44cc291239feap+260,
-    0x1.2b6c35dccd76cp+266, 0x1.18b5727f009f5p+272, 0x1.0b8cf1210c97ep+278, 0x1.0330899804332p+284,
-    0x1.fe478ee34844ap+289, 0x1.fe478ee34844ap+295, 0x1.0320568f6ab2ep+302, 0x1.0b395943e6087p+308,
-    0x1.17c0097314d0dp+314, 0x1.293c0a0a461dep+320, 0x1.4074bad313983p+326, 0x1.5e7fac56dd6e8p+332,
-    0x1.84d5a3305da69p+338, 0x1.b5705796695b6p+344, 0x1.f2f423e7902c4p+350, 0x1.207524c1df599p+357,
-    0x1.5209471331bd0p+363, 0x1.916b0466cb107p+369, 0x1.e2f4c14bac4fcp+375, 0x1.264d25ca1d009p+382,
-    0x1.6b473aa57bcccp+388, 0x1.c619094edabffp+394, 0x1.1f5bd7e3e66d7p+401, 0x1.702dac9bff3c4p+407,
-    0x1.dd7b3bda4f022p+413, 0x1.3958df4743d96p+420, 0x1.a02a088aa61cbp+426, 0x1.179c3dbd279b5p+433,
-    0x1.7c1863ed21d72p+439, 0x1.0550c4b30743ep+446, 0x1.6b645188f61a6p+452, 0x1.ff0512a89a152p+458,
-    0x1.6b4d9b43dd8b0p+465, 0x1.051fc798c73bfp+472, 0x1.7b722e0a01831p+478, 0x1.16a7d9cf591c4p+485,
-    0x1.9da1274fc845fp+491, 0x1.3638dd7bd6347p+498, 0x1.d62e2fafb0a78p+504, 0x1.67fb5c8283404p+511,
-    0x1.166c698cf183bp+518, 0x1.b30964ec395dcp+524, 0x1.574569a265440p+531, 0x1.118b502d68b23p+538,
-    0x1.b83c3509147ecp+544, 0x1.65b0eb1760a70p+551, 0x1.256b20d92d490p+558, 0x1.e5f96e67b300ep+564,
-    0x1.963e824aafa2cp+571, 0x1.56c4bdef04315p+578, 0x1.23e389bd89920p+585, 0x1.f5af14bdc472fp+591,
-    0x1.b30dd3fc905bap+598, 0x1.7cac197cfe503p+605, 0x1.500fee805882dp+612, 0x1.2b4e306a4ed48p+619,
-    0x1.0ce83f7f82d2fp+626, 0x1.e764f3171d1e4p+632, 0x1.bd824633209dbp+639, 0x1.9ab418b722116p+646,
-    0x1.7dd36efa41ac2p+653, 0x1.65f6380a9d916p+660, 0x1.5262c0fa08f37p+667, 0x1.42861fee50880p+674,
-    0x1.35ece2af0162bp+681, 0x1.2c3d7b998957ap+688, 0x1.25340ab3f01f9p+695, 0x1.209f3a89205f1p+702,
-};
-
-__constant__ double c_inv_fact[MAX_ORDER1] = {  // 1/k! rounded
-    0x1.0000000000000p+0, 0x1.0000000000000p+0, 0x1.0000000000000p-1, 0x1.5555555555555p-3,
-    0x1.5555555555555p-5, 0x1.1111111111111p-7, 0x1.6c16c16c16c17p-10, 0x1.a01a01a01a01ap-13,
-    0x1.a01a01a01a01ap-16, 0x1.71de3a556c734p-19, 0x1.27e4fb7789f5cp-22, 0x1.ae64567f544e4p-26,
-    0x1.1eed8eff8d898p-29, 0x1.6124613a86d09p-33, 0x1.93974a8c07c9dp-37, 0x1.ae7f3e733b81fp-41,
-    0x1.ae7f3e733b81fp-45, 0x1.952c77030ad4ap-49, 0x1.6827863b97d97p-53, 0x1.2f49b46814157p-57,
-    0x1.e542ba4020225p-62, 0x1.71b8ef6dcf572p-66, 0x1.0ce396db7f853p-70, 0x1.761b413163819p-75,
-    0x1.f2cf01972f578p-80, 0x1.3f3ccdd165fa9p-84, 0x1.88e85fc6a4e59p-89, 0x1.d1ab1c2dccea3p-94,
-    0x1.0a18a2635085dp-98, 0x1.259f98b4358aep-103, 0x1.3932c5047d60ep-108, 0x1.434d2e783f5bdp-113,
-    0x1.434d2e783f5bdp-118, 0x1.3981254dd0d52p-123, 0x1.2710231c0fd7ap-128, 0x1.0dc59c716d91fp-133,
-    0x1.df983290c2ca8p-139, 0x1.9ec8d1c94e85bp-144, 0x1.5d4acb9c0c3abp-149, 0x1.1e99449a4bacep-154,
-    0x1.ca8ed42a12ae4p-160, 0x1.65e61c39d0241p-165, 0x1.10af527530de8p-170, 0x1.95db45257e512p-176,
-    0x1.272b1b03fec6ap-181, 0x1.a3cb872220648p-187, 0x1.240804f659510p-192, 0x1.8da8e0a127ebap-198,
-    0x1.091b406b6ff27p-203, 0x1.5a42f0dfeb086p-209, 0x1.bb36f6e12cd79p-215, 0x1.161872bf7b824p-220,
-    0x1.56457989358c9p-226, 0x1.9d4f1058674dfp-232, 0x1.e9d8f6ed83eaap-238, 0x1.1d008faac5c50p-243,
-    0x1.45b77f9e98e12p-249, 0x1.6db793c887b97p-255, 0x1.938cc661b03f6p-261, 0x1.b5bfc17fa97d2p-267,
-    0x1.d2eeac43e7fd0p-273, 0x1.e9e56d649f768p-279, 0x1.f9b3059128bc6p-285, 0x1.00dcf6a320e1cp-290,
-    0x1.00dcf6a320e1cp-296, 0x1.f9d2a2bb5471ap-303, 0x1.ea7ead50ce01ap-309, 0x1.d48849da8f4a3p-315,
-    0x1.b8f8bdfae136cp-321, 0x1.99046602abcafp-327, 0x1.75f56494ba531p-333, 0x1.5116e3adb9fb9p-339,
-    0x1.2ba2917dfaa6cp-345, 0x1.06b1981a48762p-351, 0x1.c6639f500ea2dp-358, 0x1.83bed30a49edep-364,
-    0x1.4685bf3115d5dp-370, 0x1.0f653132c5ae6p-376, 0x1.bd5dda94f5a18p-383, 0x1.68cda75b82f10p-389,
-    0x1.20a485e2cf273p-395, 0x1.c8206e6fe560cp-402, 0x1.64005631debbep-408, 0x1.1281cd42368abp-414,
-    0x1.a24be3711628bp-421, 0x1.3af3de7343e27p-427, 0x1.d4c44522a0927p-434, 0x1.58d700d5cb749p-440,
-    0x1.f595d2ab567b0p-447, 0x1.68b0c583d6a34p-453, 0x1.007db446ff080p-459, 0x1.68c751f8f632ap-466,
-    0x1.f5f3ec7bc5d71p-473, 0x1.596e0e189e2b7p-479, 0x1.d65f64e59b771p-486, 0x1.3ce1f3216b6dep-492,
-    0x1.a6829981e4928p-499, 0x1.16c503a23d142p-505, 0x1.6c1b7275dcd65p-512, 0x1.d6c3cf76c59b9p-519,
-    0x1.2d4a1e607e781p-525, 0x1.7dd50faf84657p-532, 0x1.df297d187dfcdp-539, 0x1.29bb552f8772dp-545,
-    0x1.6e7068d8092aep-552, 0x1.beb4eb15fc8c0p-559, 0x1.0db5afbffdea5p-565, 0x1.42a4b5885d34fp-572,
-    0x1.7e64655f3f0f6p-579, 0x1.c10c3547ec1b7p-586, 0x1.05439cac2c47dp-592, 0x1.2d470c4e9d270p-599,
-    0x1.585132a2fcbeep-606, 0x1.8605e345153bep-613, 0x1.b5eba9d8cb7dap-620, 0x1.e76cb424808bcp-627,
-    0x1.0cec86b309210p-633, 0x1.263516a53c4fep-640, 0x1.3f23e47f2bba7p-647, 0x1.5746e043f2ccep-654,
-    0x1.6e2977bff1eb9p-661, 0x1.83584be68daaep-668, 0x1.9665084a05f25p-675, 0x1.a6ea2e16eb21ap-682,
-    0x1.b48ea3306e964p-689, 0x1.bf08d841fa750p-696, 0x1.c6215db8ddeccp-703, 0x1.c9b4c7476cc65p-710,
-};
 
 __device__ __forceinline__ double inv_k(int k) { return c_inv_k[k]; }
 
@@ -164,59 +101,6 @@ __device__ __forceinline__ void put_moment(const MomArgs &a, int64_t node, int k
         a.meval[node * a.estride + k] = k == 0 ? m : __dmul_rn(m, c_mev_m[k]);
         if (k == a.order && a.estride > a.order + 1)
             a.meval[node * a.estride + k + 1] = 0.0;
-    }
-}
-
-// Store from the raw power sum S_k = sum_j q_j (x_j - c)^k:
-// m_k = S_k / k!, traversal copy M_k = gamma_(k-1) S_k / k (dt_farcoef.cuh).
-__device__ __forceinline__ void put_raw_sum(const MomArgs &a, int64_t node, int k, double S)
-{
-    a.moments[node * (a.order + 1) + k] = __dmul_rn(S, c_inv_fact[k]);
-    if (a.meval) {
-        a.meval[node * a.estride + k] = k == 0 ? S : __dmul_rn(S, c_mev_s[k]);
-        if (k == a.order && a.estride > a.order + 1)
-            a.meval[node * a.estride + k + 1] = 0.0;
-    }
-}
-
-// P2M for one leaf, order + 1 <= 32, one warp: raw power sums in two
-// halves of 16 orders (2 FP64 ops per source and order), smem transpose-
-// reduce over the 32 lanes.
-__device__ void p2m_leaf_reg(const MomArgs &a, int64_t node, int64_t s, int64_t e, double c,
-                             double (*tr)[33])
-{
-    const int lane = dt_lane();
-    const int o1 = (int)a.order + 1;
-    for (int base = 0; base < o1; base += 16) {
-        double acc[16];
-#pragma unroll
-        for (int k = 0; k < 16; ++k)
-            acc[k] = 0.0;
-        for (int64_t j = s + lane; j < e; j += 32) {
-            const double t = __ldg(a.xs + j) - c;
-            double w = __ldg(a.qs + j);
-            if (base) {
-                const double t2 = t * t, t4 = t2 * t2, t8 = t4 * t4;
-                w *= t8 * t8;
-            }
-#pragma unroll
-            for (int k = 0; k < 16; ++k) {
-                acc[k] += w;
-                w *= t;
-            }
-        }
-#pragma unroll
-        for (int k = 0; k < 16; ++k)
-            tr[k][lane] = acc[k];
-        __syncwarp();
-        if (lane < 16 && base + lane < o1) {
-            double sum = 0.0;
-#pragma unroll 8
-            for (int l = 0; l < 32; ++l)
-                sum += tr[lane][l];
-            put_raw_sum(a, node, base + lane, sum);
-        }
-        __syncwarp();
     }
 }
 
@@ -323,14 +207,12 @@ __global__ void moments_prep_kernel(MomArgs a)
 
 __global__ void __launch_bounds__(MOM_THREADS) moments_kernel(MomArgs a)
 {
-    __shared__ double tr[MOM_WARPS][16][33];
     __shared__ double pw_s[MOM_WARPS][MAX_ORDER1];
     __shared__ double row_s[MOM_WARPS][MAX_ORDER1];
     const int warp = threadIdx.x >> 5, lane = dt_lane();
     const int64_t gwarp = (int64_t)blockIdx.x * MOM_WARPS + warp;
     const int64_t nwarps = (int64_t)gridDim.x * MOM_WARPS;
     const int64_t n_nodes = __ldg(a.meta + DT_META_NODES);
-    const bool reg_path = a.order + 1 <= REG_ORDER;
 
     // each warp scans 32 consecutive nodes at a time for leaves
     for (int64_t c0 = gwarp * 32; c0 < n_nodes; c0 += nwarps * 32) {
@@ -352,10 +234,7 @@ __global__ void __launch_bounds__(MOM_THREADS) moments_kernel(MomArgs a)
             const int64_t ns = __shfl_sync(DT_FULL, s, i);
             const int64_t ne = __shfl_sync(DT_FULL, e, i);
             const double nc = __shfl_sync(DT_FULL, ctr, i);
-            if (reg_path)
-                p2m_leaf_reg(a, node, ns, ne, nc, tr[warp]);
-            else
-                p2m_leaf_generic(a, node, ns, ne, nc, row_s[warp]);
+            p2m_leaf_generic(a, node, ns, ne, nc, row_s[warp]);
             // climb while this warp completes the parent's last child
             while (true) {
                 __threadfence();
@@ -383,159 +262,162 @@ __global__ void __launch_bounds__(MOM_THREADS) moments_kernel(MomArgs a)
     }
 }
 
-// ---- order + 1 <= 32: G lanes per leaf (P2M), dataflow M2M (in-place Pascal) ----
+// ---- order + 1 <= 32: one fused upward pass on traversal-layout rows ----
+//
+// Rows are stored once, in the traversal layout M_k = c_k S_k (c_0 = 1,
+// c_k = gamma_(k-1) / k = c_mev_s[k], dt_farcoef.cuh; S_k = k! m_k the raw
+// power sums), which is all the traversal reads; the reference layout m_k is
+// derived from them only on request (dt_moments_from_eval).  In this basis a
+// Pascal pass S_k += delta S_(k-1) reads
+//     M_k += e_k M_(k-1),   e_k = delta rho_k,   rho_k = c_k / c_(k-1),
+// so the binomial shift costs the same FMAs as on raw sums, and every form
+// below (warp, four parents per warp, thread per node) computes e_k as
+// __dmul_rn(delta, rho_k) and applies the passes in the same order: the rows
+// are bit-identical whichever form (and whichever rank) produced them.
 
-// P2M with G consecutive lanes per leaf: each lane sums every G-th source of
-// the leaf (the group's loads cover contiguous sectors), four sources in
-// flight, then a butterfly over the G lanes.  Leaves are gathered per warp
-// from 32 consecutive node slots (ballot) so no group idles on internal
-// nodes.  Raw power sums S_k = sum q (x - c)^k in registers.
-// KMAX: orders computed, a multiple of 8 >= order + 1, fixed at compile time
-// so the order loop has no per-step guard (a uniform branch per order step
-// costs 25% of the instructions and splits the scheduling window).
+// P2M of one leaf over G lanes: raw power sums S_k = sum q (x - c)^k for
+// k < KMAX, with the powers split as t^(8m + r) = t^r (t^8)^m: per source 7
+// products q t^r, t^8 and its powers, 8 additions and KMAX - 8 FMAs (44 FP64
+// operations at KMAX = 32 instead of 64 for the running-product form).  Two
+// sources per trip; then a butterfly over the G lanes.  Lane `sub` stores
+// orders [sub KMAX/G, (sub + 1) KMAX/G) of the row (16-byte stores; orders
+// >= order + 1 are the row's zero padding).
 template <int G, int KMAX>
-__global__ void __launch_bounds__(256) p2m_group_kernel(MomArgs a)
+__device__ __forceinline__ void p2m_split_leaf(const MomArgs &a, int64_t node, bool active,
+                                               int sub)
 {
-    const int lane = dt_lane();
-    const int sub = lane & (G - 1), grp = lane / G;
-    const int64_t n = __ldg(a.meta + DT_META_NODES);
-    const int o1 = (int)a.order + 1;
-    int64_t cut_begin = INT64_MAX, lo = 0, hi = 0;
-    if (a.plan) {
-        cut_begin = __ldg(a.plan + DT_PLAN_LEVEL_BEGIN);
-        lo = __ldg(a.plan + DT_PLAN_SRC_LO);
-        hi = __ldg(a.plan + DT_PLAN_SRC_HI);
+    static_assert(KMAX % 8 == 0 && KMAX >= 8, "KMAX must be a multiple of 8");
+    constexpr int NM = KMAX / 8;
+    int64_t s = 0, e = 0;
+    double c = 0.0;
+    if (active) {
+        s = __ldg(a.start + node);
+        e = __ldg(a.end + node);
+        c = __ldg(a.center + node);
     }
-    const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t c0 = gwarp * 32; c0 < n; c0 += nwarps * 32) {
-        const int64_t mine = c0 + lane;
-        bool leaf = false;
-        if (mine < n) {
-            const int64_t l = __ldg(a.left + mine), r = __ldg(a.right + mine);
-            if (a.parent) {  // dataflow M2M bookkeeping (m2m_flow_kernel)
-                a.arrived[mine] = 0;
-                if (l >= 0)
-                    a.parent[l] = (int32_t)mine;
-                if (r >= 0)
-                    a.parent[r] = (int32_t)mine;
-                if (mine == 0)
-                    a.parent[0] = -1;
-            }
-            leaf = l < 0 && r < 0;
-            if (leaf && mine >= cut_begin)
-                leaf = __ldg(a.start + mine) >= lo && __ldg(a.end + mine) <= hi;
+    double acc[KMAX];
+#pragma unroll
+    for (int k = 0; k < KMAX; ++k)
+        acc[k] = 0.0;
+    int64_t j = s + sub;
+    for (; j + G < e; j += 2 * G) {
+        const double t0 = __ldg(a.xs + j) - c, t1 = __ldg(a.xs + j + G) - c;
+        double p0[8], p1[8];
+        p0[0] = __ldg(a.qs + j);
+        p1[0] = __ldg(a.qs + j + G);
+#pragma unroll
+        for (int r = 1; r < 8; ++r) {
+            p0[r] = p0[r - 1] * t0;
+            p1[r] = p1[r - 1] * t1;
         }
-        unsigned leaves = __ballot_sync(DT_FULL, leaf);
-        while (leaves) {
-            // group grp takes the grp-th remaining leaf
-            unsigned m = leaves;
-            for (int i = 0; i < grp && m; ++i)
-                m &= m - 1;
-            const bool active = m != 0;
-            const int64_t node = c0 + (active ? __ffs(m) - 1 : 0);
-            for (int i = 0; i < 32 / G && leaves; ++i)
-                leaves &= leaves - 1;
-            int64_t s = 0, e = 0;
-            double c = 0.0;
-            if (active) {
-                s = __ldg(a.start + node);
-                e = __ldg(a.end + node);
-                c = __ldg(a.center + node);
-            }
-            double acc[KMAX];
 #pragma unroll
-            for (int k = 0; k < KMAX; ++k)
-                acc[k] = 0.0;
-            int64_t j = s + sub;
-            for (; j + 3 * G < e; j += 4 * G) {
-                const double t0 = __ldg(a.xs + j) - c, t1 = __ldg(a.xs + j + G) - c;
-                const double t2 = __ldg(a.xs + j + 2 * G) - c, t3 = __ldg(a.xs + j + 3 * G) - c;
-                double w0 = __ldg(a.qs + j), w1 = __ldg(a.qs + j + G);
-                double w2 = __ldg(a.qs + j + 2 * G), w3 = __ldg(a.qs + j + 3 * G);
+        for (int r = 0; r < 8; ++r)
+            acc[r] += p0[r] + p1[r];
+        if (NM > 1) {
+            const double u0 = t0 * t0, u1 = t1 * t1;
+            const double v0 = u0 * u0, v1 = u1 * u1;
+            const double w0 = v0 * v0, w1 = v1 * v1;  // t^8
+            double b0 = w0, b1 = w1;
 #pragma unroll
-                for (int k = 0; k < KMAX; ++k) {
-                    acc[k] += (w0 + w1) + (w2 + w3);
-                    w0 *= t0;
-                    w1 *= t1;
-                    w2 *= t2;
-                    w3 *= t3;
+            for (int m = 1; m < NM; ++m) {
+#pragma unroll
+                for (int r = 0; r < 8; ++r)
+                    acc[8 * m + r] = __fma_rn(p1[r], b1, __fma_rn(p0[r], b0, acc[8 * m + r]));
+                if (m + 1 < NM) {
+                    b0 *= w0;
+                    b1 *= w1;
                 }
             }
-            for (; j < e; j += G) {
-                const double t0 = __ldg(a.xs + j) - c;
-                double w0 = __ldg(a.qs + j);
+        }
+    }
+    if (j < e) {
+        const double t0 = __ldg(a.xs + j) - c;
+        double p0[8];
+        p0[0] = __ldg(a.qs + j);
 #pragma unroll
-                for (int k = 0; k < KMAX; ++k) {
-                    acc[k] += w0;
-                    w0 *= t0;
-                }
+        for (int r = 1; r < 8; ++r)
+            p0[r] = p0[r - 1] * t0;
+#pragma unroll
+        for (int r = 0; r < 8; ++r)
+            acc[r] += p0[r];
+        if (NM > 1) {
+            const double u0 = t0 * t0, v0 = u0 * u0, w0 = v0 * v0;
+            double b0 = w0;
+#pragma unroll
+            for (int m = 1; m < NM; ++m) {
+#pragma unroll
+                for (int r = 0; r < 8; ++r)
+                    acc[8 * m + r] = __fma_rn(p0[r], b0, acc[8 * m + r]);
+                if (m + 1 < NM)
+                    b0 *= w0;
             }
+        }
+    }
 #pragma unroll
-            for (int k = 0; k < KMAX; ++k) {
+    for (int k = 0; k < KMAX; ++k) {
 #pragma unroll
-                for (int o = G / 2; o > 0; o >>= 1)
-                    acc[k] += __shfl_xor_sync(DT_FULL, acc[k], o);
-            }
-            if (active) {
+        for (int o = G / 2; o > 0; o >>= 1)
+            acc[k] += __shfl_xor_sync(DT_FULL, acc[k], o);
+    }
+    if (!active)
+        return;
+    const int o1 = (int)a.order + 1;
+    double2 *row = reinterpret_cast<double2 *>(a.meval + node * a.estride);
+    constexpr int PER = KMAX / G;
 #pragma unroll
-                for (int k = 0; k < KMAX; ++k)
-                    if ((k & (G - 1)) == sub && k < o1)
-                        put_raw_sum(a, node, k, acc[k]);
-            }
+    for (int k = 0; k < KMAX; k += 2) {
+        if (k / PER == sub && k < a.estride) {
+            const double v0 = k < o1 ? (k == 0 ? acc[0] : __dmul_rn(acc[k], c_mev_s[k])) : 0.0;
+            const double v1 = k + 1 < o1 ? __dmul_rn(acc[k + 1], c_mev_s[k + 1]) : 0.0;
+            row[k >> 1] = make_double2(v0, v1);
         }
     }
 }
 
-// Form internal node P from its children, one warp, lane k = order k, on
-// raw power sums S_k = k! m_k: the binomial shift S'_k = sum_j C(k, j)
-// delta^(k-j) S_j is applied in place as 31 passes of S_k += delta S_(k-1)
-// (Pascal's rule; the previous pass's S_(k-1) comes from lane k-1).  Both
-// children run in the same passes.  Same arithmetic, term for term, as the
-// thread-per-node form m2m_level_threads (skipped orders take a zero shift).
-__device__ __forceinline__ void m2m_form_warp(const MomArgs &a, int64_t P)
+// Form internal node P from its children with one warp, lane k = order k:
+// 31 M-basis Pascal passes for both children at once (the previous pass's
+// M_(k-1) comes from lane k - 1; orders below the pass take a zero factor).
+__device__ __forceinline__ void up_form_warp(const MomArgs &a, int64_t P, const double *rho_s)
 {
     const int lane = dt_lane();
     const int o1 = (int)a.order + 1;
+    const int64_t es = a.estride;
     const int64_t l = __ldg(a.left + P), r = __ldg(a.right + P);
     const double c = __ldg(a.center + P);
     const double dl = l >= 0 ? __ldg(a.center + l) - c : 0.0;
     const double dr = r >= 0 ? __ldg(a.center + r) - c : 0.0;
-    const double fk = c_fact_km1[lane + 1];
-    double Sl = (l >= 0 && lane < o1) ? __dmul_rn(__ldcg(a.moments + l * o1 + lane), fk) : 0.0;
-    double Sr = (r >= 0 && lane < o1) ? __dmul_rn(__ldcg(a.moments + r * o1 + lane), fk) : 0.0;
+    const double rho = rho_s[lane];
+    const double el = __dmul_rn(dl, rho), er = __dmul_rn(dr, rho);
+    double Ml = (l >= 0 && lane < o1) ? __ldcg(a.meval + l * es + lane) : 0.0;
+    double Mr = (r >= 0 && lane < o1) ? __ldcg(a.meval + r * es + lane) : 0.0;
 #pragma unroll
     for (int i = 1; i < REG_ORDER; ++i) {
-        const double tl = __shfl_up_sync(DT_FULL, Sl, 1);
-        const double tr = __shfl_up_sync(DT_FULL, Sr, 1);
-        // orders below i take a zero shift (in place, as m2m_form_group8)
+        const double tl = __shfl_up_sync(DT_FULL, Ml, 1);
+        const double tr = __shfl_up_sync(DT_FULL, Mr, 1);
         const bool on = lane >= i;
-        Sl = __fma_rn(on ? dl : 0.0, tl, Sl);
-        Sr = __fma_rn(on ? dr : 0.0, tr, Sr);
+        Ml = __fma_rn(on ? el : 0.0, tl, Ml);
+        Mr = __fma_rn(on ? er : 0.0, tr, Mr);
     }
     double out = 0.0;
     if (l >= 0)
-        out += Sl;
+        out += Ml;
     if (r >= 0)
-        out += Sr;
-    if (lane < o1)
-        put_raw_sum(a, P, lane, out);
+        out += Mr;
+    if (lane < es)
+        a.meval[P * es + lane] = lane < o1 ? out : 0.0;
 }
 
-// Four parents per warp at once: lanes [8g, 8g + 8) form parent P (of group
-// g), lane l of a group holding orders 4l .. 4l + 3 of both children.  A
-// Pascal pass then needs one neighbour value per lane (the last order of
-// lane l - 1), so a parent costs 8x fewer shuffles than with one order per
-// lane.  Same arithmetic, term for term, as m2m_form_warp / the thread form
-// (orders a pass skips take a zero shift, fma(0, x, S) = S: equal values, a
-// zero's sign aside).
-__device__ __forceinline__ void m2m_form_group8(const MomArgs &a, int64_t P)
+// Four parents per warp: lanes [8g, 8g + 8) form parent P of group g, lane
+// gl of a group holding orders 4 gl .. 4 gl + 3 of both children, so a pass
+// needs one neighbour value per lane.  Term for term the arithmetic of
+// up_form_warp (a skipped order's update is fma(0, x, M) = M).
+__device__ __forceinline__ void up_form_group8(const MomArgs &a, int64_t P, const double *rho_s)
 {
-    const int gl = dt_lane() & 7;  // lane within the group
+    const int gl = dt_lane() & 7;
     const int o1 = (int)a.order + 1;
+    const int64_t es = a.estride;
     int64_t l = -1, r = -1;
     double dl = 0.0, dr = 0.0;
-    double Sl[4], Sr[4];
     if (P >= 0) {
         l = __ldg(a.left + P);
         r = __ldg(a.right + P);
@@ -545,51 +427,52 @@ __device__ __forceinline__ void m2m_form_group8(const MomArgs &a, int64_t P)
         if (r >= 0)
             dr = __ldg(a.center + r) - c;
     }
+    double Ml[4], Mr[4], el[4], er[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
         const int k = 4 * gl + u;
-        const double fk = c_fact_km1[k + 1];
-        Sl[u] = (l >= 0 && k < o1) ? __dmul_rn(__ldcg(a.moments + l * o1 + k), fk) : 0.0;
-        Sr[u] = (r >= 0 && k < o1) ? __dmul_rn(__ldcg(a.moments + r * o1 + k), fk) : 0.0;
+        el[u] = __dmul_rn(dl, rho_s[k]);
+        er[u] = __dmul_rn(dr, rho_s[k]);
+        Ml[u] = (l >= 0 && k < o1) ? __ldcg(a.meval + l * es + k) : 0.0;
+        Mr[u] = (r >= 0 && k < o1) ? __ldcg(a.meval + r * es + k) : 0.0;
     }
-    const unsigned mask = DT_FULL;
 #pragma unroll
     for (int i = 1; i < REG_ORDER; ++i) {
-        const double nl = __shfl_up_sync(mask, Sl[3], 1, 8);
-        const double nr = __shfl_up_sync(mask, Sr[3], 1, 8);
+        const double nl = __shfl_up_sync(DT_FULL, Ml[3], 1, 8);
+        const double nr = __shfl_up_sync(DT_FULL, Mr[3], 1, 8);
         // descending within the lane: every update reads the previous pass
 #pragma unroll
         for (int u = 3; u >= 0; --u) {
-            // orders k = 4 gl + u < i sit this pass out: their shift is 0,
-            // and fma(0, x, S) = S (up to the sign of a zero S), which keeps
-            // every update in place; gl >= ceil((i - u) / 4) takes at most
-            // two values per pass
             const bool on = gl >= ((i - u + 3) >> 2);
-            const double el = on ? dl : 0.0, er = on ? dr : 0.0;
-            Sl[u] = __fma_rn(el, u ? Sl[u - 1] : nl, Sl[u]);
-            Sr[u] = __fma_rn(er, u ? Sr[u - 1] : nr, Sr[u]);
+            Ml[u] = __fma_rn(on ? el[u] : 0.0, u ? Ml[u - 1] : nl, Ml[u]);
+            Mr[u] = __fma_rn(on ? er[u] : 0.0, u ? Mr[u - 1] : nr, Mr[u]);
         }
     }
     if (P < 0)
         return;
+    double v[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
         const int k = 4 * gl + u;
         double out = 0.0;
         if (l >= 0)
-            out += Sl[u];
+            out += Ml[u];
         if (r >= 0)
-            out += Sr[u];
-        if (k < o1)
-            put_raw_sum(a, P, k, out);
+            out += Mr[u];
+        v[u] = k < o1 ? out : 0.0;
+    }
+    if (4 * gl < es) {  // es is even: orders 4 gl, 4 gl + 1 share a 16-byte word
+        double2 *row = reinterpret_cast<double2 *>(a.meval + P * es);
+        row[2 * gl] = make_double2(v[0], v[1]);
+        if (4 * gl + 2 < es)
+            row[2 * gl + 1] = make_double2(v[2], v[3]);
     }
 }
 
 // Arrival on a node's counter with acquire-release semantics at GPU scope:
-// the release publishes the rows this warp formed (ordered before it by a
+// the release publishes the rows this warp wrote (ordered before it by a
 // __syncwarp), the acquire makes the rows behind earlier arrivals visible to
-// the lane that completes the node (and, after a __syncwarp, to its group).
-// One MEMBAR.ALL.GPU per round instead of two MEMBAR.SC.GPU fences.
+// the lane that completes the node (and, after a __syncwarp, to its warp).
 __device__ __forceinline__ int arrive_acq_rel(int32_t *p)
 {
     int old;
@@ -597,26 +480,28 @@ __device__ __forceinline__ int arrive_acq_rel(int32_t *p)
     return old;
 }
 
-// A leaf's arrival: its row comes from the P2M launch (ordered by the kernel
-// boundary), so only the acquire is needed.
-__device__ __forceinline__ int arrive_acquire(int32_t *p)
-{
-    int old;
-    asm volatile("atom.add.acquire.gpu.s32 %0, [%1], 1;" : "=r"(old) : "l"(p) : "memory");
-    return old;
-}
-
-// Upward pass without grid barriers (after the P2M kernel, which also wrote
-// parent[] and zeroed arrived[]): every leaf bumps its parent's arrival
-// counter; the warp whose arrival completes a parent forms it and keeps
-// climbing while it completes the next ancestor.  With a shard plan the
-// climb stops below the cut level and covers the plan's subtrees only.
-#ifndef DT_M2M_MINB
-#define DT_M2M_MINB 4  // 64 registers: 4 blocks per SM (3: 0.43 ms, 5: 0.42 ms, 4: 0.39 ms)
+// The fused upward pass (after moments_prep_kernel wrote parent[] and zeroed
+// arrived[]): warps take 32 consecutive node slots at a time, deepest
+// first (their chains are the critical path); every leaf among them is
+// formed by P2M (32 / G leaves per round), then each formed leaf arrives at
+// its parent, and a lane whose arrival completes a parent keeps it: the warp
+// forms the kept parents (four at a time, or one with all 32 lanes) and
+// those lanes climb on.  Chains start while other warps are still in P2M,
+// so the M2M latency overlaps the P2M throughput.  With a shard plan, leaves
+// below the cut outside the rank's source range are skipped and climbs stop
+// below the cut level.
+#ifndef DT_UP_MINB
+#define DT_UP_MINB 2
 #endif
-__global__ void __launch_bounds__(256, DT_M2M_MINB) m2m_flow_kernel(MomArgs a)
+template <int G, int KMAX>
+__global__ void __launch_bounds__(256, DT_UP_MINB) upward_kernel(MomArgs a)
 {
+    __shared__ double rho_s[REG_ORDER];
+    if (threadIdx.x < REG_ORDER)
+        rho_s[threadIdx.x] = c_mev_rho[threadIdx.x];
+    __syncthreads();
     const int lane = dt_lane();
+    const int sub = lane & (G - 1), grp = lane / G;
     const int64_t n = __ldg(a.meta + DT_META_NODES);
     int64_t cut_begin = 0, lo = 0, hi = 0;
     if (a.plan) {
@@ -626,69 +511,72 @@ __global__ void __launch_bounds__(256, DT_M2M_MINB) m2m_flow_kernel(MomArgs a)
     }
     const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    constexpr int CH = 32;  // nodes scanned per warp step
-    for (int64_t r0 = gwarp * CH; r0 < n; r0 += nwarps * CH) {
-        // deepest levels first: their chains are the critical path
-        const int64_t c0 = n - CH - r0;  // may be negative for the last chunk
+    for (int64_t r0 = gwarp * 32; r0 < n; r0 += nwarps * 32) {
+        const int64_t c0 = n - 32 - r0;  // may be negative for the last chunk
         const int64_t mine = c0 + lane;
-        bool done = false;
+        bool form = false, climb = false;
         int64_t par = -1;
-        if (lane < CH && mine >= 0 && mine < n && __ldg(a.left + mine) < 0 &&
-            __ldg(a.right + mine) < 0) {
+        if (mine >= 0 && mine < n && __ldg(a.left + mine) < 0 && __ldg(a.right + mine) < 0) {
+            const bool in = !a.plan ||
+                            (__ldg(a.start + mine) >= lo && __ldg(a.end + mine) <= hi);
+            // leaves above the cut are formed by every rank; they never climb
+            form = in || mine < cut_begin;
             par = __ldcg(a.parent + mine);
-            bool in = par >= cut_begin;
-            if (in && a.plan)
-                in = __ldg(a.start + mine) >= lo && __ldg(a.end + mine) <= hi;
-            if (in) {
-                const int need = (__ldg(a.left + par) >= 0) + (__ldg(a.right + par) >= 0);
-                done = arrive_acquire(a.arrived + par) == need - 1;
-            }
+            climb = in && par >= cut_begin && par >= 0;
+#if DT_UP_NOCLIMB
+            climb = false;
+#endif
         }
-        // lanes hold the parents they completed; four of them are formed at a
-        // time (one per 8-lane group), then each of those lanes arrives at its
-        // own grandparent and keeps it if the arrival completes it
+        unsigned leaves = __ballot_sync(DT_FULL, form);
+        while (leaves) {
+            // group grp takes the grp-th remaining leaf
+            unsigned m = leaves;
+            for (int i = 0; i < grp && m; ++i)
+                m &= m - 1;
+            const bool active = m != 0;
+            const int64_t node = c0 + (active ? __ffs(m) - 1 : 0);
+            for (int i = 0; i < 32 / G && leaves; ++i)
+                leaves &= leaves - 1;
+            p2m_split_leaf<G, KMAX>(a, node, active, sub);
+        }
+        __syncwarp();  // the rows precede the releasing arrivals
+        bool done = false;
+        if (climb) {
+            const int need = (__ldg(a.left + par) >= 0) + (__ldg(a.right + par) >= 0);
+            done = arrive_acq_rel(a.arrived + par) == need - 1;
+        }
         if (!done)
             par = -1;
         while (true) {
             const unsigned todo = __ballot_sync(DT_FULL, par >= 0);
             if (!todo)
                 break;
+            unsigned sel;
             if (__popc(todo) == 1) {
-                // a lone parent (the usual case high in a chain): all 32
-                // lanes, one order each, a third of the group form's work
-                const int src = __ffs(todo) - 1;
+                // a lone parent (the usual case high in a chain): all 32 lanes
+                sel = todo;
                 __syncwarp();
-                m2m_form_warp(a, __shfl_sync(DT_FULL, par, src));
-                __syncwarp();
-                if (lane == src) {
-                    const int64_t q = __ldcg(a.parent + par);
-                    int64_t nxt = -1;
-                    if (q >= cut_begin && q >= 0) {
-                        const int need = (__ldg(a.left + q) >= 0) + (__ldg(a.right + q) >= 0);
-                        if (arrive_acq_rel(a.arrived + q) == need - 1)
-                            nxt = q;
-                    }
-                    par = nxt;
-                }
-                continue;
-            }
-            unsigned sel = 0, t = todo;
-            int64_t mine_p = -1;
+                up_form_warp(a, __shfl_sync(DT_FULL, par, __ffs(todo) - 1), rho_s);
+            } else {
+                unsigned t = todo;
+                int64_t mine_p = -1;
+                sel = 0;
 #pragma unroll
-            for (int g = 0; g < 4; ++g) {
-                int64_t pg = -1;
-                if (t) {
-                    const int src = __ffs(t) - 1;
-                    t &= t - 1;
-                    sel |= 1u << src;
-                    pg = __shfl_sync(DT_FULL, par, src);
+                for (int g = 0; g < 4; ++g) {
+                    int64_t pg = -1;
+                    if (t) {
+                        const int src = __ffs(t) - 1;
+                        t &= t - 1;
+                        sel |= 1u << src;
+                        pg = __shfl_sync(DT_FULL, par, src);
+                    }
+                    if ((lane >> 3) == g)
+                        mine_p = pg;
                 }
-                if ((lane >> 3) == g)
-                    mine_p = pg;
+                __syncwarp();  // the completing lanes' acquires precede the loads
+                up_form_group8(a, mine_p, rho_s);
             }
-            __syncwarp();  // the completing lanes' acquires precede the group's loads
-            m2m_form_group8(a, mine_p);
-            __syncwarp();  // the group's stores precede the releasing arrivals
+            __syncwarp();  // the stores precede the releasing arrivals
             if ((sel >> lane) & 1u) {
                 const int64_t q = __ldcg(a.parent + par);
                 int64_t nxt = -1;
@@ -703,20 +591,17 @@ __global__ void __launch_bounds__(256, DT_M2M_MINB) m2m_flow_kernel(MomArgs a)
     }
 }
 
-// M2M of one level with one thread per internal node, on raw power sums:
-// S'_k = sum_j C(k, j) delta^(k-j) S_j (the binomial transform) computed in
-// place by k passes of S_k += delta S_(k-1) over descending k (Pascal's
-// rule), so a child row needs only its own 32 registers.
-__device__ __forceinline__ void m2m_level_threads(const MomArgs &a, int64_t f0, int64_t f1,
-                                                  int64_t tid, int64_t nthreads, bool filter,
-                                                  int64_t src_lo, int64_t src_hi)
+// M2M of one level with one thread per internal node (shard_finish): the
+// M-basis Pascal passes in place over descending k, the arithmetic of
+// up_form_warp term for term.
+__device__ __forceinline__ void up_level_threads(const MomArgs &a, int64_t f0, int64_t f1,
+                                                 int64_t tid, int64_t nthreads)
 {
     const int o1 = (int)a.order + 1;
+    const int64_t es = a.estride;
     for (int64_t node = f0 + tid; node < f1; node += nthreads) {
         const int64_t l = __ldg(a.left + node), r = __ldg(a.right + node);
         if (l < 0 && r < 0)
-            continue;
-        if (filter && (__ldg(a.start + node) < src_lo || __ldg(a.end + node) > src_hi))
             continue;
         const double c = __ldg(a.center + node);
         double out[REG_ORDER];
@@ -729,30 +614,43 @@ __device__ __forceinline__ void m2m_level_threads(const MomArgs &a, int64_t f0, 
             if (ch < 0)
                 continue;
             const double delta = __ldg(a.center + ch) - c;
-            const double *row = a.moments + ch * o1;
-            // L2-coherent loads (the row was formed earlier in this kernel),
-            // all issued before the first use
-            double S[REG_ORDER];
+            const double *row = a.meval + ch * es;
+            double M[REG_ORDER];
 #pragma unroll
             for (int k = 0; k < REG_ORDER; ++k)
-                S[k] = k < o1 ? __ldcg(row + k) : 0.0;
-#pragma unroll
-            for (int k = 0; k < REG_ORDER; ++k)
-                S[k] = __dmul_rn(S[k], c_fact_km1[k + 1]);
+                M[k] = k < o1 ? __ldcg(row + k) : 0.0;
 #pragma unroll
             for (int i = 1; i < REG_ORDER; ++i) {
 #pragma unroll
                 for (int k = REG_ORDER - 1; k >= i; --k)
-                    S[k] = __fma_rn(delta, S[k - 1], S[k]);
+                    M[k] = __fma_rn(__dmul_rn(delta, c_mev_rho[k]), M[k - 1], M[k]);
             }
 #pragma unroll
             for (int k = 0; k < REG_ORDER; ++k)
-                out[k] += S[k];
+                out[k] += M[k];
         }
 #pragma unroll
         for (int k = 0; k < REG_ORDER; ++k)
-            if (k < o1)
-                put_raw_sum(a, node, k, out[k]);
+            if (k < es)
+                a.meval[node * es + k] = k < o1 ? out[k] : 0.0;
+    }
+}
+
+// Reference-layout moments from traversal rows: m_k = M_k / ((k-1)! gamma_(k-1))
+// (tree.py:224-238 semantics, for the API's Tree.moments).
+__global__ void moments_from_eval_kernel(const double *__restrict__ meval, int64_t es,
+                                         const int64_t *meta, int64_t n, int64_t o1,
+                                         double *__restrict__ moments)
+{
+    if (meta)
+        n = __ldg(meta + DT_META_NODES);
+    const int64_t total = n * o1;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t node = i / o1;
+        const int k = (int)(i - node * o1);
+        const double v = __ldg(meval + node * es + k);
+        moments[i] = k == 0 ? v : __ddiv_rn(v, c_mev_m[k]);
     }
 }
 
@@ -864,71 +762,69 @@ __global__ void __launch_bounds__(PLAN_THREADS)
     }
 }
 
-__global__ void shard_pack_kernel(const int64_t *plan, int rank, int64_t o1, const double *moments,
-                                  const double *meval, int64_t es, double *send)
+__global__ void shard_pack_kernel(const int64_t *plan, int rank, const double *meval, int64_t es,
+                                  double *send)
 {
     const int64_t a0 = __ldg(plan + DT_PLAN_OWNER0 + rank);
     const int64_t rows = __ldg(plan + DT_PLAN_OWNER0 + rank + 1) - a0;
-    const int64_t w = o1 + es;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < rows * w;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t row = i / w, k = i - row * w;
-        send[i] = k < o1 ? __ldg(moments + (a0 + row) * o1 + k)
-                         : __ldg(meval + (a0 + row) * es + (k - o1));
-    }
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < rows * es;
+         i += (int64_t)gridDim.x * blockDim.x)
+        send[i] = __ldg(meval + a0 * es + i);
 }
 
 // One block: scatter every owner's level-l rows, then M2M levels cut-1 .. 0
-// (thread per node; the same arithmetic as m2m_form_warp, so the rows match
+// (thread per node; the same arithmetic as up_form_warp, so the rows match
 // the single-GPU pass bit for bit).
 __global__ void __launch_bounds__(256) shard_finish_kernel(MomArgs a, int world, int64_t slot_rows,
                                                            const double *recv)
 {
-    const int64_t o1 = a.order + 1, es = a.meval ? a.estride : 0, w = o1 + es;
+    const int64_t es = a.estride;
     for (int r = 0; r < world; ++r) {
         const int64_t a0 = __ldg(a.plan + DT_PLAN_OWNER0 + r);
         const int64_t rows = __ldg(a.plan + DT_PLAN_OWNER0 + r + 1) - a0;
-        const double *slot = recv + (int64_t)r * slot_rows * w;
-        for (int64_t i = threadIdx.x; i < rows * w; i += blockDim.x) {
-            const int64_t row = i / w, k = i - row * w;
-            if (k < o1)
-                a.moments[(a0 + row) * o1 + k] = slot[i];
-            else
-                a.meval[(a0 + row) * es + (k - o1)] = slot[i];
-        }
+        const double *slot = recv + (int64_t)r * slot_rows * es;
+        for (int64_t i = threadIdx.x; i < rows * es; i += blockDim.x)
+            a.meval[a0 * es + i] = slot[i];
     }
     __syncthreads();
     const int64_t cut = __ldg(a.plan + DT_PLAN_CUT);
     for (int64_t lev = cut - 1; lev >= 0; --lev) {
-        m2m_level_threads(a, __ldg(a.meta + DT_META_LEVEL0 + lev),
-                          __ldg(a.meta + DT_META_LEVEL0 + lev + 1), threadIdx.x, blockDim.x,
-                          false, 0, 0);
+        up_level_threads(a, __ldg(a.meta + DT_META_LEVEL0 + lev),
+                         __ldg(a.meta + DT_META_LEVEL0 + lev + 1), threadIdx.x, blockDim.x);
         __syncthreads();
     }
 }
 
-// Upward pass for order + 1 <= 32 (honouring a.plan): P2M, then the
-// barrier-free M2M dataflow.  Level-synchronous M2M variants (grid barrier
-// per level, one launch per level, narrow/wide phases) all measured slower
-// on configs[2] (0.47-0.95 ms against 0.36 ms): a grid barrier costs ~5 us
-// and the tree is 32 levels deep.
+// Upward pass for order + 1 <= 32 (honouring a.plan): the parent/arrival
+// bookkeeping, then the fused P2M + M2M dataflow kernel.  Level-synchronous
+// M2M variants (grid barrier per level, one launch per level) measured
+// slower in round 1 (0.47-0.95 ms against 0.36 ms at configs[2]): a grid
+// barrier costs ~5 us and the tree is 32 levels deep.
 int launch_level_moments(MomArgs &a, cudaStream_t s)
 {
     const int sms = dt_num_sms();
     if (!a.parent)
         return dt_set_error(DT_ERR_WORKSPACE, "moments workspace missing");
+    if (!a.meval)
+        return dt_set_error(DT_ERR_INVALID, "order <= 31 needs the traversal rows (moments_eval)");
+    moments_prep_kernel<<<sms * 8, 256, 0, s>>>(a);
+    DT_CUDA_TRY(cudaGetLastError());
     const int64_t o1 = a.order + 1;
+    const int grid = sms * DT_UP_MINB;
     if (o1 <= 8)
-        p2m_group_kernel<DT_P2M_G, 8><<<sms * 8, 256, 0, s>>>(a);
+        upward_kernel<DT_P2M_G, 8><<<grid, 256, 0, s>>>(a);
     else if (o1 <= 16)
-        p2m_group_kernel<DT_P2M_G, 16><<<sms * 8, 256, 0, s>>>(a);
+        upward_kernel<DT_P2M_G, 16><<<grid, 256, 0, s>>>(a);
     else if (o1 <= 24)
-        p2m_group_kernel<DT_P2M_G, 24><<<sms * 8, 256, 0, s>>>(a);
+        upward_kernel<DT_P2M_G, 24><<<grid, 256, 0, s>>>(a);
     else
-        p2m_group_kernel<DT_P2M_G, 32><<<sms * 8, 256, 0, s>>>(a);
+        upward_kernel<DT_P2M_G, 32><<<grid, 256, 0, s>>>(a);
     DT_CUDA_TRY(cudaGetLastError());
-    m2m_flow_kernel<<<sms * 8, 256, 0, s>>>(a);
-    DT_CUDA_TRY(cudaGetLastError());
+    if (a.moments) {  // the reference layout as well (API builds ask for it lazily instead)
+        moments_from_eval_kernel<<<sms * 8, 256, 0, s>>>(a.meval, a.estride, a.meta, 0, o1,
+                                                         a.moments);
+        DT_CUDA_TRY(cudaGetLastError());
+    }
     return DT_OK;
 }
 
@@ -950,8 +846,10 @@ extern "C" int dt_moments(const double *xs, const double *qs, const double *cent
                  "eval_stride must be even and >= order + 1");
     DT_CHECK_ARG(order >= 0 && order < MAX_ORDER1, "moment order must be in [0, 127]");
     DT_CHECK_ARG(node_capacity >= 1 && node_capacity < (int64_t)1 << 31, "bad node capacity");
-    DT_CHECK_ARG(xs && qs && center && start && end && left && right && meta && moments,
-                 "null pointer");
+    DT_CHECK_ARG(xs && qs && center && start && end && left && right && meta, "null pointer");
+    DT_CHECK_ARG(order + 1 <= REG_ORDER ? moments_eval != nullptr : moments != nullptr,
+                 "order <= 31 needs moments_eval, higher orders need moments");
+    DT_CHECK_ARG(((uintptr_t)moments_eval & 15) == 0, "moments_eval must be 16-byte aligned");
     if (!workspace || workspace_bytes < dt_moments_workspace(node_capacity))
         return dt_set_error(DT_ERR_WORKSPACE, "moments workspace too small");
     MomArgs a{xs, qs, center, start, end, left, right, meta, order, moments, moments_eval,
@@ -986,11 +884,28 @@ extern "C" int dt_shard_plan(const double *center, const double *half, const int
     return DT_OK;
 }
 
+extern "C" int dt_moments_from_eval(const double *moments_eval, int64_t eval_stride,
+                                    int64_t n_nodes, int64_t order, double *moments,
+                                    void *stream)
+{
+    DT_CHECK_ARG(n_nodes >= 0 && order >= 0 && order < MAX_ORDER1, "bad node count / order");
+    DT_CHECK_ARG(eval_stride >= order + 1, "eval_stride must be >= order + 1");
+    if (n_nodes == 0)
+        return DT_OK;
+    DT_CHECK_ARG(moments_eval && moments, "null pointer");
+    const int64_t total = n_nodes * (order + 1);
+    const int64_t blocks = std::min<int64_t>((total + 255) / 256, (int64_t)dt_num_sms() * 8);
+    moments_from_eval_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(
+        moments_eval, eval_stride, nullptr, n_nodes, order + 1, moments);
+    DT_CUDA_TRY(cudaGetLastError());
+    return DT_OK;
+}
+
 extern "C" size_t dt_shard_rows_bytes(int64_t cut_level, int64_t order, int64_t eval_stride)
 {
-    if (cut_level < 0 || cut_level > 20 || order < 0 || eval_stride < 0)
+    if (cut_level < 0 || cut_level > 20 || order < 0 || eval_stride < order + 1)
         return 0;
-    return ((size_t)1 << cut_level) * (size_t)(order + 1 + eval_stride) * sizeof(double);
+    return ((size_t)1 << cut_level) * (size_t)eval_stride * sizeof(double);
 }
 
 extern "C" int dt_moments_partial(const double *xs, const double *qs, const double *center,
@@ -1004,11 +919,14 @@ extern "C" int dt_moments_partial(const double *xs, const double *qs, const doub
     DT_CHECK_ARG(!moments_eval || (eval_stride >= order + 1 && eval_stride % 2 == 0),
                  "eval_stride must be even and >= order + 1");
     DT_CHECK_ARG(node_capacity >= 1 && node_capacity < (int64_t)1 << 31, "bad node capacity");
-    DT_CHECK_ARG(xs && qs && center && start && end && left && right && meta && plan && moments,
+    DT_CHECK_ARG(xs && qs && center && start && end && left && right && meta && plan &&
+                     moments_eval,
                  "null pointer");
     if (!workspace || workspace_bytes < dt_moments_workspace(node_capacity))
         return dt_set_error(DT_ERR_WORKSPACE, "moments workspace too small");
-    MomArgs a{xs, qs, center, start, end, left, right, meta, order, moments, moments_eval,
+    // the reference layout (moments) is derived by dt_shard_finish, once every row exists
+    (void)moments;
+    MomArgs a{xs, qs, center, start, end, left, right, meta, order, nullptr, moments_eval,
               eval_stride, (int32_t *)workspace, (int32_t *)workspace + node_capacity, plan};
     return launch_level_moments(a, (cudaStream_t)stream);
 }
@@ -1017,17 +935,17 @@ extern "C" int dt_shard_pack(const int64_t *plan, int rank, int64_t cut_level, i
                              const double *moments, const double *moments_eval,
                              int64_t eval_stride, double *send, void *stream)
 {
-    DT_CHECK_ARG(plan && moments && send, "null pointer");
+    (void)moments;  // the traversal rows carry everything (reference layout derived later)
+    DT_CHECK_ARG(plan && moments_eval && send, "null pointer");
     DT_CHECK_ARG(rank >= 0 && rank < DT_MAX_WORLD, "bad rank");
     DT_CHECK_ARG(cut_level >= 0 && cut_level <= 20 && order >= 0, "bad cut level / order");
-    const int64_t es = moments_eval ? eval_stride : 0;
-    DT_CHECK_ARG(!moments_eval || (eval_stride >= order + 1 && eval_stride % 2 == 0),
+    DT_CHECK_ARG(eval_stride >= order + 1 && eval_stride % 2 == 0,
                  "eval_stride must be even and >= order + 1");
-    const int64_t cells = ((int64_t)1 << cut_level) * (order + 1 + es);
+    const int64_t cells = ((int64_t)1 << cut_level) * eval_stride;
     int blocks = (int)((cells + 255) / 256);
     blocks = blocks < 1 ? 1 : (blocks > 4 * dt_num_sms() ? 4 * dt_num_sms() : blocks);
-    shard_pack_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(plan, rank, order + 1, moments,
-                                                               moments_eval, es, send);
+    shard_pack_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(plan, rank, moments_eval,
+                                                               eval_stride, send);
     DT_CUDA_TRY(cudaGetLastError());
     return DT_OK;
 }
@@ -1038,17 +956,22 @@ extern "C" int dt_shard_finish(const int64_t *plan, int world, int64_t cut_level
                                double *moments, double *moments_eval, int64_t eval_stride,
                                void *stream)
 {
-    DT_CHECK_ARG(plan && recv && center && left && right && meta && moments, "null pointer");
+    DT_CHECK_ARG(plan && recv && center && left && right && meta && moments_eval, "null pointer");
     DT_CHECK_ARG(world >= 1 && world <= DT_MAX_WORLD, "bad world size");
     DT_CHECK_ARG(cut_level >= 0 && cut_level <= 20, "bad cut level");
     DT_CHECK_ARG(order >= 0 && order + 1 <= REG_ORDER, "sharded moments need order <= 31");
-    DT_CHECK_ARG(!moments_eval || (eval_stride >= order + 1 && eval_stride % 2 == 0),
+    DT_CHECK_ARG(eval_stride >= order + 1 && eval_stride % 2 == 0,
                  "eval_stride must be even and >= order + 1");
     // start/end are only read by the range filter, which is open here
-    MomArgs a{nullptr, nullptr, center, nullptr, nullptr, left, right, meta, order, moments,
+    MomArgs a{nullptr, nullptr, center, nullptr, nullptr, left, right, meta, order, nullptr,
               moments_eval, eval_stride, nullptr, nullptr, plan};
-    shard_finish_kernel<<<1, 256, 0, (cudaStream_t)stream>>>(a, world, (int64_t)1 << cut_level,
-                                                             recv);
+    cudaStream_t s = (cudaStream_t)stream;
+    shard_finish_kernel<<<1, 256, 0, s>>>(a, world, (int64_t)1 << cut_level, recv);
     DT_CUDA_TRY(cudaGetLastError());
+    if (moments) {
+        moments_from_eval_kernel<<<dt_num_sms() * 8, 256, 0, s>>>(moments_eval, eval_stride, meta,
+                                                                  0, order + 1, moments);
+        DT_CUDA_TRY(cudaGetLastError());
+    }
     return DT_OK;
 }

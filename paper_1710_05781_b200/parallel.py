@@ -128,7 +128,7 @@ class ShardedMoments:
 
     LAUNCHES = 5  # plan, p2m, m2m, pack, finish (the all-gather is NCCL's)
 
-    def __init__(self, bufs, order: int, moments: torch.Tensor, meval: torch.Tensor | None,
+    def __init__(self, bufs, order: int, moments: torch.Tensor | None, meval: torch.Tensor,
                  estride: int, theta: float, world: int, rank: int, group=None,
                  cut_level: int | None = None):
         from . import _lib
@@ -138,12 +138,14 @@ class ShardedMoments:
         if order + 1 > 32:
             raise ValueError("sharded moments need moment order <= 31")
         self.bufs, self.order = bufs, int(order)
+        # moments (reference layout) may be None: the gathered and formed rows
+        # are traversal rows (meval); finish() derives moments when given
         self.moments, self.meval = moments, meval
-        self.estride = int(estride) if meval is not None else 0
+        self.estride = int(estride)
         self.theta = float(theta)
         self.world, self.rank, self.group = int(world), int(rank), group
         self.cut = default_cut_level(world) if cut_level is None else int(cut_level)
-        dev = moments.device
+        dev = meval.device
         nbytes = int(_lib.load().dt_shard_rows_bytes(self.cut, self.order, self.estride))
         if nbytes == 0:
             raise ValueError(f"bad cut level {self.cut}")
@@ -216,7 +218,6 @@ def build_sharded(system, kernel, config, ys_local: torch.Tensor, world: int, ra
 
             launch_moments(bufs, system.xs, system.qs, order, moments, meval)
             return
-        moments.fill_(float("nan"))
         meval.fill_(float("nan"))
         ShardedMoments(bufs, order, moments, meval, meval.shape[1], config.theta, world, rank,
                        group, cut_level).launch(system.xs, system.qs, ys_local, targets_sorted)

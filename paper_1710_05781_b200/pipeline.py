@@ -3,7 +3,7 @@
 One ``step`` is the whole hot path on inputs already in HBM:
     (a) prefix scan of q and the sign term e(y)      dt_prefix_scan, dt_sign_terms
     (b) tree build                                   dt_build_tree (cooperative)
-    (c) P2M / M2M moments                            dt_moments (cooperative)
+    (c) P2M / M2M moments                            dt_moments (prep + fused dataflow)
         interleave (x, q) for the traversal          dt_pack_sources
     (d)+(e) traversal, far + near field, += e(y)     dt_tree_eval_device
 All launches are stream-ordered and read sizes (node count, depth, level
@@ -50,7 +50,10 @@ class TreePipeline:
         self.order = moment_order_for(config)
         cap = node_capacity or initial_node_capacity(n, config.leaf_capacity)
         self.bufs = TreeBuffers(self.n, cap, self.dev)
-        self.moments = torch.empty((cap, self.order + 1), dtype=torch.float64, device=self.dev)
+        # the traversal rows are the only layout the step forms (order <= 31);
+        # higher orders also need the reference layout as the pass's input
+        self.moments = (torch.empty((cap, self.order + 1), dtype=torch.float64, device=self.dev)
+                        if self.order + 1 > 32 else None)
         self.estride = eval_stride(self.order)
         self.meval = torch.empty((cap, self.estride), dtype=torch.float64, device=self.dev)
         self.prefix = torch.empty(self.n, dtype=torch.float64, device=self.dev)

@@ -67,19 +67,34 @@ class Tree:
     end: torch.Tensor
     left: torch.Tensor
     right: torch.Tensor
-    moments: torch.Tensor
     moment_order: int
     depth: int
     leaf_count: int
     build_seconds: float
-    # device-side extras for the traversal kernel
+    # device-side extras for the traversal kernel: meval holds the moments in
+    # the traversal layout (dt_moments moments_eval), the only layout the
+    # upward pass writes for moment order <= 31
     meval: torch.Tensor = field(repr=False, default=None)
     packed: torch.Tensor = field(repr=False, default=None)
     xq: torch.Tensor = field(repr=False, default=None)
     meta: torch.Tensor = field(repr=False, default=None)
+    moments_ref: torch.Tensor | None = field(repr=False, default=None)
 
     def __len__(self) -> int:
         return int(self.lo.shape[0])
+
+    @property
+    def moments(self) -> torch.Tensor:
+        """m_k = sum q (x - c)^k / k!, [nodes, moment_order + 1] (tree.py:224-238),
+        derived from the traversal rows on first use (dt_moments_from_eval)."""
+        if self.moments_ref is None:
+            n, o1 = len(self), self.moment_order + 1
+            out = torch.empty((n, o1), dtype=torch.float64, device=self.meval.device)
+            _lib.check(_lib.load().dt_moments_from_eval(
+                _lib.ptr(self.meval), self.meval.shape[1], n, self.moment_order,
+                _lib.ptr(out), _lib.stream_handle()), "dt_moments_from_eval")
+            self.moments_ref = out
+        return self.moments_ref
 
     def node(self, index: int) -> "TreeNode":
         return TreeNode(self, index)
@@ -192,8 +207,10 @@ def eval_stride(order: int) -> int:
     return (order + 2) & ~1
 
 
-def launch_moments(bufs: TreeBuffers, xs, qs, order: int, moments: torch.Tensor,
-                   meval: torch.Tensor | None = None) -> None:
+def launch_moments(bufs: TreeBuffers, xs, qs, order: int, moments: torch.Tensor | None,
+                   meval: torch.Tensor) -> None:
+    """dt_moments: traversal rows into meval; for order > 31 (or when given)
+    the reference layout into moments as well."""
     L = _lib.load()
     p = _lib.ptr
     _lib.check(
@@ -231,7 +248,9 @@ def build(system: ChargeSystem, kernel: DiscKernel, config: EvalConfig) -> Tree:
 
 def _build(system: ChargeSystem, config: EvalConfig, upward) -> Tree:
     """Structure + moments; ``upward(bufs, order, moments, meval)`` replaces
-    the full upward pass when given (parallel.build_sharded)."""
+    the full upward pass when given (parallel.build_sharded).  For moment
+    order <= 31 only the traversal rows are formed (moments is None); the
+    reference layout is derived on first access of Tree.moments."""
     dev = _lib.require_device()
     torch.cuda.synchronize(dev)
     t0 = time.perf_counter()
@@ -246,7 +265,8 @@ def _build(system: ChargeSystem, config: EvalConfig, upward) -> Tree:
         cap *= 4
     n_nodes = int(meta[_lib.DT_META_NODES])
     order = moment_order_for(config)
-    moments = torch.empty((n_nodes, order + 1), dtype=torch.float64, device=dev)
+    moments = (torch.empty((n_nodes, order + 1), dtype=torch.float64, device=dev)
+               if order + 1 > 32 else None)
     meval = torch.empty((n_nodes, eval_stride(order)), dtype=torch.float64, device=dev)
     if upward is None:
         launch_moments(bufs, system.xs, system.qs, order, moments, meval)
@@ -260,9 +280,10 @@ def _build(system: ChargeSystem, config: EvalConfig, upward) -> Tree:
         lo=bufs.lo[:n_nodes], hi=bufs.hi[:n_nodes], center=bufs.center[:n_nodes],
         half=bufs.half[:n_nodes], level=bufs.level[:n_nodes], start=bufs.start[:n_nodes],
         end=bufs.end[:n_nodes], left=bufs.left[:n_nodes], right=bufs.right[:n_nodes],
-        moments=moments, moment_order=order, depth=int(meta[_lib.DT_META_DEPTH]),
+        moment_order=order, depth=int(meta[_lib.DT_META_DEPTH]),
         leaf_count=int(meta[_lib.DT_META_LEAVES]), build_seconds=elapsed,
         meval=meval, packed=bufs.packed[: n_nodes * 32], xq=xq, meta=bufs.meta,
+        moments_ref=moments,
     )
 
 

@@ -65,7 +65,7 @@ def test_version_and_errors_without_gpu():
                                   None) == -1
     assert b"order <= 31" in lib.dt_last_error()
     assert lib.dt_shard_rows_bytes(-1, 30, 32) == 0
-    assert lib.dt_shard_rows_bytes(4, 30, 32) == 16 * 63 * 8
+    assert lib.dt_shard_rows_bytes(4, 30, 32) == 16 * 32 * 8
 
 
 def test_order_limits_checked_before_device_work():

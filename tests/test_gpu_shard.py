@@ -77,7 +77,7 @@ def _simulate(dt, system, kernel, cfg, ys, world, cut_level=None, sorted_targets
         held.append(formed.mean())
         if i1 == i0:
             continue
-        tree_r = dataclasses.replace(full, moments=m[:n_nodes], meval=me[:n_nodes])
+        tree_r = dataclasses.replace(full, moments_ref=m[:n_nodes], meval=me[:n_nodes])
         got = torch.zeros(i1 - i0, dtype=torch.float64, device=ys.device)
         tree_phi_sum(tree_r, kernel, cfg, ys[i0:i1].contiguous(), got, accumulate=False)
         g = got.cpu().numpy()
