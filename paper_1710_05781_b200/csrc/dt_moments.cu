@@ -32,6 +32,9 @@
 #include "dt_common.cuh"
 #include "dt_farcoef.cuh"
 
+#ifndef DT_P2M_PREFETCH
+#define DT_P2M_PREFETCH 1
+#endif
 #ifndef DT_P2M_G
 #define DT_P2M_G 2
 #endif
@@ -53,6 +56,7 @@ struct MomArgs {
     int32_t *parent;   // workspace: parent index per node (-1 at the root)
     int32_t *arrived;  // workspace: finished children per node
     const int64_t *plan;  // optional shard plan (DT_PLAN_*): restrict to this rank's subtrees
+    unsigned *chunk_ctr;  // workspace: upward_kernel's chunk counter (zeroed by the prep kernel)
 };
 
 __constant__ double c_inv_k[MAX_ORDER1] = {  // 1/k rounded to nearest (k >= 1)
@@ -195,6 +199,8 @@ __global__ void moments_prep_kernel(MomArgs a)
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
         a.arrived[i] = 0;
+        if (i == 0 && a.chunk_ctr)
+            *a.chunk_ctr = 0u;
         const int64_t l = __ldg(a.left + i), r = __ldg(a.right + i);
         if (l >= 0)
             a.parent[l] = (int32_t)i;
@@ -300,11 +306,43 @@ __device__ __forceinline__ void p2m_split_leaf(const MomArgs &a, int64_t node, b
     for (int k = 0; k < KMAX; ++k)
         acc[k] = 0.0;
     int64_t j = s + sub;
+#if DT_P2M_PREFETCH
+    // the next pair's loads are issued before this pair's arithmetic
+    bool have = j + G < e;
+    double cx0 = 0.0, cx1 = 0.0, cq0 = 0.0, cq1 = 0.0;
+    if (have) {
+        cx0 = __ldg(a.xs + j);
+        cx1 = __ldg(a.xs + j + G);
+        cq0 = __ldg(a.qs + j);
+        cq1 = __ldg(a.qs + j + G);
+    }
+    while (have) {
+        const int64_t jn = j + 2 * G;
+        const bool hn = jn + G < e;
+        double nx0 = 0.0, nx1 = 0.0, nq0 = 0.0, nq1 = 0.0;
+        if (hn) {
+            nx0 = __ldg(a.xs + jn);
+            nx1 = __ldg(a.xs + jn + G);
+            nq0 = __ldg(a.qs + jn);
+            nq1 = __ldg(a.qs + jn + G);
+        }
+        const double t0 = cx0 - c, t1 = cx1 - c;
+        double p0[8], p1[8];
+        p0[0] = cq0;
+        p1[0] = cq1;
+        cx0 = nx0;
+        cx1 = nx1;
+        cq0 = nq0;
+        cq1 = nq1;
+        j = jn;
+        have = hn;
+#else
     for (; j + G < e; j += 2 * G) {
         const double t0 = __ldg(a.xs + j) - c, t1 = __ldg(a.xs + j + G) - c;
         double p0[8], p1[8];
         p0[0] = __ldg(a.qs + j);
         p1[0] = __ldg(a.qs + j + G);
+#endif
 #pragma unroll
         for (int r = 1; r < 8; ++r) {
             p0[r] = p0[r - 1] * t0;
@@ -497,6 +535,8 @@ template <int G, int KMAX>
 __global__ void __launch_bounds__(256, DT_UP_MINB) upward_kernel(MomArgs a)
 {
     __shared__ double rho_s[REG_ORDER];
+    __shared__ int64_t frontier_s[8][32];
+    const int warp = threadIdx.x >> 5;
     if (threadIdx.x < REG_ORDER)
         rho_s[threadIdx.x] = c_mev_rho[threadIdx.x];
     __syncthreads();
@@ -509,9 +549,15 @@ __global__ void __launch_bounds__(256, DT_UP_MINB) upward_kernel(MomArgs a)
         lo = __ldg(a.plan + DT_PLAN_SRC_LO);
         hi = __ldg(a.plan + DT_PLAN_SRC_HI);
     }
-    const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t r0 = gwarp * 32; r0 < n; r0 += nwarps * 32) {
+    // chunks are taken from a counter: a warp busy climbing does not hold
+    // back the leaves of the chunks after it
+    while (true) {
+        unsigned chunk = 0;
+        if (lane == 0)
+            chunk = atomicAdd(a.chunk_ctr, 1u);
+        const int64_t r0 = (int64_t)__shfl_sync(DT_FULL, chunk, 0) * 32;
+        if (r0 >= n)
+            break;
         const int64_t c0 = n - 32 - r0;  // may be negative for the last chunk
         const int64_t mine = c0 + lane;
         bool form = false, climb = false;
@@ -539,54 +585,56 @@ __global__ void __launch_bounds__(256, DT_UP_MINB) upward_kernel(MomArgs a)
                 leaves &= leaves - 1;
             p2m_split_leaf<G, KMAX>(a, node, active, sub);
         }
-        __syncwarp();  // the rows precede the releasing arrivals
-        bool done = false;
-        if (climb) {
-            const int need = (__ldg(a.left + par) >= 0) + (__ldg(a.right + par) >= 0);
-            done = arrive_acq_rel(a.arrived + par) == need - 1;
-        }
-        if (!done)
-            par = -1;
+        // Climb in rounds over a frontier of formed nodes, kept sorted and
+        // compacted in the lanes, so siblings sit in adjacent lanes: a pair of
+        // siblings (or an only child) completes its parent locally, with no
+        // atomic; a node whose sibling is outside the frontier arrives at the
+        // parent's counter (release) and keeps the parent if it is last.
+        // Then the kept parents are formed, four per call (eight lanes each)
+        // or one on the whole warp, and become the next frontier.
+        int64_t v = climb ? mine : -1;
         while (true) {
-            const unsigned todo = __ballot_sync(DT_FULL, par >= 0);
-            if (!todo)
+            __syncwarp();  // this warp's rows precede the loads and releasing arrivals
+            const unsigned fr = __ballot_sync(DT_FULL, v >= 0);
+            if (!fr)
                 break;
-            unsigned sel;
-            if (__popc(todo) == 1) {
-                // a lone parent (the usual case high in a chain): all 32 lanes
-                sel = todo;
-                __syncwarp();
-                up_form_warp(a, __shfl_sync(DT_FULL, par, __ffs(todo) - 1), rho_s);
+            const int rank = __popc(fr & ((1u << lane) - 1u));
+            if (v >= 0)
+                frontier_s[warp][rank] = v;
+            __syncwarp();
+            const int cnt = __popc(fr);
+            v = lane < cnt ? frontier_s[warp][lane] : -1;
+            int64_t p = -1;
+            if (v >= 0) {
+                p = __ldg(a.parent + v);
+                if (p < cut_begin)
+                    p = -1;
+            }
+            const int64_t p_up = __shfl_up_sync(DT_FULL, p, 1);
+            const int64_t p_dn = __shfl_down_sync(DT_FULL, p, 1);
+            const bool pair_hi = p >= 0 && lane > 0 && p_up == p;  // the lane below takes p
+            const bool pair_lo = p >= 0 && lane < 31 && p_dn == p;
+            bool take = false;
+            if (p >= 0 && !pair_hi) {
+                const int need = (__ldg(a.left + p) >= 0) + (__ldg(a.right + p) >= 0);
+                take = pair_lo || need == 1 || arrive_acq_rel(a.arrived + p) == need - 1;
+            }
+            const unsigned tk = __ballot_sync(DT_FULL, take);
+            if (!tk)
+                break;
+            if (take)
+                frontier_s[warp][__popc(tk & ((1u << lane) - 1u))] = p;
+            __syncwarp();  // the acquires and the parent list precede the loads
+            const int np = __popc(tk);
+            if (np == 1) {
+                up_form_warp(a, frontier_s[warp][0], rho_s);
             } else {
-                unsigned t = todo;
-                int64_t mine_p = -1;
-                sel = 0;
-#pragma unroll
-                for (int g = 0; g < 4; ++g) {
-                    int64_t pg = -1;
-                    if (t) {
-                        const int src = __ffs(t) - 1;
-                        t &= t - 1;
-                        sel |= 1u << src;
-                        pg = __shfl_sync(DT_FULL, par, src);
-                    }
-                    if ((lane >> 3) == g)
-                        mine_p = pg;
+                for (int c = 0; c < np; c += 4) {
+                    const int gi = c + (lane >> 3);
+                    up_form_group8(a, gi < np ? frontier_s[warp][gi] : -1, rho_s);
                 }
-                __syncwarp();  // the completing lanes' acquires precede the loads
-                up_form_group8(a, mine_p, rho_s);
             }
-            __syncwarp();  // the stores precede the releasing arrivals
-            if ((sel >> lane) & 1u) {
-                const int64_t q = __ldcg(a.parent + par);
-                int64_t nxt = -1;
-                if (q >= cut_begin && q >= 0) {
-                    const int need = (__ldg(a.left + q) >= 0) + (__ldg(a.right + q) >= 0);
-                    if (arrive_acq_rel(a.arrived + q) == need - 1)
-                        nxt = q;
-                }
-                par = nxt;
-            }
+            v = lane < np ? frontier_s[warp][lane] : -1;
         }
     }
 }
@@ -796,14 +844,16 @@ __global__ void __launch_bounds__(256) shard_finish_kernel(MomArgs a, int world,
 }
 
 // Upward pass for order + 1 <= 32 (honouring a.plan): the parent/arrival
-// bookkeeping, then the fused P2M + M2M dataflow kernel.  Level-synchronous
-// M2M variants (grid barrier per level, one launch per level) measured
-// slower in round 1 (0.47-0.95 ms against 0.36 ms at configs[2]): a grid
-// barrier costs ~5 us and the tree is 32 levels deep.
+// bookkeeping (which also zeroes the chunk counter), then the fused P2M +
+// M2M dataflow kernel.  A level-synchronous cooperative variant (P2M, grid
+// barrier, levels bottom-up two lanes per node, sparse levels in one block)
+// measured 0.43-0.55 ms at configs[2] against 0.30 ms for this one: a level
+// costs >= 2.6 us of formation latency plus ~5 us per grid barrier, and the
+// tree is 32 levels deep.
 int launch_level_moments(MomArgs &a, cudaStream_t s)
 {
     const int sms = dt_num_sms();
-    if (!a.parent)
+    if (!a.parent || !a.chunk_ctr)
         return dt_set_error(DT_ERR_WORKSPACE, "moments workspace missing");
     if (!a.meval)
         return dt_set_error(DT_ERR_INVALID, "order <= 31 needs the traversal rows (moments_eval)");
@@ -832,7 +882,7 @@ int launch_level_moments(MomArgs &a, cudaStream_t s)
 
 extern "C" size_t dt_moments_workspace(int64_t node_capacity)
 {
-    return (size_t)node_capacity * 2 * sizeof(int32_t) + 256;
+    return (size_t)node_capacity * 2 * sizeof(int32_t) + 1024;
 }
 
 extern "C" int dt_moments(const double *xs, const double *qs, const double *center,
@@ -853,7 +903,8 @@ extern "C" int dt_moments(const double *xs, const double *qs, const double *cent
     if (!workspace || workspace_bytes < dt_moments_workspace(node_capacity))
         return dt_set_error(DT_ERR_WORKSPACE, "moments workspace too small");
     MomArgs a{xs, qs, center, start, end, left, right, meta, order, moments, moments_eval,
-              eval_stride, (int32_t *)workspace, (int32_t *)workspace + node_capacity, nullptr};
+              eval_stride, (int32_t *)workspace, (int32_t *)workspace + node_capacity, nullptr,
+              (unsigned *)((int32_t *)workspace + 2 * node_capacity)};
     cudaStream_t s = (cudaStream_t)stream;
     const int sms = dt_num_sms();
     if (order + 1 <= REG_ORDER)
@@ -927,7 +978,8 @@ extern "C" int dt_moments_partial(const double *xs, const double *qs, const doub
     // the reference layout (moments) is derived by dt_shard_finish, once every row exists
     (void)moments;
     MomArgs a{xs, qs, center, start, end, left, right, meta, order, nullptr, moments_eval,
-              eval_stride, (int32_t *)workspace, (int32_t *)workspace + node_capacity, plan};
+              eval_stride, (int32_t *)workspace, (int32_t *)workspace + node_capacity, plan,
+              (unsigned *)((int32_t *)workspace + 2 * node_capacity)};
     return launch_level_moments(a, (cudaStream_t)stream);
 }
 
