@@ -2,10 +2,16 @@
 //
 // Reference: charges.py:130 (prefix = np.cumsum(qs), sequential) and
 // charges.py:183-187 (_sign_terms).  The scan is a fixed-shape reduction
-// tree (tile sums -> one-block scan of tile sums -> tile scans), so repeated
-// calls are bit-identical; it differs from the sequential cumsum by
-// round-off (<= ~1e-15 * sum|q| at 2^24).  HBM traffic: 8N (tile sums) +
-// 16N (scan pass) + 16T (sign terms).
+// tree (tile sums and group sums of 64 tiles -> tile scans offset by the
+// group and tile sums below them, the second pass in reverse tile order so
+// most of its reads of q hit L2), so repeated calls
+// are bit-identical; it differs from the sequential cumsum by round-off
+// (<= ~1e-15 * sum|q| at 2^24).  Algorithmic HBM traffic 16N (read q, write
+// prefix) + 16T (sign terms).  A single-pass variant (tile sums published
+// and summed in a fixed order by every later tile, no look-back) measured
+// 97 us against 79 us for the earlier three passes: its tiles wait on their
+// predecessors while holding their SM slots; a decoupled look-back would
+// make the last bits depend on timing.
 #include <algorithm>
 
 #include "dt_common.cuh"
@@ -15,45 +21,21 @@ namespace {
 constexpr int SCAN_THREADS = 256;
 constexpr int SCAN_ITEMS = 16;
 constexpr int SCAN_TILE = SCAN_THREADS * SCAN_ITEMS;  // 4096 elements
-constexpr int PARTIAL_THREADS = 1024;
 
-// Block-wide inclusive scan of one double per thread; returns the block total.
-__device__ double block_inclusive_scan(double v, double *warp_tot)
-{
-    const int lane = dt_lane(), warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        double t = __shfl_up_sync(DT_FULL, v, o);
-        if (lane >= o)
-            v += t;
-    }
-    if (lane == 31)
-        warp_tot[warp] = v;
-    __syncthreads();
-    if (warp == 0) {
-        double w = lane < nw ? warp_tot[lane] : 0.0;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            double t = __shfl_up_sync(DT_FULL, w, o);
-            if (lane >= o)
-                w += t;
-        }
-        if (lane < nw)
-            warp_tot[lane] = w;  // inclusive over warps
-    }
-    __syncthreads();
-    if (warp > 0)
-        v += warp_tot[warp - 1];
-    __syncthreads();
-    return v;
-}
+constexpr int SCAN_GROUP = 64;  // tiles per group sum
 
-// Pass 1: per-tile sums, coalesced (thread t sums elements t, t+256, ...).
+// Pass 1: per-tile sums A_t, coalesced (thread t sums elements t, t+256,
+// ...), fixed-order block reduction.  The last tile of a group of 64 to
+// finish (arrival counter) also forms the group sum B_g = A_(64g) + ... in
+// index order, so pass 2 needs no separate scan of the tile sums.
 __global__ void __launch_bounds__(SCAN_THREADS) tile_sums_kernel(const double *__restrict__ q,
-                                                                 int64_t n,
-                                                                 double *__restrict__ tile_sum)
+                                                                 int64_t n, int64_t n_tiles,
+                                                                 double *tile_sum,
+                                                                 double *group_sum,
+                                                                 unsigned *group_ctr)
 {
     __shared__ double wt[SCAN_THREADS / 32];
+    __shared__ bool last_s;
     const int64_t base = (int64_t)blockIdx.x * SCAN_TILE + threadIdx.x;
     double s = 0.0;
 #pragma unroll
@@ -67,55 +49,54 @@ __global__ void __launch_bounds__(SCAN_THREADS) tile_sums_kernel(const double *_
     if (dt_lane() == 0)
         wt[threadIdx.x >> 5] = s;
     __syncthreads();
+    const int64_t g = blockIdx.x / SCAN_GROUP, g0 = g * SCAN_GROUP;
+    const int64_t g1 = min(n_tiles, g0 + SCAN_GROUP);
     if (threadIdx.x == 0) {
         double t = 0.0;
         for (int w = 0; w < SCAN_THREADS / 32; ++w)
             t += wt[w];
         tile_sum[blockIdx.x] = t;
+        __threadfence();  // the sum precedes the arrival
+        last_s = atomicAdd(group_ctr + g, 1u) == (unsigned)(g1 - g0 - 1);
+    }
+    __syncthreads();
+    if (last_s && threadIdx.x < 32) {
+        __threadfence();  // every arrival's sum is visible after ours
+        double b = 0.0;
+        for (int64_t i = g0 + threadIdx.x; i < g1; i += 32)
+            b += __ldcg(tile_sum + i);
+        b = dt_warp_sum(b);
+        if (threadIdx.x == 0)
+            group_sum[g] = b;
     }
 }
 
-// Pass 2: exclusive scan of the tile sums in one block (sequential chunks per
-// thread, then a block scan of the chunk totals).
-__global__ void __launch_bounds__(PARTIAL_THREADS) tile_scan_kernel(double *__restrict__ tile_sum,
-                                                                    int64_t n_tiles)
-{
-    __shared__ double wt[PARTIAL_THREADS / 32];
-    const int64_t per = (n_tiles + PARTIAL_THREADS - 1) / PARTIAL_THREADS;
-    const int64_t b0 = (int64_t)threadIdx.x * per;
-    double s = 0.0;
-    for (int64_t i = 0; i < per; ++i)
-        if (b0 + i < n_tiles)
-            s += tile_sum[b0 + i];
-    double incl = block_inclusive_scan(s, wt);
-    double run = incl - s;  // exclusive offset of this thread's chunk
-    // recompute exclusive prefix sequentially within the chunk
-    for (int64_t i = 0; i < per; ++i) {
-        int64_t b = b0 + i;
-        if (b < n_tiles) {
-            double v = tile_sum[b];
-            tile_sum[b] = run;
-            run += v;
-        }
-    }
-}
-
-// Pass 3: scan each tile with its exclusive offset.  Warp w owns 512
+// Pass 2: scan each tile with its exclusive offset.  Warp w owns 512
 // consecutive elements, read/written coalesced in 16 rows of 32; each row is
 // a warp shuffle scan carried across rows, then warps are offset in order.
-__global__ void __launch_bounds__(SCAN_THREADS) tile_apply_kernel(const double *__restrict__ q,
+// Tiles run in reverse order: pass 1 left the last ~100 MB of q in L2 (126 MB),
+// so most of this pass's reads hit L2 instead of HBM; q is read with an
+// evict-first hint and prefix written with streaming stores so they do not
+// push the rest of q out.
+#ifndef DT_SCAN_MINB
+#define DT_SCAN_MINB 4  // 64 registers: 78 us against 91 us at 82 registers (configs[2])
+#endif
+__global__ void __launch_bounds__(SCAN_THREADS, DT_SCAN_MINB) tile_apply_kernel(const double *__restrict__ q,
                                                                   int64_t n,
-                                                                  const double *__restrict__ tile_off,
+                                                                  const double *__restrict__ tile_sum,
+                                                                  const double *__restrict__ group_sum,
                                                                   double *__restrict__ prefix)
 {
     __shared__ double wt[SCAN_THREADS / 32];
+    __shared__ double part_s[2];
     const int lane = dt_lane(), warp = threadIdx.x >> 5;
-    const int64_t base = (int64_t)blockIdx.x * SCAN_TILE + (int64_t)warp * (32 * SCAN_ITEMS) + lane;
+    const int64_t tile = (int64_t)gridDim.x - 1 - blockIdx.x;
+    const int64_t base = tile * SCAN_TILE + (int64_t)warp * (32 * SCAN_ITEMS) + lane;
     double v[SCAN_ITEMS];
 #pragma unroll
     for (int i = 0; i < SCAN_ITEMS; ++i) {
         const int64_t j = base + 32 * i;
-        v[i] = j < n ? __ldg(q + j) : 0.0;
+        v[i] = j < n ? __ldcs(q + j) : 0.0;
     }
     double carry = 0.0;
 #pragma unroll
@@ -133,15 +114,31 @@ __global__ void __launch_bounds__(SCAN_THREADS) tile_apply_kernel(const double *
     }
     if (lane == 31)
         wt[warp] = carry;
+    // exclusive offset (B_0 + .. + B_(G-1)) + (A_(64G) + .. + A_(t-1)), each
+    // a fixed-order warp reduction (identical on every call)
+    const int64_t g = tile / SCAN_GROUP;
+    if (warp < 2) {
+        double a = 0.0;
+        if (warp == 0) {
+            for (int64_t i = lane; i < g; i += 32)
+                a += __ldg(group_sum + i);
+        } else {
+            for (int64_t i = g * SCAN_GROUP + lane; i < tile; i += 32)
+                a += __ldg(tile_sum + i);
+        }
+        a = dt_warp_sum(a);
+        if (lane == 0)
+            part_s[warp] = a;
+    }
     __syncthreads();
-    double off = tile_off[blockIdx.x];
+    double off = part_s[0] + part_s[1];
     for (int w = 0; w < warp; ++w)
         off += wt[w];
 #pragma unroll
     for (int i = 0; i < SCAN_ITEMS; ++i) {
         const int64_t j = base + 32 * i;
         if (j < n)
-            prefix[j] = off + v[i];
+            __stcs(prefix + j, off + v[i]);
     }
 }
 
@@ -236,10 +233,12 @@ __global__ void __launch_bounds__(SIGN_THREADS) sign_terms_kernel(
 
 }  // namespace
 
+// Workspace: tile sums, group sums (8 bytes each), group arrival counters.
 extern "C" size_t dt_prefix_scan_workspace(int64_t n)
 {
-    int64_t tiles = (n + SCAN_TILE - 1) / SCAN_TILE;
-    return (size_t)(tiles > 0 ? tiles : 1) * sizeof(double);
+    const int64_t tiles = n > 0 ? (n + SCAN_TILE - 1) / SCAN_TILE : 1;
+    const int64_t groups = (tiles + SCAN_GROUP - 1) / SCAN_GROUP;
+    return (size_t)(tiles + groups) * sizeof(double) + (size_t)groups * sizeof(unsigned);
 }
 
 extern "C" int dt_prefix_scan(const double *qs, double *prefix, int64_t n, void *workspace,
@@ -251,12 +250,16 @@ extern "C" int dt_prefix_scan(const double *qs, double *prefix, int64_t n, void 
     DT_CHECK_ARG(qs && prefix, "null pointer");
     if (workspace_bytes < dt_prefix_scan_workspace(n) || !workspace)
         return dt_set_error(DT_ERR_WORKSPACE, "prefix scan workspace too small");
+    DT_CHECK_ARG(((uintptr_t)workspace & 7) == 0, "scan workspace must be 8-byte aligned");
     cudaStream_t s = (cudaStream_t)stream;
-    int64_t tiles = (n + SCAN_TILE - 1) / SCAN_TILE;
-    double *tsum = (double *)workspace;
-    tile_sums_kernel<<<(unsigned)tiles, SCAN_THREADS, 0, s>>>(qs, n, tsum);
-    tile_scan_kernel<<<1, PARTIAL_THREADS, 0, s>>>(tsum, tiles);
-    tile_apply_kernel<<<(unsigned)tiles, SCAN_THREADS, 0, s>>>(qs, n, tsum, prefix);
+    const int64_t tiles = (n + SCAN_TILE - 1) / SCAN_TILE;
+    DT_CHECK_ARG(tiles < ((int64_t)1 << 31), "too many values");
+    const int64_t groups = (tiles + SCAN_GROUP - 1) / SCAN_GROUP;
+    double *tsum = (double *)workspace, *gsum = tsum + tiles;
+    unsigned *gctr = (unsigned *)(gsum + groups);
+    DT_CUDA_TRY(cudaMemsetAsync(gctr, 0, (size_t)groups * sizeof(unsigned), s));
+    tile_sums_kernel<<<(unsigned)tiles, SCAN_THREADS, 0, s>>>(qs, n, tiles, tsum, gsum, gctr);
+    tile_apply_kernel<<<(unsigned)tiles, SCAN_THREADS, 0, s>>>(qs, n, tsum, gsum, prefix);
     DT_CUDA_TRY(cudaGetLastError());
     return DT_OK;
 }
