@@ -151,6 +151,17 @@ def ncu_traffic():
 
 
 # ------------------------------------------------------------------ CPU oracle
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def cpu_reference_rate(w, seconds: float, threads: int | None = None):
     """Reference algorithm (oracle/ C restatement) on the host cores: full
     build + a strided target sample sized to ~`seconds`, extrapolated to all
@@ -179,7 +190,7 @@ def cpu_reference_rate(w, seconds: float, threads: int | None = None):
     t_eval = time.perf_counter() - t0
     t_full = t_build + t_eval * T / len(sample)
     info = {
-        "cores": cores,
+        "cores": cores, "cpu_model": cpu_model(), "host_threads": os.cpu_count(),
         "sample": f"full build ({len(tree)} nodes, {t_build:.2f} s) + every {stride}-th target "
                   f"({len(sample)} of {T}, {t_eval:.2f} s), eval extrapolated to all targets",
         "build_s": t_build, "eval_sample_s": t_eval, "n_sample": len(sample),
@@ -214,7 +225,7 @@ def run_reference(args):
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": config_dict(w, 1),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": info["cores"], "kind": "port",
-                         "sample": info["sample"]},
+                         "sample": info["sample"], "cpu_model": info["cpu_model"]},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -241,9 +252,17 @@ def run_ours(args):
         # multi-rank code path with several ranks on one GPU (no timing value)
         backend = os.environ.get("DISCTREE_BENCH_BACKEND", "nccl")
         if backend == "nccl":
+            # communicator init lines (nranks, NVLS/NVLink transport) on stderr
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+            os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
             dist.init_process_group(backend)
+        nccl_info = {"backend": dist.get_backend(), "world_size": dist.get_world_size(),
+                     "nccl_version": ".".join(map(str, torch.cuda.nccl.version()))}
+        if rank == 0:
+            print(f"[bench] process group {nccl_info}", file=sys.stderr, flush=True)
 
     def barrier():
         if world > 1:
@@ -383,10 +402,13 @@ def run_ours(args):
                          "flops_all_ranks": flops_all},
         "check": {"max_abs_diff_vs_api_over_sum_abs_q": diff / scale},
     }
+    if world > 1:
+        line["process_group"] = nccl_info
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         rate, info = cpu_reference_rate(w, args.cpu_seconds)
         line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": info["cores"],
-                                "kind": "port", "sample": info["sample"]}
+                                "kind": "port", "sample": info["sample"],
+                                "cpu_model": info["cpu_model"]}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:

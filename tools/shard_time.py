@@ -19,7 +19,6 @@ bufs = TreeBuffers(len(xs), initial_node_capacity(len(xs), 64), xs.device)
 bufs.launch(xs, 64)
 order = moment_order_for(cfg)
 es = eval_stride(order)
-m = torch.empty((bufs.capacity, order + 1), dtype=torch.float64, device="cuda")
 me = torch.empty((bufs.capacity, es), dtype=torch.float64, device="cuda")
 
 
@@ -35,11 +34,11 @@ def timeit(fn, reps=5):
     return min(ts[1:])
 
 
-print("full moments ms %.3f" % timeit(lambda: launch_moments(bufs, xs, qs, order, m, me)))
+print("full moments ms %.3f" % timeit(lambda: launch_moments(bufs, xs, qs, order, None, me)))
 for G in (2, 4, 8):
     for r in (0, G // 2, G - 1):
         i0, i1 = shard_bounds(len(ys), G, r)
-        sh = ShardedMoments(bufs, order, m, me, es, cfg.theta, G, r)
+        sh = ShardedMoments(bufs, order, None, me, es, cfg.theta, G, r)
         yr = ys[i0:i1]
 
         def go():
