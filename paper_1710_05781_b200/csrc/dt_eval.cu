@@ -422,13 +422,77 @@ __device__ __forceinline__ int pt_level(int hi0, double h)
     return (hi0 - __double2hiint(h) + 0x80000) >> 20;
 }
 
+// The breakpoints depend only on the inputs below; they are kept in the
+// workspace slot with this key and rebuilt only when it changes (the
+// regula falsi is ~45 us; a device-resident step repeats the same tree
+// depth, root half-width, r_d, tolerance and tables).
+struct PtKey {
+    unsigned long long magic, h0, rd2, tol, theta, tables;
+    long long p_cap, used_depth, n_samples;
+    unsigned long long bp_hash;  // the breakpoint table's content (the slot may be reused)
+};
+constexpr int PT_BP_WORDS = 2 * PT_LEVELS * PT_N + PT_LEVELS;
+
+// Order-independent 64-bit hash of the breakpoint table, by the whole block.
+__device__ unsigned long long pt_bp_hash(const double *bp)
+{
+    __shared__ unsigned long long part_s[32];
+    unsigned long long h = 0;
+    for (int i = threadIdx.x; i < PT_BP_WORDS; i += blockDim.x) {
+        unsigned long long z = (unsigned long long)__double_as_longlong(__ldcg(bp + i)) +
+                               0x9e3779b97f4a7c15ull * (unsigned long long)(i + 1);
+        z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+        z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+        h += z ^ (z >> 31);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+        h += __shfl_xor_sync(DT_FULL, h, o);
+    if (dt_lane() == 0)
+        part_s[threadIdx.x >> 5] = h;
+    __syncthreads();
+    unsigned long long t = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w)
+        t += part_s[w];
+    __syncthreads();
+    return t;
+}
+constexpr unsigned long long PT_KEY_MAGIC = 0x6474707472656531ull;
+
+__device__ PtKey pt_key_of(const EvalArgs &a)
+{
+    PtKey k;
+    k.magic = PT_KEY_MAGIC;
+    k.h0 = (unsigned long long)__double_as_longlong(__ldg(&a.nodes[0].half));
+    k.rd2 = (unsigned long long)__double_as_longlong(a.rd2);
+    k.tol = (unsigned long long)__double_as_longlong(a.meta ? tol_share_of(a) : a.tol_share);
+    k.theta = (unsigned long long)__double_as_longlong(a.theta);
+    unsigned long long f = 0x9e3779b97f4a7c15ull;  // fingerprint of the contour tables
+    for (int t = 0; t < a.n_samples; ++t) {
+        f = (f ^ (unsigned long long)__double_as_longlong(__ldg(a.cos_tab + t))) * 0x100000001b3ull;
+        f = (f ^ (unsigned long long)__double_as_longlong(__ldg(a.sin_tab + t))) * 0x100000001b3ull;
+    }
+    k.tables = f;
+    k.p_cap = a.p_cap;
+    k.used_depth = a.meta ? __ldg(a.meta + DT_META_DEPTH) : -1;
+    k.n_samples = a.n_samples;
+    return k;
+}
+
+__device__ __forceinline__ bool pt_key_equal(const PtKey &x, const PtKey &y)
+{
+    return x.magic == y.magic && x.h0 == y.h0 && x.rd2 == y.rd2 && x.tol == y.tol &&
+           x.theta == y.theta && x.tables == y.tables && x.p_cap == y.p_cap &&
+           x.used_depth == y.used_depth && x.n_samples == y.n_samples && x.bp_hash == y.bp_hash;
+}
+
 // bp[L][n] = b_n for h_L: the R with V_n(R) = tol_share (h_L / theta if V_n
 // <= tol there already, +inf if never); 0 for n >= p_cap (the reference's
 // loop stops there).  One warp per entry.  First, a grid-stride scan of the
 // nodes sets bad[L] for every level L = pt_level(h) holding a node with
 // |h - h_L| > PT_DH h_L (or lying below the tree's depth, where no
 // breakpoints are computed); bad[] is zeroed by the caller.
-__global__ void psel_breakpoints_kernel(EvalArgs a, double *bp, unsigned *bad)
+__global__ void psel_breakpoints_kernel(EvalArgs a, double *bp, unsigned *bad, const PtKey *key)
 {
     {
         const double h0 = __ldg(&a.nodes[0].half);
@@ -443,6 +507,19 @@ __global__ void psel_breakpoints_kernel(EvalArgs a, double *bp, unsigned *bad)
                 (L > dep || !(fabs(h - ldexp(h0, -L)) <= PT_DH * ldexp(h0, -L))))
                 atomicOr(bad + L, 1u);
         }
+    }
+    {
+        // tables from an earlier call with the same key are still valid
+        __shared__ int same_s;
+        const unsigned long long hbp = pt_bp_hash(bp);
+        if (threadIdx.x == 0) {
+            PtKey cur = pt_key_of(a);
+            cur.bp_hash = hbp;
+            same_s = pt_key_equal(cur, *key);
+        }
+        __syncthreads();
+        if (same_s)
+            return;
     }
     const int id = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     if (id >= PT_LEVELS * PT_N)
@@ -546,9 +623,17 @@ __device__ unsigned char psel_bin_interval(const EvalArgs &a, double rlo, double
 // bins[L][j]: the order of bin j, PT_SPLIT | m for a bin holding b_m only,
 // PT_FALLBACK otherwise
 __global__ void psel_bins_kernel(EvalArgs a, const double *bp, const unsigned *bad,
-                                 unsigned char *bins)
+                                 unsigned char *bins, PtKey *key)
 {
     const int id = blockIdx.x * blockDim.x + threadIdx.x;
+    if (blockIdx.x == 0) {  // the breakpoints now match this key (stream order)
+        const unsigned long long hbp = pt_bp_hash(bp);
+        if (threadIdx.x == 0) {
+            PtKey k = pt_key_of(a);
+            k.bp_hash = hbp;
+            *key = k;
+        }
+    }
     if (id >= PT_LEVELS * PT_BINS)
         return;
     const int L = id / PT_BINS, j = id % PT_BINS;
@@ -597,6 +682,9 @@ static_assert(DT_EVAL_SEGMENTS * 4 <= PT_BAD_OFFSET && PT_BAD_OFFSET + 4 * PT_LE
               "counter slot layout");
 static_assert(PT_BP_OFFSET + sizeof(double) * (2 * PT_LEVELS * PT_N + PT_LEVELS) <= PT_BINS_OFFSET,
               "breakpoint table overlaps the bins");
+constexpr size_t PT_KEY_OFFSET = PT_BINS_OFFSET + PT_LEVELS * PT_BINS;
+static_assert(PT_KEY_OFFSET % 8 == 0 && PT_KEY_OFFSET + sizeof(PtKey) <= DT_EVAL_COUNTER_BYTES,
+              "key slot");
 static_assert(PT_BINS_OFFSET + PT_LEVELS * PT_BINS <= DT_EVAL_COUNTER_BYTES,
               "order tables exceed the workspace slot");
 
@@ -1182,8 +1270,10 @@ int launch_eval(EvalArgs &a, bool adaptive, bool stats, cudaStream_t s)
         double *bp = reinterpret_cast<double *>(reinterpret_cast<char *>(a.counter) + PT_BP_OFFSET);
         unsigned char *bins = reinterpret_cast<unsigned char *>(a.counter) + PT_BINS_OFFSET;
         unsigned *bad = reinterpret_cast<unsigned *>(reinterpret_cast<char *>(a.counter) + PT_BAD_OFFSET);
-        psel_breakpoints_kernel<<<(PT_LEVELS * PT_N * 32 + 255) / 256, 256, 0, s>>>(a, bp, bad);
-        psel_bins_kernel<<<(PT_LEVELS * PT_BINS + 255) / 256, 256, 0, s>>>(a, bp, bad, bins);
+        PtKey *key = reinterpret_cast<PtKey *>(reinterpret_cast<char *>(a.counter) + PT_KEY_OFFSET);
+        psel_breakpoints_kernel<<<(PT_LEVELS * PT_N * 32 + 255) / 256, 256, 0, s>>>(a, bp, bad,
+                                                                                   key);
+        psel_bins_kernel<<<(PT_LEVELS * PT_BINS + 255) / 256, 256, 0, s>>>(a, bp, bad, bins, key);
         DT_CUDA_TRY(cudaGetLastError());
         a.pt_bp = bp;
         a.pt_bins = bins;
