@@ -50,6 +50,8 @@ struct BuildArgs {
     int64_t *block_total;    // [gridDim]
     int64_t *dy_split;       // [DYADIC] global lower_bound of each top dyadic midpoint
     double *dy_mid;          // [DYADIC] that midpoint
+    int k_top;               // levels 0..k_top built in one pass (0: level by level)
+    unsigned *irregular;     // set if some top dyadic interval has mid not strictly inside
 };
 
 // Splits of the top dyadic levels, all at once.  The bisection intervals do
@@ -60,7 +62,7 @@ struct BuildArgs {
 // levels 0..K are found by independent searches in one parallel phase
 // instead of K + 1 dependent rounds of DRAM-latency binary searches.
 #ifndef DT_DYADIC_LEVELS
-#define DT_DYADIC_LEVELS 16  // 12: 0.398 ms, 14: 0.383, 16: 0.370, 18: 0.368, 20: 0.408 (configs[2])
+#define DT_DYADIC_LEVELS 18  // with the one-pass top: 16: 0.254 ms, 18: 0.248, 20: 0.384 (configs[2])
 #endif
 constexpr int DYADIC_LEVELS = DT_DYADIC_LEVELS;  // levels 0..DYADIC_LEVELS-1
 constexpr int DYADIC = (1 << DYADIC_LEVELS) - 1;
@@ -132,6 +134,8 @@ __device__ void dyadic_splits(const BuildArgs &a)
         const double mid = mid_of(lo, hi);
         a.dy_mid[idx] = mid;
         a.dy_split[idx] = dt_lower_bound(a.xs, 0, a.n, mid);
+        if (!(lo < mid && mid < hi))  // degenerate interval: no one-pass top
+            atomicOr(a.irregular, 1u);
     }
 }
 
@@ -287,11 +291,172 @@ __device__ int64_t level_in_block(const BuildArgs &a, int64_t f0, int64_t f1, in
     return next - f1;
 }
 
+// ---- the top levels in one pass
+//
+// Every node of level L <= k_top is a dyadic interval [k/2^L, (k+1)/2^L) of
+// the root (its bounds are midpoints of its ancestors, recorded by
+// dyadic_splits), and its source range is [lower_bound(lo), lower_bound(hi))
+// of the whole array (the clamp in node_children never binds, since the
+// ranges nest).  So which slots become nodes is known in closed form:
+//     slot (L, k) is a node  iff  count(L, k) > 0 and (L = 0 or the parent
+//     slot splits: count(L-1, k/2) > leaf_capacity and L-1 < max_depth),
+// (counts shrink down the path, so the parent's test covers every ancestor)
+// and its breadth-first index is the number of node slots before it in
+// level-major order.  One exclusive scan over the 2^(k_top+1) - 1 slots
+// replaces 2 (k_top + 1) grid barriers of the level-by-level build.
+// Requires every top interval to be regular (lo < mid < hi, else the
+// reference's one-child cases apply and the build goes level by level).
+
+// Bound k of level L (0 <= k <= 2^L): its value and lower_bound in xs.
+__device__ __forceinline__ void top_point(const BuildArgs &a, int L, int64_t k, double lo0,
+                                          double hi0, double *v, int64_t *lb)
+{
+    if (k == 0) {
+        *v = lo0;
+        *lb = 0;
+        return;
+    }
+    if (k == ((int64_t)1 << L)) {
+        *v = hi0;
+        *lb = a.n;
+        return;
+    }
+    const int z = __ffsll(k) - 1;               // k = (2 kp + 1) 2^z
+    const int Lp = L - z - 1;                   // the midpoint of node (Lp, kp)
+    const int64_t idx = ((int64_t)1 << Lp) - 1 + (k >> (z + 1));
+    *v = __ldcg(a.dy_mid + idx);
+    *lb = __ldcg(a.dy_split + idx);
+}
+
+struct TopSlot {
+    int L;
+    int64_t k;
+    double lo, hi;
+    int64_t s, e;
+    bool node, splits;
+};
+
+__device__ __forceinline__ TopSlot top_slot(const BuildArgs &a, int64_t f, double lo0, double hi0)
+{
+    TopSlot t;
+    t.L = 63 - __clzll(f + 1);
+    t.k = f + 1 - ((int64_t)1 << t.L);
+    top_point(a, t.L, t.k, lo0, hi0, &t.lo, &t.s);
+    top_point(a, t.L, t.k + 1, lo0, hi0, &t.hi, &t.e);
+    bool parent_splits = true;
+    if (t.L > 0) {
+        double v;
+        int64_t ps, pe;
+        top_point(a, t.L - 1, t.k >> 1, lo0, hi0, &v, &ps);
+        top_point(a, t.L - 1, (t.k >> 1) + 1, lo0, hi0, &v, &pe);
+        parent_splits = pe - ps > a.leaf_capacity && t.L - 1 < a.max_depth;
+    }
+    t.node = t.e > t.s && parent_splits;
+    t.splits = t.node && t.e - t.s > a.leaf_capacity && t.L < a.max_depth;
+    return t;
+}
+
+// Returns the first level for the level-by-level loop (k_top, or 0 if the
+// top cannot be built in one pass).  Grid-uniform.
+__device__ int64_t build_top(const BuildArgs &a, cg::grid_group &grid, int *warp_sums,
+                             int64_t *bases_s)
+{
+    const int K = a.k_top;
+    if (K <= 0 || *(volatile unsigned *)a.irregular)
+        return 0;
+    double lo0, hi0;
+    root_interval(a, &lo0, &hi0);
+    const int G = gridDim.x;
+    const int64_t S = ((int64_t)2 << K) - 1;  // slots of levels 0..K
+    const int64_t chunk = (S + G - 1) / G;
+    const int64_t b0 = (int64_t)blockIdx.x * chunk, b1 = min(S, b0 + chunk);
+    // pass 1: node flags, block-local exclusive offsets, leaves above level K
+    int64_t run = 0, leaves = 0;
+    for (int64_t t0 = b0; t0 < b1; t0 += blockDim.x) {
+        const int64_t f = t0 + threadIdx.x;
+        int flag = 0;
+        if (f < b1) {
+            const TopSlot t = top_slot(a, f, lo0, hi0);
+            flag = t.node;
+            leaves += t.node && !t.splits && t.L < K;
+        }
+        int excl;
+        const int tot = block_excl_scan(flag, &excl, warp_sums);
+        if (f < b1)
+            a.scratch_off[f] = (int32_t)(run + excl);
+        run += tot;
+    }
+    if (threadIdx.x == 0)
+        a.block_total[blockIdx.x] = run;
+    {
+        int64_t lv = leaves;
+        for (int o = 16; o > 0; o >>= 1)
+            lv += __shfl_xor_sync(DT_FULL, lv, o);
+        if (dt_lane() == 0 && lv)
+            atomicAdd((unsigned long long *)&a.meta[DT_META_LEAVES], (unsigned long long)lv);
+    }
+    grid.sync();
+    // every block's base, fixed order (G <= blockDim.x)
+    if (threadIdx.x == 0) {
+        int64_t acc = 0;
+        for (int b = 0; b < G; ++b) {
+            bases_s[b] = acc;
+            acc += ((volatile int64_t *)a.block_total)[b];
+        }
+        bases_s[G] = acc;
+    }
+    __syncthreads();
+    const int64_t total = bases_s[G];
+    if (total > a.capacity) {  // every block sees the same total
+        if (blockIdx.x == 0 && threadIdx.x == 0)
+            a.meta[DT_META_OVERFLOW] = 1;
+        return -1;
+    }
+    auto index_of = [&](int64_t f) -> int64_t {  // exclusive node count before slot f
+        return f >= S ? total : bases_s[f / chunk] + __ldcg(a.scratch_off + f);
+    };
+    // pass 2: write the nodes and their child slots
+    for (int64_t f = b0 + threadIdx.x; f < b1; f += blockDim.x) {
+        const TopSlot t = top_slot(a, f, lo0, hi0);
+        if (!t.node)
+            continue;
+        const int64_t c = index_of(f);
+        write_node(a, c, t.lo, t.hi, t.L, t.s, t.e);
+        if (t.splits && t.L < K) {
+            const int64_t split = __ldcg(a.dy_split + f);  // this slot's own midpoint
+            const int64_t fl = 2 * f + 1;                  // slot (L + 1, 2k)
+            const int64_t l_slot = split > t.s ? index_of(fl) : -1;
+            const int64_t r_slot = t.e > split ? index_of(fl + 1) : -1;
+            a.left[c] = l_slot;
+            a.right[c] = r_slot;
+            if (a.packed) {
+                a.packed[c].left = (int32_t)l_slot;
+                a.packed[c].right = (int32_t)r_slot;
+            }
+        }
+    }
+    if (blockIdx.x == 0 && threadIdx.x <= K + 1) {
+        const int L = threadIdx.x;  // level offsets 0 .. K + 1
+        a.meta[DT_META_LEVEL0 + L] = index_of(((int64_t)1 << L) - 1);
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        a.meta[DT_META_NODES] = total;
+        int depth = 0;
+        for (int L = 0; L <= K; ++L)
+            if (index_of(((int64_t)2 << L) - 1) > index_of(((int64_t)1 << L) - 1))
+                depth = L;
+        a.meta[DT_META_DEPTH] = depth;
+    }
+    grid.sync();
+    return K;
+}
+
 __global__ void __launch_bounds__(BUILD_THREADS) build_kernel(BuildArgs a)
 {
     cg::grid_group grid = cg::this_grid();
     __shared__ int warp_sums[BUILD_THREADS / 32];
     __shared__ int64_t sh_i64[4];
+    __shared__ int64_t top_bases_s[BUILD_THREADS + 1];
     extern __shared__ double samples_s[];  // BUILD_SAMPLES
     volatile int64_t *meta = a.meta;
     const int G = gridDim.x;
@@ -317,10 +482,24 @@ __global__ void __launch_bounds__(BUILD_THREADS) build_kernel(BuildArgs a)
     if (blockIdx.x == 0 && threadIdx.x == 0)
         *small_flag = 0;
 #endif
+#ifdef DT_BUILD_TRACE
+#define BUILD_STAMP(slot)                                                                    \
+    if (blockIdx.x == 0 && threadIdx.x == 0) {                                               \
+        unsigned long long t_;                                                               \
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                              \
+        a.block_total[2048 + (slot)] = (int64_t)t_;                                          \
+    }
+#else
+#define BUILD_STAMP(slot)
+#endif
+    BUILD_STAMP(70)
     dyadic_splits(a);
     grid.sync();
-
-    int64_t lev = 0;
+    BUILD_STAMP(71)
+    int64_t lev = build_top(a, grid, warp_sums, top_bases_s);
+    BUILD_STAMP(72)
+    if (lev < 0)
+        return;  // capacity overflow (flagged in meta)
     while (lev <= a.max_depth) {
 #ifdef DT_BUILD_TRACE
         if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -503,7 +682,7 @@ extern "C" size_t dt_build_workspace(int64_t n, int64_t node_capacity)
 {
     (void)n;
     return (size_t)node_capacity * 2 * sizeof(int32_t) + 4096 * sizeof(int64_t) + 16 +
-           (size_t)DYADIC * (sizeof(int64_t) + sizeof(double));
+           (size_t)DYADIC * (sizeof(int64_t) + sizeof(double)) + 16;
 }
 
 extern "C" int dt_build_tree(const double *xs, int64_t n, int64_t leaf_capacity, int64_t max_depth, int64_t node_capacity,
@@ -548,6 +727,20 @@ extern "C" int dt_build_tree(const double *xs, int64_t n, int64_t leaf_capacity,
     a.block_total = (int64_t *)(((uintptr_t)a.block_total + 7) & ~(uintptr_t)7);
     a.dy_split = a.block_total + 4096;
     a.dy_mid = (double *)(a.dy_split + DYADIC);
+    a.irregular = (unsigned *)(a.dy_mid + DYADIC);
+    // one-pass top: levels 0..k_top need 2^(k_top+1) - 1 scratch slots and
+    // the dyadic midpoints of levels < k_top
+    a.k_top = 0;
+#ifndef DT_BUILD_TOP
+#define DT_BUILD_TOP 1
+#endif
+    if (DT_BUILD_TOP)
+        for (int K = DYADIC_LEVELS; K >= 1; --K)
+            if (((int64_t)2 << K) - 1 <= node_capacity) {
+                a.k_top = K;
+                break;
+            }
+    DT_CUDA_TRY(cudaMemsetAsync(a.irregular, 0, sizeof(unsigned), (cudaStream_t)stream));
 
     int dev = 0, per_sm = 0;
     DT_CUDA_TRY(cudaGetDevice(&dev));

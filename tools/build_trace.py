@@ -20,6 +20,8 @@ cap = bufs.capacity
 bt = bufs.ws.view(torch.uint8)[cap * 8: cap * 8 + 4096 * 8].view(torch.int64).cpu().numpy()
 depth = int(bufs.meta[1])
 t = bt[2048: 2048 + depth + 2]
+ph = bt[2048 + 70: 2048 + 73]
+print("dyadic splits + barrier %.1f us, one-pass top %.1f us" % ((ph[1] - ph[0]) / 1e3, (ph[2] - ph[1]) / 1e3))
 lv = bufs.meta[8: 8 + depth + 2].cpu().numpy()
 print("per-level us (level: nodes us):")
 for l in range(depth + 1):
