@@ -352,6 +352,24 @@ size_t dt_phi_sum_symmetric_workspace(int64_t n);
 int dt_phi_sum_symmetric(const double *xs, const double *qs, int64_t n, double rd2, double *out,
                          int accumulate, void *workspace, size_t workspace_bytes, void *stream);
 
+/* ---------------------------------------------------------------- sorting */
+
+/* Stable sort of v[0..n) (charges.py:127: np.argsort(x, kind="stable") in
+ * from_particles; unsorted targets in evaluate_all): LSD radix sort on
+ * order-preserving 64-bit codes (-0.0 taken as +0.0: equal keys keep their
+ * input order, as numpy's).  Outputs (each may be NULL): sorted[i] =
+ * v[perm[i]], perm[i], payload_out[i] = payload[perm[i]].  n < 2^31.  Reads
+ * the eight digit histograms back to the host once to skip passes whose digit
+ * is the same for every key (synchronises the stream).  NaN keys sort by
+ * their bits (callers reject them first). */
+size_t dt_sort_workspace(int64_t n);
+int dt_sort_stable(const double *v, int64_t n, double *sorted, int64_t *perm,
+                   const double *payload, double *payload_out, void *workspace,
+                   size_t workspace_bytes, void *stream);
+/* dst[i] = src[perm[i]] (scatter == 0) or dst[perm[i]] = src[i] (scatter != 0). */
+int dt_permute(const double *src, const int64_t *perm, int64_t n, double *dst, int scatter,
+               void *stream);
+
 /* ---------------------------------------------------------------- diagnostics */
 
 /* FP64 FMA throughput probe for the roofline denominator: `blocks` x 256

@@ -82,6 +82,9 @@ SIGNATURES = {
         C.c_int, [_P, _P, _P, _P, _P, _P, _P, _P, _I64, _P, _P, _I64, _I64, _P, _SZ, _P],
     ),
     "dt_moments_from_eval": (C.c_int, [_P, _I64, _I64, _I64, _P, _P]),
+    "dt_sort_workspace": (_SZ, [_I64]),
+    "dt_sort_stable": (C.c_int, [_P, _I64, _P, _P, _P, _P, _P, _SZ, _P]),
+    "dt_permute": (C.c_int, [_P, _P, _I64, _P, C.c_int, _P]),
     "dt_shard_plan": (
         C.c_int,
         [_P, _P, _P, _P, _P, _I64, _P, _I64, C.c_int, _D, _I64, C.c_int, C.c_int, _P, _P],

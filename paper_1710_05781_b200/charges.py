@@ -112,6 +112,35 @@ def check_values(v: torch.Tensor, flags: torch.Tensor | None = None) -> torch.Te
     return flags
 
 
+def sort_stable(v: torch.Tensor, payload: torch.Tensor | None = None):
+    """(sorted v, permutation int64, payload[perm] or None) on the device:
+    the stable radix sort dt_sort_stable (np.argsort(kind="stable"))."""
+    n = v.numel()
+    out = torch.empty_like(v)
+    perm = torch.empty(n, dtype=torch.int64, device=v.device)
+    pay = torch.empty_like(payload) if payload is not None else None
+    if n:
+        L = _lib.load()
+        wsb = int(L.dt_sort_workspace(n))
+        ws = torch.empty(wsb, dtype=torch.uint8, device=v.device)
+        _lib.check(L.dt_sort_stable(_lib.ptr(v), n, _lib.ptr(out), _lib.ptr(perm),
+                                    _lib.ptr(payload), _lib.ptr(pay), _lib.ptr(ws), wsb,
+                                    _lib.stream_handle()), "dt_sort_stable")
+    return out, perm, pay
+
+
+def permute(src: torch.Tensor, perm: torch.Tensor, scatter: bool = False,
+            out: torch.Tensor | None = None) -> torch.Tensor:
+    """out[i] = src[perm[i]], or out[perm[i]] = src[i] with scatter (dt_permute)."""
+    if out is None:
+        out = torch.empty_like(src)
+    if src.numel():
+        _lib.check(_lib.load().dt_permute(_lib.ptr(src), _lib.ptr(perm), src.numel(),
+                                          _lib.ptr(out), int(bool(scatter)),
+                                          _lib.stream_handle()), "dt_permute")
+    return out
+
+
 def from_particles(raw) -> ChargeSystem:
     """Sorted ChargeSystem from (x, q) pairs (charges.py:114-132).
 
@@ -138,9 +167,8 @@ def from_particles(raw) -> ChargeSystem:
     bad, desc = flags.tolist()
     if bad:
         raise ValueError("positions and strengths must all be finite")
-    if desc:
-        x, order = torch.sort(x, stable=True)
-        q = q[order].contiguous()
+    if desc:  # stable sort by position (charges.py:127), q carried along
+        x, _, q = sort_stable(x, q)
     return from_sorted(x, q)
 
 

@@ -18,7 +18,8 @@ import numpy as np
 import torch
 
 from . import _lib
-from .charges import ChargeSystem, _sign_terms, as_targets, check_values, host_targets
+from .charges import (ChargeSystem, _sign_terms, as_targets, check_values, host_targets,
+                      permute, sort_stable)
 from .direct import FieldResult
 from .kernel import DEFAULT_CONTOUR_SAMPLES, DEFAULT_P_MAX, DiscKernel
 
@@ -387,10 +388,10 @@ def evaluate_all(tree: Tree, kernel: DiscKernel, config: EvalConfig, system: Cha
     T = t.numel()
     if T:
         if T > 1 and check_values(t).tolist()[1]:
-            ys, perm = torch.sort(t)
-            vs = values[perm].contiguous()
-            tree_phi_sum(tree, kernel, config, ys.contiguous(), vs)
-            values[perm] = vs
+            # sorted targets traverse coherently; the field goes back in place
+            ys, perm, vs = sort_stable(t, values)
+            tree_phi_sum(tree, kernel, config, ys, vs)
+            permute(vs, perm, scatter=True, out=values)
         else:
             tree_phi_sum(tree, kernel, config, t, values)
     torch.cuda.synchronize(dev)
