@@ -50,11 +50,21 @@ if len(sys.argv) > 5:
     r = list(csv.reader(io.StringIO(raw)))
     h, u = r[0], r[1]
     nodes, leaves = b["config"]["nodes"], b["config"]["leaves"]
-    alg = {"build_kernel": 8 * 2**24 + 72 * nodes,
-           "p2m_group_kernel": 16 * 2**24 + 8 * (31 + 32) * leaves,
-           "m2m_flow_kernel": 8 * (2 * 31 + 31 + 32) * (nodes - leaves)}
-    aux = {"capture": "ncu --set full --clock-control none -k regex:'p2m|m2m|build_kernel' "
-                      "-s 3 -c 3 python tools/moments_time.py (configs[2])", "kernels": []}
+    N, P1 = 2**24, 31
+    # B_build = 8N + 72 nodes; B_P2M + B_M2M = 16N + 8(P+1) leaves
+    # + 24(P+1) internal nodes (the fused upward kernel does both); B_scan = 16N
+    # over the two scan passes (reported per pass: q read + prefix write).
+    alg = {"build_kernel": 8 * N + 72 * nodes,
+           "upward_kernel": 16 * N + 8 * P1 * leaves + 24 * P1 * (nodes - leaves),
+           "moments_prep_kernel": 0,
+           "tile_sums_kernel": 8 * N,
+           "tile_apply_kernel": 8 * N + 8 * N}
+    aux = {"capture": "ncu --set full --clock-control none --import-source on -k "
+                      "regex:'build_kernel|upward|moments_prep|tile_' -s 6 -c 5 python "
+                      "tools/prof_eval.py (configs[2]; the second pipeline step)",
+           "note": "ncu flushes caches between kernels: tile_apply's L2 reuse of q is not "
+                   "seen here; moments_prep (parent / arrival bookkeeping) has no 8(d) bytes",
+           "kernels": []}
     for v in r[2:]:
         gv = lambda k: float(v[h.index(k)]) * scale.get(u[h.index(k)], 1)
         name = v[h.index("Kernel Name")]
@@ -65,6 +75,7 @@ if len(sys.argv) > 5:
             "kernel": name.split("(")[0], "duration_ms": t,
             "dram_bytes": gv("dram__bytes_read.sum") + gv("dram__bytes_write.sum"),
             "algorithmic_bytes": alg[key], "algorithmic_GBps": alg[key] / (t * 1e-3) / 1e9,
+            "frac_of_hbm_6553GBps": alg[key] / (t * 1e-3) / 1e9 / 6553.0,
             "fp64_pipe_active_pct": float(v[h.index("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active")]),
             "issue_active_pct": float(v[h.index("smsp__issue_active.avg.pct_of_peak_sustained_active")]),
             "warps_active_pct": float(v[h.index("sm__warps_active.avg.pct_of_peak_sustained_active")]),
