@@ -13,10 +13,11 @@
 //     rows M_k = c_k S_k only (the reference layout is derived on request):
 //     warps take 32 node slots at a time, deepest first, form the leaves
 //     among them (P2M with split powers, 2 lanes per leaf), and every formed
-//     leaf bumps its parent's arrival counter; the lane whose arrival
-//     completes a parent keeps it, and the warp forms kept parents (four at
-//     a time, 8 lanes and 4 orders per lane, or a lone one on 32 lanes)
-//     before those lanes climb on.  The M2M chains thus run while other
+//     leaf climbs: sibling pairs formed by the same warp complete their
+//     parent directly, others bump the parent's arrival counter and the
+//     lane whose arrival completes a parent keeps it; the warp forms the
+//     kept parents two lanes per parent (one child each, raw sums in
+//     registers) before those lanes climb on.  The M2M chains thus run while other
 //     warps are still in P2M.  The shard plan (multi-GPU) restricts it to
 //     one rank's subtrees; shard_finish_kernel forms the levels above the
 //     cut with the same arithmetic, thread per node.
@@ -273,13 +274,11 @@ __global__ void __launch_bounds__(MOM_THREADS) moments_kernel(MomArgs a)
 // Rows are stored once, in the traversal layout M_k = c_k S_k (c_0 = 1,
 // c_k = gamma_(k-1) / k = c_mev_s[k], dt_farcoef.cuh; S_k = k! m_k the raw
 // power sums), which is all the traversal reads; the reference layout m_k is
-// derived from them only on request (dt_moments_from_eval).  In this basis a
-// Pascal pass S_k += delta S_(k-1) reads
-//     M_k += e_k M_(k-1),   e_k = delta rho_k,   rho_k = c_k / c_(k-1),
-// so the binomial shift costs the same FMAs as on raw sums, and every form
-// below (warp, four parents per warp, thread per node) computes e_k as
-// __dmul_rn(delta, rho_k) and applies the passes in the same order: the rows
-// are bit-identical whichever form (and whichever rank) produced them.
+// derived from them only on request (dt_moments_from_eval).  A parent is
+// formed by shift_child on each child row (to raw sums, binomial shift, back)
+// and one addition; the two-lane form (form_node_pair) and the thread form
+// (up_level_threads, shard_finish) do exactly that, so the rows are
+// bit-identical whichever form (and whichever rank) produced them.
 
 // P2M of one leaf over G lanes: raw power sums S_k = sum q (x - c)^k for
 // k < KMAX, with the powers split as t^(8m + r) = t^r (t^8)^m: per source 7
@@ -412,101 +411,6 @@ __device__ __forceinline__ void p2m_split_leaf(const MomArgs &a, int64_t node, b
     }
 }
 
-// Form internal node P from its children with one warp, lane k = order k:
-// 31 M-basis Pascal passes for both children at once (the previous pass's
-// M_(k-1) comes from lane k - 1; orders below the pass take a zero factor).
-__device__ __forceinline__ void up_form_warp(const MomArgs &a, int64_t P, const double *rho_s)
-{
-    const int lane = dt_lane();
-    const int o1 = (int)a.order + 1;
-    const int64_t es = a.estride;
-    const int64_t l = __ldg(a.left + P), r = __ldg(a.right + P);
-    const double c = __ldg(a.center + P);
-    const double dl = l >= 0 ? __ldg(a.center + l) - c : 0.0;
-    const double dr = r >= 0 ? __ldg(a.center + r) - c : 0.0;
-    const double rho = rho_s[lane];
-    const double el = __dmul_rn(dl, rho), er = __dmul_rn(dr, rho);
-    double Ml = (l >= 0 && lane < o1) ? __ldcg(a.meval + l * es + lane) : 0.0;
-    double Mr = (r >= 0 && lane < o1) ? __ldcg(a.meval + r * es + lane) : 0.0;
-#pragma unroll
-    for (int i = 1; i < REG_ORDER; ++i) {
-        const double tl = __shfl_up_sync(DT_FULL, Ml, 1);
-        const double tr = __shfl_up_sync(DT_FULL, Mr, 1);
-        const bool on = lane >= i;
-        Ml = __fma_rn(on ? el : 0.0, tl, Ml);
-        Mr = __fma_rn(on ? er : 0.0, tr, Mr);
-    }
-    double out = 0.0;
-    if (l >= 0)
-        out += Ml;
-    if (r >= 0)
-        out += Mr;
-    if (lane < es)
-        a.meval[P * es + lane] = lane < o1 ? out : 0.0;
-}
-
-// Four parents per warp: lanes [8g, 8g + 8) form parent P of group g, lane
-// gl of a group holding orders 4 gl .. 4 gl + 3 of both children, so a pass
-// needs one neighbour value per lane.  Term for term the arithmetic of
-// up_form_warp (a skipped order's update is fma(0, x, M) = M).
-__device__ __forceinline__ void up_form_group8(const MomArgs &a, int64_t P, const double *rho_s)
-{
-    const int gl = dt_lane() & 7;
-    const int o1 = (int)a.order + 1;
-    const int64_t es = a.estride;
-    int64_t l = -1, r = -1;
-    double dl = 0.0, dr = 0.0;
-    if (P >= 0) {
-        l = __ldg(a.left + P);
-        r = __ldg(a.right + P);
-        const double c = __ldg(a.center + P);
-        if (l >= 0)
-            dl = __ldg(a.center + l) - c;
-        if (r >= 0)
-            dr = __ldg(a.center + r) - c;
-    }
-    double Ml[4], Mr[4], el[4], er[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-        const int k = 4 * gl + u;
-        el[u] = __dmul_rn(dl, rho_s[k]);
-        er[u] = __dmul_rn(dr, rho_s[k]);
-        Ml[u] = (l >= 0 && k < o1) ? __ldcg(a.meval + l * es + k) : 0.0;
-        Mr[u] = (r >= 0 && k < o1) ? __ldcg(a.meval + r * es + k) : 0.0;
-    }
-#pragma unroll
-    for (int i = 1; i < REG_ORDER; ++i) {
-        const double nl = __shfl_up_sync(DT_FULL, Ml[3], 1, 8);
-        const double nr = __shfl_up_sync(DT_FULL, Mr[3], 1, 8);
-        // descending within the lane: every update reads the previous pass
-#pragma unroll
-        for (int u = 3; u >= 0; --u) {
-            const bool on = gl >= ((i - u + 3) >> 2);
-            Ml[u] = __fma_rn(on ? el[u] : 0.0, u ? Ml[u - 1] : nl, Ml[u]);
-            Mr[u] = __fma_rn(on ? er[u] : 0.0, u ? Mr[u - 1] : nr, Mr[u]);
-        }
-    }
-    if (P < 0)
-        return;
-    double v[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-        const int k = 4 * gl + u;
-        double out = 0.0;
-        if (l >= 0)
-            out += Ml[u];
-        if (r >= 0)
-            out += Mr[u];
-        v[u] = k < o1 ? out : 0.0;
-    }
-    if (4 * gl < es) {  // es is even: orders 4 gl, 4 gl + 1 share a 16-byte word
-        double2 *row = reinterpret_cast<double2 *>(a.meval + P * es);
-        row[2 * gl] = make_double2(v[0], v[1]);
-        if (4 * gl + 2 < es)
-            row[2 * gl + 1] = make_double2(v[2], v[3]);
-    }
-}
-
 // Arrival on a node's counter with acquire-release semantics at GPU scope:
 // the release publishes the rows this warp wrote (ordered before it by a
 // __syncwarp), the acquire makes the rows behind earlier arrivals visible to
@@ -518,13 +422,91 @@ __device__ __forceinline__ int arrive_acq_rel(int32_t *p)
     return old;
 }
 
+// ---- M2M: two lanes per node (or one thread), raw sums in registers ----
+//
+// Child shift: a child row (M basis) is
+// converted to raw sums S_k = M_k / c_k, shifted to the parent's centre by
+// 31 in-place Pascal passes S_k += delta S_(k-1) (descending k, so every
+// update reads the previous pass), and converted back, T_k = S_k c_k; the
+// parent row is T(left) + T(right) (an only child's T as it is).  One
+// thread holds the whole row in registers: no shuffles or selects, and the
+// 496 FMAs of a pass sequence are independent within a pass.
+__device__ __forceinline__ void shift_child(const double *__restrict__ row, int o1, double delta,
+                                            double (&T)[REG_ORDER])
+{
+    const double2 *r2 = reinterpret_cast<const double2 *>(row);
+#pragma unroll
+    for (int k = 0; k < REG_ORDER; k += 2) {
+        double2 v = k < o1 ? __ldcg(r2 + (k >> 1)) : make_double2(0.0, 0.0);
+        T[k] = k == 0 ? v.x : __dmul_rn(v.x, c_inv_mevs[k]);
+        T[k + 1] = k + 1 < o1 ? __dmul_rn(v.y, c_inv_mevs[k + 1]) : 0.0;
+    }
+#pragma unroll
+    for (int i = 1; i < REG_ORDER; ++i) {
+#pragma unroll
+        for (int k = REG_ORDER - 1; k >= i; --k)
+            T[k] = __fma_rn(delta, T[k - 1], T[k]);
+    }
+#pragma unroll
+    for (int k = 1; k < REG_ORDER; ++k)
+        T[k] = __dmul_rn(T[k], c_mev_s[k]);
+}
+
+// Node `node` (internal) formed by the lane pair (sub 0: left child, sub 1:
+// right child); each lane then stores half of the row.  Both lanes of the
+// pair must call it (inactive pairs with node < 0).
+__device__ __forceinline__ void form_node_pair(const MomArgs &a, int64_t node, int sub)
+{
+    const int o1 = (int)a.order + 1;
+    const int64_t es = a.estride;
+    int64_t ch = -1, other = -1;
+    double delta = 0.0;
+    if (node >= 0) {
+        const int64_t l = __ldg(a.left + node), r = __ldg(a.right + node);
+        ch = sub ? r : l;
+        other = sub ? l : r;
+        if (ch >= 0)
+            delta = __ldg(a.center + ch) - __ldg(a.center + node);
+    }
+    double T[REG_ORDER];
+    if (ch >= 0) {
+        shift_child(a.meval + ch * es, o1, delta, T);
+    } else {
+#pragma unroll
+        for (int k = 0; k < REG_ORDER; ++k)
+            T[k] = 0.0;
+    }
+    // lane sub keeps orders [16 sub, 16 sub + 16): its own T plus the partner's
+    double out[REG_ORDER / 2];
+#pragma unroll
+    for (int k = 0; k < REG_ORDER / 2; ++k) {
+        const double give = sub ? T[k] : T[k + REG_ORDER / 2];
+        const double mine = sub ? T[k + REG_ORDER / 2] : T[k];
+        const double got = __shfl_xor_sync(DT_FULL, give, 1);
+        // left + right in that order; an only child's T as it is
+        const double tl = sub ? got : mine, tr = sub ? mine : got;
+        const bool has_l = sub ? other >= 0 : ch >= 0, has_r = sub ? ch >= 0 : other >= 0;
+        out[k] = has_l && has_r ? tl + tr : (has_l ? tl : tr);
+    }
+    if (node < 0)
+        return;
+    double2 *dst = reinterpret_cast<double2 *>(a.meval + node * es);
+#pragma unroll
+    for (int k = 0; k < REG_ORDER / 2; k += 2) {
+        const int kk = 16 * sub + k;
+        if (kk < es)
+            dst[kk >> 1] = make_double2(kk < o1 ? out[k] : 0.0, kk + 1 < o1 ? out[k + 1] : 0.0);
+    }
+}
+
 // The fused upward pass (after moments_prep_kernel wrote parent[] and zeroed
 // arrived[]): warps take 32 consecutive node slots at a time, deepest
 // first (their chains are the critical path); every leaf among them is
 // formed by P2M (32 / G leaves per round), then each formed leaf arrives at
 // its parent, and a lane whose arrival completes a parent keeps it: the warp
-// forms the kept parents (four at a time, or one with all 32 lanes) and
-// those lanes climb on.  Chains start while other warps are still in P2M,
+// forms the kept parents (16 per call, two lanes each: 0.287 ms at
+// configs[2] against 0.300 ms for the earlier 4-parents-per-warp Pascal
+// passes on 8 lanes) and those lanes climb on.  Chains start while other warps are still in P2M,
 // so the M2M latency overlaps the P2M throughput.  With a shard plan, leaves
 // below the cut outside the rank's source range are skipped and climbs stop
 // below the cut level.
@@ -534,12 +516,8 @@ __device__ __forceinline__ int arrive_acq_rel(int32_t *p)
 template <int G, int KMAX>
 __global__ void __launch_bounds__(256, DT_UP_MINB) upward_kernel(MomArgs a)
 {
-    __shared__ double rho_s[REG_ORDER];
     __shared__ int64_t frontier_s[8][32];
     const int warp = threadIdx.x >> 5;
-    if (threadIdx.x < REG_ORDER)
-        rho_s[threadIdx.x] = c_mev_rho[threadIdx.x];
-    __syncthreads();
     const int lane = dt_lane();
     const int sub = lane & (G - 1), grp = lane / G;
     const int64_t n = __ldg(a.meta + DT_META_NODES);
@@ -593,7 +571,11 @@ __global__ void __launch_bounds__(256, DT_UP_MINB) upward_kernel(MomArgs a)
         // Then the kept parents are formed, four per call (eight lanes each)
         // or one on the whole warp, and become the next frontier.
         int64_t v = climb ? mine : -1;
+#ifdef DT_UP_MAXROUNDS
+        for (int round_ = 0; round_ < DT_UP_MAXROUNDS; ++round_) {
+#else
         while (true) {
+#endif
             __syncwarp();  // this warp's rows precede the loads and releasing arrivals
             const unsigned fr = __ballot_sync(DT_FULL, v >= 0);
             if (!fr)
@@ -626,13 +608,10 @@ __global__ void __launch_bounds__(256, DT_UP_MINB) upward_kernel(MomArgs a)
                 frontier_s[warp][__popc(tk & ((1u << lane) - 1u))] = p;
             __syncwarp();  // the acquires and the parent list precede the loads
             const int np = __popc(tk);
-            if (np == 1) {
-                up_form_warp(a, frontier_s[warp][0], rho_s);
-            } else {
-                for (int c = 0; c < np; c += 4) {
-                    const int gi = c + (lane >> 3);
-                    up_form_group8(a, gi < np ? frontier_s[warp][gi] : -1, rho_s);
-                }
+            // two lanes per parent (left child, right child), 16 parents per call
+            for (int c = 0; c < np; c += 16) {
+                const int gi = c + (lane >> 1);
+                form_node_pair(a, gi < np ? frontier_s[warp][gi] : -1, lane & 1);
             }
             v = lane < np ? frontier_s[warp][lane] : -1;
         }
@@ -640,8 +619,7 @@ __global__ void __launch_bounds__(256, DT_UP_MINB) upward_kernel(MomArgs a)
 }
 
 // M2M of one level with one thread per internal node (shard_finish): the
-// M-basis Pascal passes in place over descending k, the arithmetic of
-// up_form_warp term for term.
+// child shift of form_node_pair, so the rows match bit for bit.
 __device__ __forceinline__ void up_level_threads(const MomArgs &a, int64_t f0, int64_t f1,
                                                  int64_t tid, int64_t nthreads)
 {
@@ -652,37 +630,20 @@ __device__ __forceinline__ void up_level_threads(const MomArgs &a, int64_t f0, i
         if (l < 0 && r < 0)
             continue;
         const double c = __ldg(a.center + node);
-        double out[REG_ORDER];
+        double tl[REG_ORDER], tr[REG_ORDER];
+        if (l >= 0)
+            shift_child(a.meval + l * es, o1, __ldg(a.center + l) - c, tl);
+        if (r >= 0)
+            shift_child(a.meval + r * es, o1, __ldg(a.center + r) - c, tr);
 #pragma unroll
-        for (int k = 0; k < REG_ORDER; ++k)
-            out[k] = 0.0;
-#pragma unroll 1
-        for (int ci = 0; ci < 2; ++ci) {
-            const int64_t ch = ci == 0 ? l : r;
-            if (ch < 0)
-                continue;
-            const double delta = __ldg(a.center + ch) - c;
-            const double *row = a.meval + ch * es;
-            double M[REG_ORDER];
-#pragma unroll
-            for (int k = 0; k < REG_ORDER; ++k)
-                M[k] = k < o1 ? __ldcg(row + k) : 0.0;
-#pragma unroll
-            for (int i = 1; i < REG_ORDER; ++i) {
-#pragma unroll
-                for (int k = REG_ORDER - 1; k >= i; --k)
-                    M[k] = __fma_rn(__dmul_rn(delta, c_mev_rho[k]), M[k - 1], M[k]);
-            }
-#pragma unroll
-            for (int k = 0; k < REG_ORDER; ++k)
-                out[k] += M[k];
-        }
-#pragma unroll
-        for (int k = 0; k < REG_ORDER; ++k)
+        for (int k = 0; k < REG_ORDER; ++k) {
+            const double v = l >= 0 && r >= 0 ? tl[k] + tr[k] : (l >= 0 ? tl[k] : tr[k]);
             if (k < es)
-                a.meval[node * es + k] = k < o1 ? out[k] : 0.0;
+                a.meval[node * es + k] = k < o1 ? v : 0.0;
+        }
     }
 }
+
 
 // Reference-layout moments from traversal rows: m_k = M_k / ((k-1)! gamma_(k-1))
 // (tree.py:224-238 semantics, for the API's Tree.moments).
@@ -821,8 +782,8 @@ __global__ void shard_pack_kernel(const int64_t *plan, int rank, const double *m
 }
 
 // One block: scatter every owner's level-l rows, then M2M levels cut-1 .. 0
-// (thread per node; the same arithmetic as up_form_warp, so the rows match
-// the single-GPU pass bit for bit).
+// (thread per node; the arithmetic of form_node_pair, so the rows match the
+// single-GPU pass bit for bit).
 __global__ void __launch_bounds__(256) shard_finish_kernel(MomArgs a, int world, int64_t slot_rows,
                                                            const double *recv)
 {
