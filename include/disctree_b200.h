@@ -291,6 +291,18 @@ int dt_tree_phi_sum_packed(const void *packed_nodes, int64_t n_nodes, const doub
                            const dt_eval_stats *stats, void *workspace,
                            size_t workspace_bytes, void *stream);
 
+/* dt_tree_eval_device with the sign term fused (the field E = e + phi, as
+ * dt_tree_field_packed): out[i] = E(ys[i]) for i in [i0, i1); xs / prefix
+ * are the sorted sources and their inclusive prefix sums; a workspace of
+ * dt_tree_field_workspace(i1 - i0) bytes adds the per-tile search brackets. */
+int dt_tree_field_device(const void *packed_nodes, const int64_t *meta, int64_t node_capacity,
+                         const double *moments, int64_t moment_stride, const double *xq,
+                         const double *xs, const double *prefix, int64_t n_src, double rd2,
+                         double theta, int64_t p, int adaptive, double tolerance, int64_t p_cap,
+                         const double *cos_tab, const double *sin_tab, int64_t n_samples,
+                         const double *ys, double *out, int64_t i0, int64_t i1, void *workspace,
+                         size_t workspace_bytes, void *stream);
+
 /* Whole field E(y) = e(y) + phi(y) (tree.py:340-373) in one kernel: the
  * sign term is computed per target from the sorted sources xs[0..n_src) and
  * their inclusive prefix sums exactly as dt_sign_terms does, then added to

@@ -121,6 +121,11 @@ SIGNATURES = {
         [_P, _P, _I64, _P, _I64, _P, _I64, _D, _D, _I64, C.c_int, _D, _I64, _P, _P, _I64, _P,
          _P, _I64, _I64, C.c_int, _P, _SZ, _P],
     ),
+    "dt_tree_field_device": (
+        C.c_int,
+        [_P, _P, _I64, _P, _I64, _P, _P, _P, _I64, _D, _D, _I64, C.c_int, _D, _I64, _P, _P,
+         _I64, _P, _P, _I64, _I64, _P, _SZ, _P],
+    ),
     "dt_fp64_probe": (C.c_int, [_P, _I64, C.c_int, _P]),
     "dt_choose_p_batch": (
         C.c_int, [_P, _P, _I64, _D, _D, _I64, _P, _P, _I64, C.c_int, _P, _P, _P],

@@ -1544,6 +1544,72 @@ extern "C" int dt_tree_eval_device(const void *packed_nodes, const int64_t *meta
     return launch_eval(a, adaptive != 0, false, (cudaStream_t)stream);
 }
 
+extern "C" int dt_tree_field_device(const void *packed_nodes, const int64_t *meta,
+                                    int64_t node_capacity, const double *moments,
+                                    int64_t moment_stride, const double *xq, const double *xs,
+                                    const double *prefix, int64_t n_src, double rd2,
+                                    double theta, int64_t p, int adaptive, double tolerance,
+                                    int64_t p_cap, const double *cos_tab, const double *sin_tab,
+                                    int64_t n_samples, const double *ys, double *out, int64_t i0,
+                                    int64_t i1, void *workspace, size_t workspace_bytes,
+                                    void *stream)
+{
+    DT_CHECK_ARG(meta != nullptr, "null meta");
+    int rc = check_eval_args(node_capacity, n_src, p, adaptive, tolerance, p_cap, n_samples, rd2,
+                             theta, i0, i1, moment_stride);
+    if (rc != DT_OK)
+        return rc;
+    if (i1 == i0)
+        return DT_OK;
+    DT_CHECK_ARG(packed_nodes && moments && ys && out && (n_src == 0 || (xq && xs && prefix)),
+                 "null pointer");
+    DT_CHECK_ARG(!adaptive || (cos_tab && sin_tab), "null contour tables");
+    DT_CHECK_ARG(((uintptr_t)packed_nodes & 31) == 0 && ((uintptr_t)xq & 15) == 0 &&
+                     ((uintptr_t)moments & 15) == 0,
+                 "packed nodes must be 32-byte aligned, sources and moments 16-byte aligned");
+    DT_CHECK_ARG((moment_stride & 1) == 0, "moment_stride must be even (16-byte rows)");
+    if (!workspace || workspace_bytes < DT_EVAL_COUNTER_BYTES)
+        return dt_set_error(DT_ERR_WORKSPACE, "eval workspace too small");
+    DT_CHECK_ARG(((uintptr_t)workspace & 15) == 0, "eval workspace must be 16-byte aligned");
+    EvalArgs a{};
+    a.nodes = (const dt_node *)packed_nodes;
+    a.n_nodes = node_capacity;
+    a.moments = moments;
+    a.stride = moment_stride;
+    a.xq = (const double2 *)xq;
+    a.rd2 = rd2;
+    a.theta = theta;
+    a.p = (int)p;
+    a.p_cap = (int)p_cap;
+    a.tol_share = 1.0;
+    a.tolerance = tolerance;
+    a.meta = adaptive ? meta : nullptr;
+    a.cos_tab = cos_tab;
+    a.sin_tab = sin_tab;
+    a.n_samples = (int)n_samples;
+    a.ys = ys;
+    a.out = out;
+    a.i0 = i0;
+    a.i1 = i1;
+    a.accumulate = 0;
+    a.psel_mode = DT_PSEL_FAST;
+    a.stats = dt_eval_stats{nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+    a.counter = (unsigned long long *)workspace;
+    a.sign_xs = xs ? xs : ys;  // non-null selects the fused form
+    a.sign_prefix = prefix;
+    a.sign_n = n_src;
+    const int64_t nb = (i1 - i0 + FIELD_TILE - 1) / FIELD_TILE;
+    const size_t bracket_bytes = (size_t)(nb + 1) * sizeof(int64_t);
+    if (n_src > 0 && workspace_bytes >= DT_EVAL_COUNTER_BYTES + bracket_bytes) {
+        int64_t *br = (int64_t *)((char *)workspace + DT_EVAL_COUNTER_BYTES);
+        field_bracket_kernel<<<(unsigned)((nb + 1 + 127) / 128), 128, 0, (cudaStream_t)stream>>>(
+            xs, n_src, ys, i0, i1, br, nb);
+        DT_CUDA_TRY(cudaGetLastError());
+        a.sign_bracket = br;
+    }
+    return launch_eval(a, adaptive != 0, false, (cudaStream_t)stream);
+}
+
 extern "C" int dt_tree_phi_sum(const double *centers, const double *halves, const int64_t *starts,
                                const int64_t *ends, const int64_t *lefts, const int64_t *rights,
                                const double *moments, int64_t moment_stride, int64_t n_nodes,

@@ -17,6 +17,7 @@ pass with one all-gather of the cut-level moment rows).
 
 from __future__ import annotations
 
+import os
 
 import torch
 
@@ -43,7 +44,7 @@ ORDER_TABLE_LAUNCHES = 2
 class TreePipeline:
     def __init__(self, n: int, n_targets: int, kernel: DiscKernel, config: EvalConfig,
                  node_capacity: int | None = None, device=None, world: int = 1, rank: int = 0,
-                 group=None, cut_level: int | None = None):
+                 group=None, cut_level: int | None = None, fused_sign: bool | None = None):
         self.dev = device or _lib.require_device()
         self.n, self.T = int(n), int(n_targets)
         self.kernel, self.config = kernel, config
@@ -61,8 +62,16 @@ class TreePipeline:
         self.scan_ws_bytes = int(L.dt_prefix_scan_workspace(self.n))
         self.scan_ws = torch.empty(self.scan_ws_bytes, dtype=torch.uint8, device=self.dev)
         self.xq = torch.empty(2 * self.n, dtype=torch.float64, device=self.dev)
-        self.eval_ws = torch.empty(_lib.DT_EVAL_COUNTER_BYTES, dtype=torch.uint8,
-                                   device=self.dev)
+        # the sign term as its own kernel on the side stream (dt_sign_terms,
+        # default: hidden beside the upward pass) or inside the traversal
+        # kernel (dt_tree_field_device: +0.22 ms of traversal at configs[2],
+        # step 12.61 against 12.52 ms)
+        if fused_sign is None:
+            fused_sign = os.environ.get("DT_PIPE_FUSED_SIGN", "0") == "1"
+        self.fused_sign = bool(fused_sign)
+        ws_bytes = (int(L.dt_tree_field_workspace(self.T)) if self.fused_sign
+                    else _lib.DT_EVAL_COUNTER_BYTES)
+        self.eval_ws = torch.empty(ws_bytes, dtype=torch.uint8, device=self.dev)
         self.sign_ws_bytes = int(L.dt_sign_terms_workspace(self.T))
         self.sign_ws = torch.empty(self.sign_ws_bytes, dtype=torch.uint8, device=self.dev)
         self.cos_t, self.sin_t = contour_tables(self.dev)
@@ -123,9 +132,11 @@ class TreePipeline:
         self.side.wait_event(self.ev_scan)
         with torch.cuda.stream(self.side):
             pack_sources(xs, qs, self.xq)
-            _lib.check(L.dt_sign_terms(p(xs), p(self.prefix), self.n, p(ys_part), p(out_part),
-                                       i1 - i0, p(self.sign_ws), self.sign_ws_bytes,
-                                       _lib.stream_handle()), "dt_sign_terms")
+            if not self.fused_sign:
+                _lib.check(L.dt_sign_terms(p(xs), p(self.prefix), self.n, p(ys_part),
+                                           p(out_part), i1 - i0, p(self.sign_ws),
+                                           self.sign_ws_bytes, _lib.stream_handle()),
+                           "dt_sign_terms")
             self.ev_side.record(self.side)
         if self.shard is None:
             launch_moments(self.bufs, xs, qs, self.order, self.moments, self.meval)
@@ -134,16 +145,30 @@ class TreePipeline:
         main.wait_event(self.ev_side)
         if eval_events is not None:
             eval_events[0].record()
-        _lib.check(
-            L.dt_tree_eval_device(
-                p(self.bufs.packed), p(self.bufs.meta), self.bufs.capacity, p(self.meval),
-                self.estride, p(self.xq), self.n, self.kernel.r_d * self.kernel.r_d,
-                float(cfg.theta), int(cfg.p), int(bool(cfg.adaptive)), float(cfg.tolerance),
-                self.order, p(self.cos_t), p(self.sin_t), self.cos_t.numel(), p(ys), p(out),
-                int(i0), int(i1), 1, p(self.eval_ws), self.eval_ws.numel(), s,
-            ),
-            "dt_tree_eval_device",
-        )
+        if self.fused_sign:
+            _lib.check(
+                L.dt_tree_field_device(
+                    p(self.bufs.packed), p(self.bufs.meta), self.bufs.capacity, p(self.meval),
+                    self.estride, p(self.xq), p(xs), p(self.prefix), self.n,
+                    self.kernel.r_d * self.kernel.r_d, float(cfg.theta), int(cfg.p),
+                    int(bool(cfg.adaptive)), float(cfg.tolerance), self.order, p(self.cos_t),
+                    p(self.sin_t), self.cos_t.numel(), p(ys), p(out), int(i0), int(i1),
+                    p(self.eval_ws), self.eval_ws.numel(), s,
+                ),
+                "dt_tree_field_device",
+            )
+        else:
+            _lib.check(
+                L.dt_tree_eval_device(
+                    p(self.bufs.packed), p(self.bufs.meta), self.bufs.capacity, p(self.meval),
+                    self.estride, p(self.xq), self.n, self.kernel.r_d * self.kernel.r_d,
+                    float(cfg.theta), int(cfg.p), int(bool(cfg.adaptive)),
+                    float(cfg.tolerance), self.order, p(self.cos_t), p(self.sin_t),
+                    self.cos_t.numel(), p(ys), p(out), int(i0), int(i1), 1, p(self.eval_ws),
+                    self.eval_ws.numel(), s,
+                ),
+                "dt_tree_eval_device",
+            )
         if eval_events is not None:
             eval_events[1].record()
 

@@ -168,3 +168,25 @@ def test_check_values_counts(dt):
     bad, desc = check_values(v).tolist()
     assert bad == 2
     assert desc == 2  # 1.0 -> 0.5 and inf -> 2.0 (comparisons with NaN are false)
+
+
+def test_pipeline_fused_sign_matches_separate():
+    """The device pipeline with the sign term fused into the traversal
+    (dt_tree_field_device) gives the same field bit for bit as the separate
+    sign-term kernel + accumulate."""
+    import paper_1710_05781_b200 as dt
+    from paper_1710_05781_b200 import workloads as W
+    from paper_1710_05781_b200.pipeline import TreePipeline
+
+    w = W.cfg2(cells=1 << 14)
+    k = dt.DiscKernel(w.r_d)
+    cfg = dt.EvalConfig(p=w.p, leaf_capacity=w.leaf_capacity, adaptive=True, tolerance=1e-10)
+    xs, qs, ys = (torch.from_numpy(a).cuda() for a in (w.xs, w.qs, w.targets))
+    outs = []
+    for fused in (False, True):
+        pipe = TreePipeline.planned(xs, ys.numel(), k, cfg, fused_sign=fused)
+        out = torch.full_like(ys, float("nan"))
+        pipe.step(xs, qs, ys, out)
+        pipe.check()
+        outs.append(out)
+    assert torch.equal(outs[0], outs[1])
