@@ -154,6 +154,15 @@ int dt_moments(const double *xs, const double *qs, const double *center, const i
                const int64_t *meta, int64_t order, double *moments, double *moments_eval,
                int64_t eval_stride, int64_t node_capacity, void *workspace,
                size_t workspace_bytes, void *stream);
+/* dt_moments that also writes xq[2 n_src], the interleaved (x, q) pairs of
+ * dt_pack_sources, from the loads P2M makes anyway (every source lies in one
+ * leaf), so a step needs no separate pack pass (orders > 31: the pack kernel
+ * runs after).  moments_eval is required. */
+int dt_moments_pack(const double *xs, const double *qs, int64_t n_src, const double *center,
+                    const int64_t *start, const int64_t *end, const int64_t *left,
+                    const int64_t *right, const int64_t *meta, int64_t order, double *moments,
+                    double *moments_eval, int64_t eval_stride, int64_t node_capacity, double *xq,
+                    void *workspace, size_t workspace_bytes, void *stream);
 /* Reference-layout moments[n_nodes][order + 1] from traversal rows:
  * m_k = M_k / ((k-1)! gamma_(k-1)) (one rounding per entry). */
 int dt_moments_from_eval(const double *moments_eval, int64_t eval_stride, int64_t n_nodes,

@@ -81,6 +81,10 @@ SIGNATURES = {
     "dt_moments": (
         C.c_int, [_P, _P, _P, _P, _P, _P, _P, _P, _I64, _P, _P, _I64, _I64, _P, _SZ, _P],
     ),
+    "dt_moments_pack": (
+        C.c_int,
+        [_P, _P, _I64, _P, _P, _P, _P, _P, _P, _I64, _P, _P, _I64, _I64, _P, _P, _SZ, _P],
+    ),
     "dt_moments_from_eval": (C.c_int, [_P, _I64, _I64, _I64, _P, _P]),
     "dt_sort_workspace": (_SZ, [_I64]),
     "dt_sort_stable": (C.c_int, [_P, _I64, _P, _P, _P, _P, _P, _SZ, _P]),

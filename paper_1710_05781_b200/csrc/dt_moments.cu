@@ -58,6 +58,7 @@ struct MomArgs {
     int32_t *arrived;  // workspace: finished children per node
     const int64_t *plan;  // optional shard plan (DT_PLAN_*): restrict to this rank's subtrees
     unsigned *chunk_ctr;  // workspace: upward_kernel's chunk counter (zeroed by the prep kernel)
+    double2 *xq;          // optional: the traversal's (x, q) pairs, written by P2M
 };
 
 __constant__ double c_inv_k[MAX_ORDER1] = {  // 1/k rounded to nearest (k >= 1)
@@ -325,6 +326,10 @@ __device__ __forceinline__ void p2m_split_leaf(const MomArgs &a, int64_t node, b
             nq0 = __ldg(a.qs + jn);
             nq1 = __ldg(a.qs + jn + G);
         }
+        if (a.xq) {  // the traversal's interleaved (x, q), every source written once
+            a.xq[j] = make_double2(cx0, cq0);
+            a.xq[j + G] = make_double2(cx1, cq1);
+        }
         const double t0 = cx0 - c, t1 = cx1 - c;
         double p0[8], p1[8];
         p0[0] = cq0;
@@ -337,10 +342,15 @@ __device__ __forceinline__ void p2m_split_leaf(const MomArgs &a, int64_t node, b
         have = hn;
 #else
     for (; j + G < e; j += 2 * G) {
-        const double t0 = __ldg(a.xs + j) - c, t1 = __ldg(a.xs + j + G) - c;
+        const double x0 = __ldg(a.xs + j), x1 = __ldg(a.xs + j + G);
+        const double t0 = x0 - c, t1 = x1 - c;
         double p0[8], p1[8];
         p0[0] = __ldg(a.qs + j);
         p1[0] = __ldg(a.qs + j + G);
+        if (a.xq) {
+            a.xq[j] = make_double2(x0, p0[0]);
+            a.xq[j + G] = make_double2(x1, p1[0]);
+        }
 #endif
 #pragma unroll
         for (int r = 1; r < 8; ++r) {
@@ -368,9 +378,12 @@ __device__ __forceinline__ void p2m_split_leaf(const MomArgs &a, int64_t node, b
         }
     }
     if (j < e) {
-        const double t0 = __ldg(a.xs + j) - c;
+        const double x0 = __ldg(a.xs + j);
+        const double t0 = x0 - c;
         double p0[8];
         p0[0] = __ldg(a.qs + j);
+        if (a.xq)
+            a.xq[j] = make_double2(x0, p0[0]);
 #pragma unroll
         for (int r = 1; r < 8; ++r)
             p0[r] = p0[r - 1] * t0;
@@ -894,6 +907,41 @@ extern "C" int dt_shard_plan(const double *center, const double *half, const int
         world, rank, plan);
     DT_CUDA_TRY(cudaGetLastError());
     return DT_OK;
+}
+
+// dt_moments that also writes the traversal's interleaved sources xq[2n]
+// (what dt_pack_sources does) from the loads P2M makes anyway: every source
+// lies in exactly one leaf.  Orders > 31 pack with the separate kernel.
+extern "C" int dt_pack_sources(const double *xs, const double *qs, int64_t n, double *xq,
+                               void *stream);
+extern "C" int dt_moments_pack(const double *xs, const double *qs, int64_t n_src,
+                               const double *center, const int64_t *start, const int64_t *end,
+                               const int64_t *left, const int64_t *right, const int64_t *meta,
+                               int64_t order, double *moments, double *moments_eval,
+                               int64_t eval_stride, int64_t node_capacity, double *xq,
+                               void *workspace, size_t workspace_bytes, void *stream)
+{
+    DT_CHECK_ARG(n_src >= 0 && (n_src == 0 || xq), "null xq");
+    DT_CHECK_ARG(((uintptr_t)xq & 15) == 0, "xq must be 16-byte aligned");
+    DT_CHECK_ARG(eval_stride >= order + 1 && eval_stride % 2 == 0,
+                 "eval_stride must be even and >= order + 1");
+    DT_CHECK_ARG(order >= 0 && order < MAX_ORDER1, "moment order must be in [0, 127]");
+    DT_CHECK_ARG(node_capacity >= 1 && node_capacity < (int64_t)1 << 31, "bad node capacity");
+    DT_CHECK_ARG(xs && qs && center && start && end && left && right && meta, "null pointer");
+    if (order + 1 > REG_ORDER) {
+        const int rc = dt_moments(xs, qs, center, start, end, left, right, meta, order, moments,
+                                  moments_eval, eval_stride, node_capacity, workspace,
+                                  workspace_bytes, stream);
+        return rc != DT_OK ? rc : dt_pack_sources(xs, qs, n_src, xq, stream);
+    }
+    DT_CHECK_ARG(moments_eval && ((uintptr_t)moments_eval & 15) == 0,
+                 "moments_eval must be given and 16-byte aligned");
+    if (!workspace || workspace_bytes < dt_moments_workspace(node_capacity))
+        return dt_set_error(DT_ERR_WORKSPACE, "moments workspace too small");
+    MomArgs a{xs, qs, center, start, end, left, right, meta, order, moments, moments_eval,
+              eval_stride, (int32_t *)workspace, (int32_t *)workspace + node_capacity, nullptr,
+              (unsigned *)((int32_t *)workspace + 2 * node_capacity), (double2 *)xq};
+    return launch_level_moments(a, (cudaStream_t)stream);
 }
 
 extern "C" int dt_moments_from_eval(const double *moments_eval, int64_t eval_stride,

@@ -126,7 +126,7 @@ class ShardedMoments:
     Rows of subtrees no target of this rank can open are left untouched.
     """
 
-    LAUNCHES = 5  # plan, p2m, m2m, pack, finish (the all-gather is NCCL's)
+    LAUNCHES = 5  # plan, prep, upward, row pack, finish (the all-gather is NCCL's)
 
     def __init__(self, bufs, order: int, moments: torch.Tensor | None, meval: torch.Tensor,
                  estride: int, theta: float, world: int, rank: int, group=None,

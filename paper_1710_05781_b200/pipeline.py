@@ -3,8 +3,8 @@
 One ``step`` is the whole hot path on inputs already in HBM:
     (a) prefix scan of q and the sign term e(y)      dt_prefix_scan, dt_sign_terms
     (b) tree build                                   dt_build_tree (cooperative)
-    (c) P2M / M2M moments                            dt_moments (prep + fused dataflow)
-        interleave (x, q) for the traversal          dt_pack_sources
+    (c) P2M / M2M moments, and the (x, q) pairs       dt_moments_pack (prep + fused dataflow)
+        for the traversal (sharded: dt_pack_sources)
     (d)+(e) traversal, far + near field, += e(y)     dt_tree_eval_device
 All launches are stream-ordered and read sizes (node count, depth, level
 ranges, tol_share) from device memory, so the step can be timed back to back
@@ -35,9 +35,10 @@ from .tree import (
 )
 
 # kernels launched per step (memset of the work counter not counted):
-# scan(3) sign(2) build moments(2) pack eval, plus the two order-table
-# kernels ahead of an adaptive evaluation with moment order <= 31, theta <= 1/2
-LAUNCHES_PER_STEP = 3 + 2 + 1 + 2 + 1 + 1
+# scan(2) sign(2) build moments(2) eval, plus the two order-table kernels
+# ahead of an adaptive evaluation with moment order <= 31, theta <= 1/2 (the
+# sharded pass adds its own launches and the separate pack)
+LAUNCHES_PER_STEP = 2 + 2 + 1 + 2 + 1
 ORDER_TABLE_LAUNCHES = 2
 
 
@@ -86,8 +87,11 @@ class TreePipeline:
                                         self.estride, config.theta, world, rank, group,
                                         cut_level)
         tables = bool(config.adaptive) and self.order <= 31 and config.theta <= 0.5
-        self.launches_per_step = LAUNCHES_PER_STEP + (
-            self.shard.LAUNCHES - 2 if self.shard else 0) + (ORDER_TABLE_LAUNCHES if tables else 0)
+        # fused sign: the bracket kernel instead of the two sign-term kernels;
+        # sharded: its launches replace the two moments kernels, plus the pack
+        self.launches_per_step = LAUNCHES_PER_STEP + (-1 if self.fused_sign else 0) + (
+            self.shard.LAUNCHES - 2 + 1 if self.shard else 0) + (
+            ORDER_TABLE_LAUNCHES if tables else 0)
 
     @classmethod
     def planned(cls, xs: torch.Tensor, n_targets: int, kernel: DiscKernel,
@@ -131,15 +135,16 @@ class TreePipeline:
         self.ev_scan.record(main)
         self.side.wait_event(self.ev_scan)
         with torch.cuda.stream(self.side):
-            pack_sources(xs, qs, self.xq)
+            if self.shard is not None:  # the full upward pass writes xq itself
+                pack_sources(xs, qs, self.xq)
             if not self.fused_sign:
                 _lib.check(L.dt_sign_terms(p(xs), p(self.prefix), self.n, p(ys_part),
                                            p(out_part), i1 - i0, p(self.sign_ws),
                                            self.sign_ws_bytes, _lib.stream_handle()),
                            "dt_sign_terms")
             self.ev_side.record(self.side)
-        if self.shard is None:
-            launch_moments(self.bufs, xs, qs, self.order, self.moments, self.meval)
+        if self.shard is None:  # moments + the traversal's (x, q) pairs (dt_moments_pack)
+            launch_moments(self.bufs, xs, qs, self.order, self.moments, self.meval, xq=self.xq)
         else:  # this rank's subtrees + all-gather of the cut-level rows
             self.shard.launch(xs, qs, ys_part, targets_sorted=True)
         main.wait_event(self.ev_side)

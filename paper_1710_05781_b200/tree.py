@@ -209,11 +209,22 @@ def eval_stride(order: int) -> int:
 
 
 def launch_moments(bufs: TreeBuffers, xs, qs, order: int, moments: torch.Tensor | None,
-                   meval: torch.Tensor) -> None:
+                   meval: torch.Tensor, xq: torch.Tensor | None = None) -> None:
     """dt_moments: traversal rows into meval; for order > 31 (or when given)
-    the reference layout into moments as well."""
+    the reference layout into moments as well; with xq, the interleaved
+    (x, q) pairs too (dt_moments_pack: no separate pack pass)."""
     L = _lib.load()
     p = _lib.ptr
+    if xq is not None:
+        _lib.check(
+            L.dt_moments_pack(p(xs), p(qs), xs.numel(), p(bufs.center), p(bufs.start),
+                              p(bufs.end), p(bufs.left), p(bufs.right), p(bufs.meta),
+                              int(order), p(moments), p(meval), eval_stride(order),
+                              bufs.capacity, p(xq), p(bufs.mws), bufs.mws_bytes,
+                              _lib.stream_handle()),
+            "dt_moments_pack",
+        )
+        return
     _lib.check(
         L.dt_moments(p(xs), p(qs), p(bufs.center), p(bufs.start), p(bufs.end), p(bufs.left),
                      p(bufs.right), p(bufs.meta), int(order), p(moments), p(meval),
@@ -269,11 +280,12 @@ def _build(system: ChargeSystem, config: EvalConfig, upward) -> Tree:
     moments = (torch.empty((n_nodes, order + 1), dtype=torch.float64, device=dev)
                if order + 1 > 32 else None)
     meval = torch.empty((n_nodes, eval_stride(order)), dtype=torch.float64, device=dev)
-    if upward is None:
-        launch_moments(bufs, system.xs, system.qs, order, moments, meval)
+    xq = torch.empty(2 * n, dtype=torch.float64, device=dev)
+    if upward is None:  # moments and the traversal's (x, q) pairs in one pass
+        launch_moments(bufs, system.xs, system.qs, order, moments, meval, xq=xq)
     else:
         upward(bufs, order, moments, meval)
-    xq = pack_sources(system.xs, system.qs)
+        pack_sources(system.xs, system.qs, xq)
     torch.cuda.synchronize(dev)
     elapsed = time.perf_counter() - t0
     return Tree(
