@@ -147,10 +147,16 @@ __global__ void __launch_bounds__(SCAN_THREADS, DT_SCAN_MINB) tile_apply_kernel(
 // them) two threads bracket the block's source range with global searches,
 // the range is staged in shared memory and every target is located there;
 // otherwise each target is searched in global memory.
+#ifndef DT_SIGN_PER_THREAD
+#define DT_SIGN_PER_THREAD 2  // 512-target tiles: 0.159 ms at configs[2] (8: 0.201, 4: 0.171, 1: 0.206)
+#endif
+#ifndef DT_SIGN_SMEM
+#define DT_SIGN_SMEM 1024
+#endif
 constexpr int SIGN_THREADS = 256;
-constexpr int SIGN_PER_THREAD = 8;
+constexpr int SIGN_PER_THREAD = DT_SIGN_PER_THREAD;
 constexpr int SIGN_TILE = SIGN_THREADS * SIGN_PER_THREAD;
-constexpr int SIGN_SMEM = 4096;
+constexpr int SIGN_SMEM = DT_SIGN_SMEM;
 
 // bracket[b] = lower_bound(xs, ys[b * SIGN_TILE]) for every tile boundary
 // (and the last target), all searched in parallel.
