@@ -387,6 +387,16 @@ size_t dt_sort_workspace(int64_t n);
 int dt_sort_stable(const double *v, int64_t n, double *sorted, int64_t *perm,
                    const double *payload, double *payload_out, void *workspace,
                    size_t workspace_bytes, void *stream);
+/* Order-preserving compaction (with_images, charges.py:164-180): the r-th
+ * kept (xs[i], qs[i]) (keep[i] != 0, index order) goes to out_pairs[2 (offset
+ * + r)]; *count (device int64) receives the number kept.  Workspace
+ * dt_compact_workspace(n) bytes. */
+size_t dt_compact_workspace(int64_t n);
+int dt_compact_pairs(const double *xs, const double *qs, const uint8_t *keep, int64_t n,
+                     double *out_pairs, int64_t offset, int64_t *count, void *workspace,
+                     size_t workspace_bytes, void *stream);
+/* Stream-ordered zero fill of device memory (flag words of the checks). */
+int dt_zero(void *p, size_t bytes, void *stream);
 /* dst[i] = src[perm[i]] (scatter == 0) or dst[perm[i]] = src[i] (scatter != 0). */
 int dt_permute(const double *src, const int64_t *perm, int64_t n, double *dst, int scatter,
                void *stream);

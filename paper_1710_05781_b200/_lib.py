@@ -89,6 +89,9 @@ SIGNATURES = {
     "dt_sort_workspace": (_SZ, [_I64]),
     "dt_sort_stable": (C.c_int, [_P, _I64, _P, _P, _P, _P, _P, _SZ, _P]),
     "dt_permute": (C.c_int, [_P, _P, _I64, _P, C.c_int, _P]),
+    "dt_compact_workspace": (_SZ, [_I64]),
+    "dt_compact_pairs": (C.c_int, [_P, _P, _P, _I64, _P, _I64, _P, _P, _SZ, _P]),
+    "dt_zero": (C.c_int, [_P, _SZ, _P]),
     "dt_shard_plan": (
         C.c_int,
         [_P, _P, _P, _P, _P, _I64, _P, _I64, C.c_int, _D, _I64, C.c_int, C.c_int, _P, _P],
@@ -193,6 +196,15 @@ def stream_handle():
     import torch
 
     return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def zeros_i64(n: int, device):
+    """int64 device words zeroed by dt_zero (flag counters; no torch fill kernel)."""
+    import torch
+
+    t = torch.empty(n, dtype=torch.int64, device=device)
+    check(load().dt_zero(C.c_void_p(t.data_ptr()), 8 * n, stream_handle()), "dt_zero")
+    return t
 
 
 def ptr(t) -> C.c_void_p:

@@ -105,7 +105,7 @@ def check_values(v: torch.Tensor, flags: torch.Tensor | None = None) -> torch.Te
     the device flags (non-finite count, descent count), accumulated into
     ``flags`` when given."""
     if flags is None:
-        flags = torch.zeros(2, dtype=torch.int64, device=v.device)
+        flags = _lib.zeros_i64(2, v.device)
     if v.numel():
         _lib.check(_lib.load().dt_check_values(_lib.ptr(v), v.numel(), _lib.ptr(flags),
                                                _lib.stream_handle()), "dt_check_values")
@@ -159,7 +159,7 @@ def from_particles(raw) -> ChargeSystem:
     n = arr.shape[0]
     x = torch.empty(n, dtype=torch.float64, device=arr.device)
     q = torch.empty(n, dtype=torch.float64, device=arr.device)
-    flags = torch.zeros(2, dtype=torch.int64, device=arr.device)
+    flags = _lib.zeros_i64(2, arr.device)
     if n:
         _lib.check(_lib.load().dt_unpack_pairs(_lib.ptr(arr), n, _lib.ptr(x), _lib.ptr(q),
                                                _lib.ptr(flags), _lib.stream_handle()),
@@ -320,18 +320,28 @@ def with_images(system: ChargeSystem, spec: ImageSpec) -> ChargeSystem:
         planes.append(spec.lower_electrode)
     if spec.reflect_upper:
         planes.append(spec.lower_electrode + spec.gap_length)
-    xs_parts, qs_parts = [system.xs], [system.qs]
     n = len(system)
-    for plane in planes:
+    dev = system.xs.device
+    L = _lib.load()
+    pairs = torch.empty((n * (1 + len(planes)), 2), dtype=torch.float64, device=dev)
+    if n:  # the originals, then each plane's kept images, in index order
+        _lib.check(L.dt_pack_sources(_lib.ptr(system.xs), _lib.ptr(system.qs), n,
+                                     _lib.ptr(pairs), _lib.stream_handle()), "dt_pack_sources")
+    total = n
+    if planes and n:
         xm = torch.empty_like(system.xs)
         qm = torch.empty_like(system.qs)
-        keep = torch.empty(n, dtype=torch.uint8, device=system.xs.device)
-        _lib.check(_lib.load().dt_mirror_charges(
-            _lib.ptr(system.xs), _lib.ptr(system.qs), n, float(plane), float(spec.gap_length),
-            _lib.ptr(xm), _lib.ptr(qm), _lib.ptr(keep), _lib.stream_handle()),
-            "dt_mirror_charges")
-        k = keep.bool()
-        xs_parts.append(xm[k])
-        qs_parts.append(qm[k])
-    pairs = torch.stack([torch.cat(xs_parts), torch.cat(qs_parts)], dim=1).contiguous()
-    return from_particles(pairs)
+        keep = torch.empty(n, dtype=torch.uint8, device=dev)
+        count = torch.empty(1, dtype=torch.int64, device=dev)
+        wsb = int(L.dt_compact_workspace(n))
+        ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
+        for plane in planes:
+            _lib.check(L.dt_mirror_charges(
+                _lib.ptr(system.xs), _lib.ptr(system.qs), n, float(plane),
+                float(spec.gap_length), _lib.ptr(xm), _lib.ptr(qm), _lib.ptr(keep),
+                _lib.stream_handle()), "dt_mirror_charges")
+            _lib.check(L.dt_compact_pairs(_lib.ptr(xm), _lib.ptr(qm), _lib.ptr(keep), n,
+                                          _lib.ptr(pairs), total, _lib.ptr(count), _lib.ptr(ws),
+                                          wsb, _lib.stream_handle()), "dt_compact_pairs")
+            total += int(count.item())
+    return from_particles(pairs[:total])

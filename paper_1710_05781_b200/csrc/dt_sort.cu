@@ -304,3 +304,122 @@ extern "C" int dt_permute(const double *src, const int64_t *perm, int64_t n, dou
     DT_CUDA_TRY(cudaGetLastError());
     return DT_OK;
 }
+
+// ---- order-preserving compaction (with_images, charges.py:164-180) ----
+//
+// out[2 (offset + r)] = (xs[i], qs[i]) for the r-th i with keep[i] != 0, in
+// index order.  Two passes over 4096-element tiles: kept counts per tile,
+// then each tile's rank base = the counts of the tiles before it (summed in
+// a fixed order by the tile's first warp) plus a block scan.  *count (device)
+// receives the number kept.
+namespace {
+
+__global__ void __launch_bounds__(SORT_THREADS) compact_count_kernel(const uint8_t *__restrict__ keep,
+                                                                     int64_t n,
+                                                                     unsigned *__restrict__ tile_cnt)
+{
+    __shared__ unsigned c_s;
+    if (threadIdx.x == 0)
+        c_s = 0;
+    __syncthreads();
+    const int64_t base = (int64_t)blockIdx.x * SORT_TILE;
+    unsigned c = 0;
+#pragma unroll
+    for (int r = 0; r < SORT_ITEMS; ++r) {
+        const int64_t i = base + (int64_t)r * SORT_THREADS + threadIdx.x;
+        c += i < n && __ldg(keep + i);
+    }
+    for (int o = 16; o > 0; o >>= 1)
+        c += __shfl_xor_sync(DT_FULL, c, o);
+    if (dt_lane() == 0)
+        atomicAdd(&c_s, c);
+    __syncthreads();
+    if (threadIdx.x == 0)
+        tile_cnt[blockIdx.x] = c_s;
+}
+
+__global__ void __launch_bounds__(SORT_THREADS) compact_write_kernel(
+    const double *__restrict__ xs, const double *__restrict__ qs, const uint8_t *__restrict__ keep,
+    int64_t n, const unsigned *__restrict__ tile_cnt, int64_t tiles, double2 *__restrict__ out,
+    int64_t offset, int64_t *count)
+{
+    __shared__ unsigned long long base_s;
+    __shared__ unsigned wsum[SORT_WARPS];
+    const int lane = dt_lane(), warp = threadIdx.x >> 5;
+    if (warp == 0) {
+        unsigned long long b = 0;
+        for (int64_t t = lane; t < blockIdx.x; t += 32)
+            b += __ldg(tile_cnt + t);
+        for (int o = 16; o > 0; o >>= 1)
+            b += __shfl_xor_sync(DT_FULL, b, o);
+        if (lane == 0) {
+            base_s = b;
+            if (blockIdx.x == tiles - 1)
+                *count = (int64_t)(b + __ldg(tile_cnt + blockIdx.x));
+        }
+    }
+    // keys of this tile in index order: warp w owns 512 consecutive elements
+    const int64_t t0 = (int64_t)blockIdx.x * SORT_TILE + (int64_t)warp * (32 * SORT_ITEMS);
+    unsigned mine = 0;
+    unsigned masks[SORT_ITEMS];
+#pragma unroll
+    for (int r = 0; r < SORT_ITEMS; ++r) {
+        const int64_t i = t0 + 32 * r + lane;
+        masks[r] = __ballot_sync(DT_FULL, i < n && __ldg(keep + i));
+        mine += __popc(masks[r]);
+    }
+    if (lane == 0)
+        wsum[warp] = mine;
+    __syncthreads();
+    unsigned long long off = base_s;
+    for (int w = 0; w < warp; ++w)
+        off += wsum[w];
+#pragma unroll
+    for (int r = 0; r < SORT_ITEMS; ++r) {
+        const int64_t i = t0 + 32 * r + lane;
+        if ((masks[r] >> lane) & 1u)
+            out[offset + (int64_t)off + __popc(masks[r] & ((1u << lane) - 1u))] =
+                make_double2(__ldg(xs + i), __ldg(qs + i));
+        off += __popc(masks[r]);
+    }
+}
+
+}  // namespace
+
+extern "C" size_t dt_compact_workspace(int64_t n)
+{
+    return (size_t)(n > 0 ? (n + SORT_TILE - 1) / SORT_TILE : 1) * sizeof(unsigned);
+}
+
+extern "C" int dt_compact_pairs(const double *xs, const double *qs, const uint8_t *keep, int64_t n,
+                                double *out_pairs, int64_t offset, int64_t *count,
+                                void *workspace, size_t workspace_bytes, void *stream)
+{
+    DT_CHECK_ARG(n >= 0 && offset >= 0, "negative size");
+    DT_CHECK_ARG(count, "null count");
+    cudaStream_t s = (cudaStream_t)stream;
+    if (n == 0) {
+        DT_CUDA_TRY(cudaMemsetAsync(count, 0, sizeof(int64_t), s));
+        return DT_OK;
+    }
+    DT_CHECK_ARG(xs && qs && keep && out_pairs, "null pointer");
+    DT_CHECK_ARG(((uintptr_t)out_pairs & 15) == 0, "out_pairs must be 16-byte aligned");
+    if (!workspace || workspace_bytes < dt_compact_workspace(n))
+        return dt_set_error(DT_ERR_WORKSPACE, "compaction workspace too small");
+    const int64_t tiles = (n + SORT_TILE - 1) / SORT_TILE;
+    unsigned *cnt = (unsigned *)workspace;
+    compact_count_kernel<<<(unsigned)tiles, SORT_THREADS, 0, s>>>(keep, n, cnt);
+    compact_write_kernel<<<(unsigned)tiles, SORT_THREADS, 0, s>>>(xs, qs, keep, n, cnt, tiles,
+                                                                (double2 *)out_pairs, offset, count);
+    DT_CUDA_TRY(cudaGetLastError());
+    return DT_OK;
+}
+
+extern "C" int dt_zero(void *p, size_t bytes, void *stream)
+{
+    if (bytes == 0)
+        return DT_OK;
+    DT_CHECK_ARG(p, "null pointer");
+    DT_CUDA_TRY(cudaMemsetAsync(p, 0, bytes, (cudaStream_t)stream));
+    return DT_OK;
+}

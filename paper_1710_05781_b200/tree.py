@@ -182,7 +182,7 @@ class TreeBuffers:
         for k in self.I64:
             setattr(self, k, torch.empty(capacity, dtype=torch.int64, device=device))
         self.packed = torch.empty(capacity * 32, dtype=torch.uint8, device=device)
-        self.meta = torch.zeros(_lib.DT_META_WORDS, dtype=torch.int64, device=device)
+        self.meta = _lib.zeros_i64(_lib.DT_META_WORDS, device)
         L = _lib.load()
         self.ws_bytes = int(L.dt_build_workspace(n, capacity))
         self.ws = torch.empty(self.ws_bytes, dtype=torch.uint8, device=device)
@@ -438,7 +438,7 @@ def _evaluate_host_pipelined(tree: Tree, kernel: DiscKernel, config: EvalConfig,
     out_h = torch.empty(T, dtype=torch.float64, pin_memory=True)
     d_t = torch.empty(T, dtype=torch.float64, device=dev)
     d_o = torch.empty(T, dtype=torch.float64, device=dev)
-    flags = torch.zeros(2, dtype=torch.int64, device=dev)
+    flags = _lib.zeros_i64(2, dev)
     chunks = [(i, min(T, i + PIPELINE_CHUNK)) for i in range(0, T, PIPELINE_CHUNK)]
     L = _lib.load()
     p = _lib.ptr
@@ -510,7 +510,7 @@ def _evaluate_host_mapped(tree: Tree, kernel: DiscKernel, config: EvalConfig,
     dev = _lib.require_device()
     T = host.numel()
     out_h = torch.empty(T, dtype=torch.float64, pin_memory=True)
-    flags = torch.zeros(2, dtype=torch.int64, device=dev)
+    flags = _lib.zeros_i64(2, dev)
     ws = torch.empty(int(_lib.load().dt_tree_field_workspace(T)), dtype=torch.uint8, device=dev)
     cos_t, sin_t = contour_tables(dev)
     p = _lib.ptr
