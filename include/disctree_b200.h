@@ -53,6 +53,7 @@ extern "C" {
 #define DT_META_LEAVES 2   /* Tree.leaf_count                          */
 #define DT_META_OVERFLOW 3 /* nonzero: node_capacity was too small     */
 #define DT_META_CURLEVEL 4 /* internal                                 */
+#define DT_META_P2M_UPTO 5 /* leaves below this index already formed (dt_build_tree_p2m) */
 #define DT_META_LEVEL0 8
 #define DT_META_WORDS 72
 
@@ -131,6 +132,19 @@ int dt_build_tree(const double *xs, int64_t n, int64_t leaf_capacity, int64_t ma
                   int64_t *level, int64_t *start, int64_t *end, int64_t *left, int64_t *right,
                   void *packed, int64_t *meta, void *workspace, size_t workspace_bytes,
                   void *stream);
+
+/* dt_build_tree, and while block 0 runs the sparse deep levels the other
+ * blocks form the leaves of the finished levels (P2M into moments_eval, the
+ * traversal layout of dt_moments, and the (x, q) pairs into xq); meta[
+ * DT_META_P2M_UPTO] records how far (leaves below that node index are
+ * formed), and dt_moments / dt_moments_pack with the same moments_eval and
+ * order skip those leaves.  order <= 31. */
+int dt_build_tree_p2m(const double *xs, const double *qs, int64_t n, int64_t leaf_capacity,
+                      int64_t max_depth, int64_t node_capacity, double *lo, double *hi,
+                      double *center, double *half, int64_t *level, int64_t *start, int64_t *end,
+                      int64_t *left, int64_t *right, void *packed, int64_t *meta, int64_t order,
+                      double *moments_eval, int64_t eval_stride, double *xq, void *workspace,
+                      size_t workspace_bytes, void *stream);
 
 /* ---------------------------------------------------------------- (c) */
 

@@ -24,6 +24,7 @@ DT_META_NODES = 0
 DT_META_DEPTH = 1
 DT_META_LEAVES = 2
 DT_META_OVERFLOW = 3
+DT_META_P2M_UPTO = 5
 DT_META_LEVEL0 = 8
 DT_META_WORDS = 72
 DT_EVAL_COUNTER_BYTES = 65536
@@ -76,6 +77,11 @@ SIGNATURES = {
     "dt_build_tree": (
         C.c_int,
         [_P, _I64, _I64, _I64, _I64, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P],
+    ),
+    "dt_build_tree_p2m": (
+        C.c_int,
+        [_P, _P, _I64, _I64, _I64, _I64, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I64, _P,
+         _I64, _P, _P, _SZ, _P],
     ),
     "dt_moments_workspace": (_SZ, [_I64]),
     "dt_moments": (

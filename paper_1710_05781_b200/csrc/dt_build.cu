@@ -18,6 +18,7 @@
 #include <cooperative_groups.h>
 
 #include "dt_common.cuh"
+#include "dt_p2m.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -52,7 +53,54 @@ struct BuildArgs {
     double *dy_mid;          // [DYADIC] that midpoint
     int k_top;               // levels 0..k_top built in one pass (0: level by level)
     unsigned *irregular;     // set if some top dyadic interval has mid not strictly inside
+    // optional (dt_build_tree_p2m): while block 0 runs a sparse level run,
+    // the other blocks form the leaves of the finished levels (P2M)
+    int p2m_kmax;                    // 0: off, else 8/16/24/32 (order + 1 rounded up)
+    P2mArgs p2m;
+    unsigned long long *p2m_ctr;     // next 32-node chunk to form (zeroed per launch)
 };
+
+// One warp forms leaves of 32-node chunks below `upto` (final nodes: the
+// levels before block 0's current run), claimed with one atomicAdd each,
+// until the chunks run out or block 0 publishes `phase` on `flag`.  Claims
+// are contiguous from 0, so every chunk below min(counter, limit) was handed
+// out and is formed before the kernel ends.  (A CAS-bounded claim loop,
+// tried first, let 2352 warps hammer one L2 line and slowed block 0's own
+// traffic by ~1 ms.)
+template <int KMAX>
+__device__ void build_p2m_until(const BuildArgs &a, unsigned long long limit,
+                                unsigned long long phase, const unsigned long long *flag)
+{
+    constexpr int G = DT_P2M_G;
+    const int lane = dt_lane(), sub = lane & (G - 1), grp = lane / G;
+    while (true) {
+        long long c = -1;
+        if (lane == 0) {
+            unsigned long long v;
+            asm volatile("ld.acquire.gpu.u64 %0, [%1];" : "=l"(v) : "l"(flag) : "memory");
+            if (v < phase) {
+                const unsigned long long got = atomicAdd(a.p2m_ctr, 1ull);
+                c = got < limit ? (long long)got : -1;
+            }
+        }
+        c = __shfl_sync(DT_FULL, c, 0);
+        if (c < 0)
+            return;
+        const int64_t c0 = (int64_t)c * 32, mine = c0 + lane;
+        const bool leaf = __ldcg(a.left + mine) < 0 && __ldcg(a.right + mine) < 0;
+        unsigned leaves = __ballot_sync(DT_FULL, leaf);
+        while (leaves) {
+            unsigned m = leaves;
+            for (int i = 0; i < grp && m; ++i)
+                m &= m - 1;
+            const bool active = m != 0;
+            const int64_t node = c0 + (active ? __ffs(m) - 1 : 0);
+            for (int i = 0; i < 32 / G && leaves; ++i)
+                leaves &= leaves - 1;
+            p2m_split_leaf<G, KMAX, true>(a.p2m, node, active, sub);
+        }
+    }
+}
 
 // Splits of the top dyadic levels, all at once.  The bisection intervals do
 // not depend on the data (only which of them become nodes does), and for a
@@ -479,6 +527,7 @@ __global__ void __launch_bounds__(BUILD_THREADS) build_kernel(BuildArgs a)
     unsigned long long *const small_flag =
         reinterpret_cast<unsigned long long *>(a.block_total + 4095);
     unsigned long long small_phase = 0;
+    unsigned long long p2m_limit = 0;  // chunks of the first sparse run (0: none yet)
     if (blockIdx.x == 0 && threadIdx.x == 0)
         *small_flag = 0;
 #endif
@@ -575,6 +624,8 @@ __global__ void __launch_bounds__(BUILD_THREADS) build_kernel(BuildArgs a)
                     a.meta[DT_META_CURLEVEL] = l;
                 __threadfence();
             }
+            if (blockIdx.x == 0 && a.p2m_kmax && p2m_limit == 0 && f0 >= 32)
+                p2m_limit = (unsigned long long)(f0 / 32);  // as the other blocks
 #if DT_BUILD_FLAGWAIT
             // block 0 announces the end of its run with a release store; the
             // other blocks wait on it with back-off instead of polling a grid
@@ -586,6 +637,17 @@ __global__ void __launch_bounds__(BUILD_THREADS) build_kernel(BuildArgs a)
                     asm volatile("st.release.gpu.u64 [%0], %1;" ::"l"(small_flag), "l"(small_phase)
                                  : "memory");
             } else {
+                if (a.p2m_kmax && p2m_limit == 0 && f0 >= 32) {
+                    // meanwhile (the first run with whole chunks before it
+                    // only): form the leaves of the levels before this run
+                    p2m_limit = (unsigned long long)(f0 / 32);
+                    switch (a.p2m_kmax) {
+                    case 8: build_p2m_until<8>(a, p2m_limit, small_phase, small_flag); break;
+                    case 16: build_p2m_until<16>(a, p2m_limit, small_phase, small_flag); break;
+                    case 24: build_p2m_until<24>(a, p2m_limit, small_phase, small_flag); break;
+                    default: build_p2m_until<32>(a, p2m_limit, small_phase, small_flag); break;
+                    }
+                }
                 if (threadIdx.x == 0) {
                     unsigned long long v;
                     while (true) {
@@ -674,6 +736,11 @@ __global__ void __launch_bounds__(BUILD_THREADS) build_kernel(BuildArgs a)
         grid.sync();
         ++lev;
     }
+    // every chunk below min(claims, limit) is formed before the kernel ends
+    if (a.p2m_kmax && blockIdx.x == 0 && threadIdx.x == 0) {
+        const unsigned long long got = *(volatile unsigned long long *)a.p2m_ctr;
+        a.meta[DT_META_P2M_UPTO] = (int64_t)(32 * (got < p2m_limit ? got : p2m_limit));
+    }
 }
 
 }  // namespace
@@ -682,14 +749,15 @@ extern "C" size_t dt_build_workspace(int64_t n, int64_t node_capacity)
 {
     (void)n;
     return (size_t)node_capacity * 2 * sizeof(int32_t) + 4096 * sizeof(int64_t) + 16 +
-           (size_t)DYADIC * (sizeof(int64_t) + sizeof(double)) + 16;
+           (size_t)DYADIC * (sizeof(int64_t) + sizeof(double)) + 32;
 }
 
-extern "C" int dt_build_tree(const double *xs, int64_t n, int64_t leaf_capacity, int64_t max_depth, int64_t node_capacity,
-                             double *lo, double *hi, double *center, double *half,
-                             int64_t *level, int64_t *start, int64_t *end, int64_t *left,
-                             int64_t *right, void *packed, int64_t *meta, void *workspace,
-                             size_t workspace_bytes, void *stream)
+static int build_launch(const double *xs, int64_t n, int64_t leaf_capacity, int64_t max_depth,
+                        int64_t node_capacity, double *lo, double *hi, double *center,
+                        double *half, int64_t *level, int64_t *start, int64_t *end,
+                        int64_t *left, int64_t *right, void *packed, int64_t *meta,
+                        void *workspace, size_t workspace_bytes, void *stream,
+                        const P2mArgs *p2m)
 {
     DT_CHECK_ARG(n > 0, "cannot build a tree over an empty charge system");
     DT_CHECK_ARG(n < (int64_t)1 << 31, "n must be < 2^31");
@@ -740,7 +808,15 @@ extern "C" int dt_build_tree(const double *xs, int64_t n, int64_t leaf_capacity,
                 a.k_top = K;
                 break;
             }
-    DT_CUDA_TRY(cudaMemsetAsync(a.irregular, 0, sizeof(unsigned), (cudaStream_t)stream));
+    a.p2m_ctr = (unsigned long long *)(a.irregular + 2);
+    a.p2m_kmax = 0;
+    if (p2m) {
+        a.p2m = *p2m;
+        const int64_t o1 = p2m->order + 1;
+        a.p2m_kmax = o1 <= 8 ? 8 : o1 <= 16 ? 16 : o1 <= 24 ? 24 : 32;
+    }
+    // the irregular flag and the chunk counter
+    DT_CUDA_TRY(cudaMemsetAsync(a.irregular, 0, 16, (cudaStream_t)stream));
 
     int dev = 0, per_sm = 0;
     DT_CUDA_TRY(cudaGetDevice(&dev));
@@ -761,4 +837,36 @@ extern "C" int dt_build_tree(const double *xs, int64_t n, int64_t leaf_capacity,
     DT_CUDA_TRY(cudaLaunchCooperativeKernel((const void *)build_kernel, grid, BUILD_THREADS, args,
                                             smem, (cudaStream_t)stream));
     return DT_OK;
+}
+
+extern "C" int dt_build_tree(const double *xs, int64_t n, int64_t leaf_capacity, int64_t max_depth,
+                             int64_t node_capacity, double *lo, double *hi, double *center,
+                             double *half, int64_t *level, int64_t *start, int64_t *end,
+                             int64_t *left, int64_t *right, void *packed, int64_t *meta,
+                             void *workspace, size_t workspace_bytes, void *stream)
+{
+    return build_launch(xs, n, leaf_capacity, max_depth, node_capacity, lo, hi, center, half,
+                        level, start, end, left, right, packed, meta, workspace, workspace_bytes,
+                        stream, nullptr);
+}
+
+extern "C" int dt_build_tree_p2m(const double *xs, const double *qs, int64_t n,
+                                 int64_t leaf_capacity, int64_t max_depth, int64_t node_capacity,
+                                 double *lo, double *hi, double *center, double *half,
+                                 int64_t *level, int64_t *start, int64_t *end, int64_t *left,
+                                 int64_t *right, void *packed, int64_t *meta, int64_t order,
+                                 double *moments_eval, int64_t eval_stride, double *xq,
+                                 void *workspace, size_t workspace_bytes, void *stream)
+{
+    DT_CHECK_ARG(order >= 0 && order + 1 <= 32, "dt_build_tree_p2m needs moment order <= 31");
+    DT_CHECK_ARG(qs && moments_eval && xq, "null pointer");
+    DT_CHECK_ARG(eval_stride >= order + 1 && eval_stride % 2 == 0,
+                 "eval_stride must be even and >= order + 1");
+    DT_CHECK_ARG(((uintptr_t)moments_eval & 15) == 0 && ((uintptr_t)xq & 15) == 0,
+                 "moments_eval and xq must be 16-byte aligned");
+    const P2mArgs p2m{xs, qs, center, start, end, order, moments_eval, eval_stride,
+                      (double2 *)xq};
+    return build_launch(xs, n, leaf_capacity, max_depth, node_capacity, lo, hi, center, half,
+                        level, start, end, left, right, packed, meta, workspace, workspace_bytes,
+                        stream, &p2m);
 }

@@ -32,13 +32,8 @@
 
 #include "dt_common.cuh"
 #include "dt_farcoef.cuh"
+#include "dt_p2m.cuh"
 
-#ifndef DT_P2M_PREFETCH
-#define DT_P2M_PREFETCH 1
-#endif
-#ifndef DT_P2M_G
-#define DT_P2M_G 2
-#endif
 
 namespace {
 
@@ -281,160 +276,6 @@ __global__ void __launch_bounds__(MOM_THREADS) moments_kernel(MomArgs a)
 // (up_level_threads, shard_finish) do exactly that, so the rows are
 // bit-identical whichever form (and whichever rank) produced them.
 
-// P2M of one leaf over G lanes: raw power sums S_k = sum q (x - c)^k for
-// k < KMAX, with the powers split as t^(8m + r) = t^r (t^8)^m: per source 7
-// products q t^r, t^8 and its powers, 8 additions and KMAX - 8 FMAs (44 FP64
-// operations at KMAX = 32 instead of 64 for the running-product form).  Two
-// sources per trip; then a butterfly over the G lanes.  Lane `sub` stores
-// orders [sub KMAX/G, (sub + 1) KMAX/G) of the row (16-byte stores; orders
-// >= order + 1 are the row's zero padding).
-template <int G, int KMAX>
-__device__ __forceinline__ void p2m_split_leaf(const MomArgs &a, int64_t node, bool active,
-                                               int sub)
-{
-    static_assert(KMAX % 8 == 0 && KMAX >= 8, "KMAX must be a multiple of 8");
-    constexpr int NM = KMAX / 8;
-    int64_t s = 0, e = 0;
-    double c = 0.0;
-    if (active) {
-        s = __ldg(a.start + node);
-        e = __ldg(a.end + node);
-        c = __ldg(a.center + node);
-    }
-    double acc[KMAX];
-#pragma unroll
-    for (int k = 0; k < KMAX; ++k)
-        acc[k] = 0.0;
-    int64_t j = s + sub;
-#if DT_P2M_PREFETCH
-    // the next pair's loads are issued before this pair's arithmetic
-    bool have = j + G < e;
-    double cx0 = 0.0, cx1 = 0.0, cq0 = 0.0, cq1 = 0.0;
-    if (have) {
-        cx0 = __ldg(a.xs + j);
-        cx1 = __ldg(a.xs + j + G);
-        cq0 = __ldg(a.qs + j);
-        cq1 = __ldg(a.qs + j + G);
-    }
-    while (have) {
-        const int64_t jn = j + 2 * G;
-        const bool hn = jn + G < e;
-        double nx0 = 0.0, nx1 = 0.0, nq0 = 0.0, nq1 = 0.0;
-        if (hn) {
-            nx0 = __ldg(a.xs + jn);
-            nx1 = __ldg(a.xs + jn + G);
-            nq0 = __ldg(a.qs + jn);
-            nq1 = __ldg(a.qs + jn + G);
-        }
-        if (a.xq) {  // the traversal's interleaved (x, q), every source written once
-            a.xq[j] = make_double2(cx0, cq0);
-            a.xq[j + G] = make_double2(cx1, cq1);
-        }
-        const double t0 = cx0 - c, t1 = cx1 - c;
-        double p0[8], p1[8];
-        p0[0] = cq0;
-        p1[0] = cq1;
-        cx0 = nx0;
-        cx1 = nx1;
-        cq0 = nq0;
-        cq1 = nq1;
-        j = jn;
-        have = hn;
-#else
-    for (; j + G < e; j += 2 * G) {
-        const double x0 = __ldg(a.xs + j), x1 = __ldg(a.xs + j + G);
-        const double t0 = x0 - c, t1 = x1 - c;
-        double p0[8], p1[8];
-        p0[0] = __ldg(a.qs + j);
-        p1[0] = __ldg(a.qs + j + G);
-        if (a.xq) {
-            a.xq[j] = make_double2(x0, p0[0]);
-            a.xq[j + G] = make_double2(x1, p1[0]);
-        }
-#endif
-#pragma unroll
-        for (int r = 1; r < 8; ++r) {
-            p0[r] = p0[r - 1] * t0;
-            p1[r] = p1[r - 1] * t1;
-        }
-#pragma unroll
-        for (int r = 0; r < 8; ++r)
-            acc[r] += p0[r] + p1[r];
-        if (NM > 1) {
-            const double u0 = t0 * t0, u1 = t1 * t1;
-            const double v0 = u0 * u0, v1 = u1 * u1;
-            const double w0 = v0 * v0, w1 = v1 * v1;  // t^8
-            double b0 = w0, b1 = w1;
-#pragma unroll
-            for (int m = 1; m < NM; ++m) {
-#pragma unroll
-                for (int r = 0; r < 8; ++r)
-                    acc[8 * m + r] = __fma_rn(p1[r], b1, __fma_rn(p0[r], b0, acc[8 * m + r]));
-                if (m + 1 < NM) {
-                    b0 *= w0;
-                    b1 *= w1;
-                }
-            }
-        }
-    }
-    if (j < e) {
-        const double x0 = __ldg(a.xs + j);
-        const double t0 = x0 - c;
-        double p0[8];
-        p0[0] = __ldg(a.qs + j);
-        if (a.xq)
-            a.xq[j] = make_double2(x0, p0[0]);
-#pragma unroll
-        for (int r = 1; r < 8; ++r)
-            p0[r] = p0[r - 1] * t0;
-#pragma unroll
-        for (int r = 0; r < 8; ++r)
-            acc[r] += p0[r];
-        if (NM > 1) {
-            const double u0 = t0 * t0, v0 = u0 * u0, w0 = v0 * v0;
-            double b0 = w0;
-#pragma unroll
-            for (int m = 1; m < NM; ++m) {
-#pragma unroll
-                for (int r = 0; r < 8; ++r)
-                    acc[8 * m + r] = __fma_rn(p0[r], b0, acc[8 * m + r]);
-                if (m + 1 < NM)
-                    b0 *= w0;
-            }
-        }
-    }
-#pragma unroll
-    for (int k = 0; k < KMAX; ++k) {
-#pragma unroll
-        for (int o = G / 2; o > 0; o >>= 1)
-            acc[k] += __shfl_xor_sync(DT_FULL, acc[k], o);
-    }
-    if (!active)
-        return;
-    const int o1 = (int)a.order + 1;
-    double2 *row = reinterpret_cast<double2 *>(a.meval + node * a.estride);
-    constexpr int PER = KMAX / G;
-#pragma unroll
-    for (int k = 0; k < KMAX; k += 2) {
-        if (k / PER == sub && k < a.estride) {
-            const double v0 = k < o1 ? (k == 0 ? acc[0] : __dmul_rn(acc[k], c_mev_s[k])) : 0.0;
-            const double v1 = k + 1 < o1 ? __dmul_rn(acc[k + 1], c_mev_s[k + 1]) : 0.0;
-            row[k >> 1] = make_double2(v0, v1);
-        }
-    }
-}
-
-// Arrival on a node's counter with acquire-release semantics at GPU scope:
-// the release publishes the rows this warp wrote (ordered before it by a
-// __syncwarp), the acquire makes the rows behind earlier arrivals visible to
-// the lane that completes the node (and, after a __syncwarp, to its warp).
-__device__ __forceinline__ int arrive_acq_rel(int32_t *p)
-{
-    int old;
-    asm volatile("atom.add.acq_rel.gpu.s32 %0, [%1], 1;" : "=r"(old) : "l"(p) : "memory");
-    return old;
-}
-
 // ---- M2M: two lanes per node (or one thread), raw sums in registers ----
 //
 // Child shift: a child row (M basis) is
@@ -533,6 +374,10 @@ __global__ void __launch_bounds__(256, DT_UP_MINB) upward_kernel(MomArgs a)
     const int warp = threadIdx.x >> 5;
     const int lane = dt_lane();
     const int sub = lane & (G - 1), grp = lane / G;
+    const P2mArgs p2m{a.xs, a.qs, a.center, a.start, a.end, a.order, a.meval, a.estride, a.xq};
+    // leaves below this node index were formed by the build's idle blocks
+    // (dt_build_tree_p2m); they only climb here
+    const int64_t preformed = a.plan ? 0 : __ldg(a.meta + DT_META_P2M_UPTO);
     const int64_t n = __ldg(a.meta + DT_META_NODES);
     int64_t cut_begin = 0, lo = 0, hi = 0;
     if (a.plan) {
@@ -557,7 +402,7 @@ __global__ void __launch_bounds__(256, DT_UP_MINB) upward_kernel(MomArgs a)
             const bool in = !a.plan ||
                             (__ldg(a.start + mine) >= lo && __ldg(a.end + mine) <= hi);
             // leaves above the cut are formed by every rank; they never climb
-            form = in || mine < cut_begin;
+            form = (in || mine < cut_begin) && mine >= preformed;
             par = __ldcg(a.parent + mine);
             climb = in && par >= cut_begin && par >= 0;
 #if DT_UP_NOCLIMB
@@ -574,7 +419,7 @@ __global__ void __launch_bounds__(256, DT_UP_MINB) upward_kernel(MomArgs a)
             const int64_t node = c0 + (active ? __ffs(m) - 1 : 0);
             for (int i = 0; i < 32 / G && leaves; ++i)
                 leaves &= leaves - 1;
-            p2m_split_leaf<G, KMAX>(a, node, active, sub);
+            p2m_split_leaf<G, KMAX, false>(p2m, node, active, sub);
         }
         // Climb in rounds over a frontier of formed nodes, kept sorted and
         // compacted in the lanes, so siblings sit in adjacent lanes: a pair of

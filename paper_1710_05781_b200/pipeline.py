@@ -131,7 +131,11 @@ class TreePipeline:
         # already running.
         _lib.check(L.dt_prefix_scan(p(qs), p(self.prefix), self.n, p(self.scan_ws),
                                     self.scan_ws_bytes, s), "dt_prefix_scan")
-        self.bufs.launch(xs, cfg.leaf_capacity)
+        if self.shard is None and self.order + 1 <= 32:
+            # the build's idle blocks start the P2M of the finished levels
+            self.bufs.launch(xs, cfg.leaf_capacity, p2m=(qs, self.order, self.meval, self.xq))
+        else:
+            self.bufs.launch(xs, cfg.leaf_capacity)
         self.ev_scan.record(main)
         self.side.wait_event(self.ev_scan)
         with torch.cuda.stream(self.side):

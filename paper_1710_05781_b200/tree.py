@@ -189,9 +189,25 @@ class TreeBuffers:
         self.mws_bytes = int(L.dt_moments_workspace(capacity))
         self.mws = torch.empty(self.mws_bytes, dtype=torch.uint8, device=device)
 
-    def launch(self, xs: torch.Tensor, leaf_capacity: int, max_depth: int = MAX_DEPTH) -> None:
+    def launch(self, xs: torch.Tensor, leaf_capacity: int, max_depth: int = MAX_DEPTH,
+               p2m=None) -> None:
+        """dt_build_tree; with p2m = (qs, order, meval, xq) the build's idle
+        blocks also form the leaves of finished levels (dt_build_tree_p2m)."""
         L = _lib.load()
         p = _lib.ptr
+        if p2m is not None:
+            qs, order, meval, xq = p2m
+            _lib.check(
+                L.dt_build_tree_p2m(
+                    p(xs), p(qs), self.n, int(leaf_capacity), int(max_depth), self.capacity,
+                    p(self.lo), p(self.hi), p(self.center), p(self.half), p(self.level),
+                    p(self.start), p(self.end), p(self.left), p(self.right), p(self.packed),
+                    p(self.meta), int(order), p(meval), meval.shape[1], p(xq), p(self.ws),
+                    self.ws_bytes, _lib.stream_handle(),
+                ),
+                "dt_build_tree_p2m",
+            )
+            return
         _lib.check(
             L.dt_build_tree(
                 p(xs), self.n, int(leaf_capacity), int(max_depth), self.capacity, p(self.lo),
@@ -267,20 +283,27 @@ def _build(system: ChargeSystem, config: EvalConfig, upward) -> Tree:
     torch.cuda.synchronize(dev)
     t0 = time.perf_counter()
     n = len(system)
+    order = moment_order_for(config)
+    # orders <= 31 on one device: the build's idle blocks start the leaves'
+    # P2M (rows of up to capacity nodes; the tree keeps the first n_nodes)
+    fused = upward is None and order + 1 <= 32
+    xq = torch.empty(2 * n, dtype=torch.float64, device=dev)
     cap = initial_node_capacity(n, config.leaf_capacity)
     while True:
         bufs = TreeBuffers(n, cap, dev)
-        bufs.launch(system.xs, config.leaf_capacity)
+        meval = (torch.empty((cap, eval_stride(order)), dtype=torch.float64, device=dev)
+                 if fused else None)
+        bufs.launch(system.xs, config.leaf_capacity,
+                    p2m=(system.qs, order, meval, xq) if fused else None)
         meta = bufs.meta[:8].cpu().tolist()
         if not meta[_lib.DT_META_OVERFLOW]:
             break
         cap *= 4
     n_nodes = int(meta[_lib.DT_META_NODES])
-    order = moment_order_for(config)
     moments = (torch.empty((n_nodes, order + 1), dtype=torch.float64, device=dev)
                if order + 1 > 32 else None)
-    meval = torch.empty((n_nodes, eval_stride(order)), dtype=torch.float64, device=dev)
-    xq = torch.empty(2 * n, dtype=torch.float64, device=dev)
+    if meval is None:
+        meval = torch.empty((n_nodes, eval_stride(order)), dtype=torch.float64, device=dev)
     if upward is None:  # moments and the traversal's (x, q) pairs in one pass
         launch_moments(bufs, system.xs, system.qs, order, moments, meval, xq=xq)
     else:
@@ -295,7 +318,7 @@ def _build(system: ChargeSystem, config: EvalConfig, upward) -> Tree:
         end=bufs.end[:n_nodes], left=bufs.left[:n_nodes], right=bufs.right[:n_nodes],
         moment_order=order, depth=int(meta[_lib.DT_META_DEPTH]),
         leaf_count=int(meta[_lib.DT_META_LEAVES]), build_seconds=elapsed,
-        meval=meval, packed=bufs.packed[: n_nodes * 32], xq=xq, meta=bufs.meta,
+        meval=meval[:n_nodes], packed=bufs.packed[: n_nodes * 32], xq=xq, meta=bufs.meta,
         moments_ref=moments,
     )
 

@@ -64,6 +64,20 @@ for i in range(reps):
     assert torch.equal(cur, ref), f"upward pass differs at rep {i}"
 report["upward"] = {"identical_finite_runs": reps}
 
+# the build's idle-block P2M followed by the rest of the upward pass
+xq = torch.empty(2 * len(xs), dtype=torch.float64, device="cuda")
+for i in range(reps):
+    me.fill_(float("nan"))
+    xq.fill_(float("nan"))
+    bufs.launch(xs, cfg.leaf_capacity, p2m=(qs, order, me, xq))
+    launch_moments(bufs, xs, qs, order, None, me, xq=xq)
+    cur = me[:n_nodes].clone()
+    assert bool(torch.isfinite(cur).all()), f"build + upward read an unpublished row (rep {i})"
+    assert torch.equal(cur, ref), f"build-time P2M rows differ at rep {i}"
+    assert bool(torch.isfinite(xq).all())
+report["build_p2m"] = {"identical_finite_runs": reps,
+                       "preformed_nodes": int(bufs.meta[_lib.DT_META_P2M_UPTO])}
+
 # prefix scan
 ref = None
 for i in range(reps):
