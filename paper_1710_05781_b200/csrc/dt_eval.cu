@@ -52,6 +52,12 @@ namespace {
 #define DT_EVAL_SEGMENTS 148  // per-SM task segments (0: one global counter)
 #endif
 static_assert(DT_EVAL_SEGMENTS * 4 <= DT_EVAL_COUNTER_BYTES, "counter slot too small");
+#ifndef DT_EVAL_SP
+#define DT_EVAL_SP 1  // the warp stack walked by a shared-memory pointer above a sentinel
+#endif
+#ifndef DT_EVAL_FAR2
+#define DT_EVAL_FAR2 1  // far field: orders 1 and 2 through the recurrence
+#endif
 #ifndef DT_EVAL_UTIL
 #define DT_EVAL_UTIL 0  // development: lane-utilisation counters (variant builds only)
 #endif
@@ -728,6 +734,69 @@ __device__ __forceinline__ int psel_table(double R, int hiR, double h, const uns
 // the rest up to the warp maximum is masked per lane.  Even orders go to acc
 // and odd ones to acc1 on both paths, so a target's result depends on its
 // own p only, not on which warp (pmin, pmax) evaluated it.
+#if DT_EVAL_FAR2
+template <bool WIDE>
+__device__ __forceinline__ double far_field(double d, double rd2, const double2 *__restrict__ M2,
+                                            int pu, int pmin, int pmax)
+{
+    const double s2 = __fma_rn(d, d, rd2);
+    const double r = dt_rsqrt(s2);
+    const double w = r * r;
+    const double u = d * w;
+    double acc = (d * r) * __ldg(M2).x;
+    double acc1 = 0.0;
+    // Start values below order 1 chosen so that the recurrence itself yields
+    // h_1 = (r_d^2 r) w and h_2 = (-3 u) h_1 with the same roundings (c_1 = 0,
+    // c_2 = -3): h_(-1) = -(r_d^2 r), h_0' = 0.  Orders 1 and 2 then need no
+    // special case.
+    double hm2 = -(rd2 * r), hm1 = 0.0;
+    int k = 1;
+#define DT_FAR_STEP(KK, H2, H1, OUT)                                              \
+    const double OUT = __fma_rn(u * c_hcoef[(KK) + 1], H1, -(w * H2));
+    if (!WIDE) {
+        // unmasked pairs (odd, even): the two recurrence values swap roles
+        // every order, so each pair ends with them back in place
+#pragma unroll
+        for (int kk = 1; kk + 1 <= 31; kk += 2) {
+            if (kk + 1 > pmin)
+                break;
+            DT_FAR_STEP(kk, hm2, hm1, v0)
+            DT_FAR_STEP(kk + 1, hm1, v0, v1)
+            // kk odd: M_kk = M2[kk / 2].y, M_(kk+1) = M2[(kk + 1) / 2].x
+            acc1 = __fma_rn(v0, __ldg(M2 + kk / 2).y, acc1);
+            acc = __fma_rn(v1, __ldg(M2 + (kk + 1) / 2).x, acc);
+            hm2 = v0;
+            hm1 = v1;
+        }
+        // the pairs above ran for kk = 1, 3, .. while kk + 1 <= min(pmin, 31)
+        k = 1 + (min(pmin, 31) & ~1);
+    }
+    const double *M = reinterpret_cast<const double *>(M2);
+#pragma unroll 1
+    for (; k <= pmax; k += 2) {
+        DT_FAR_STEP(k, hm2, hm1, t0)
+        if (k <= pu) {
+            if (k & 1)
+                acc1 = __fma_rn(t0, __ldg(M + k), acc1);
+            else
+                acc = __fma_rn(t0, __ldg(M + k), acc);
+        }
+        if (k + 1 > pmax)
+            break;
+        DT_FAR_STEP(k + 1, hm1, t0, t1)
+        if (k + 1 <= pu) {
+            if ((k + 1) & 1)
+                acc1 = __fma_rn(t1, __ldg(M + k + 1), acc1);
+            else
+                acc = __fma_rn(t1, __ldg(M + k + 1), acc);
+        }
+        hm2 = t0;
+        hm1 = t1;
+    }
+#undef DT_FAR_STEP
+    return acc + acc1;
+}
+#else
 template <bool WIDE>
 __device__ __forceinline__ double far_field(double d, double rd2, const double2 *__restrict__ M2,
                                             int pu, int pmin, int pmax)
@@ -796,6 +865,7 @@ __device__ __forceinline__ double far_field(double d, double rd2, const double2 
 #undef DT_FAR_STEP
     return acc + acc1;
 }
+#endif
 
 // acc + q (x - y) / sqrt((x - y)^2 + r_d^2) (nvcc contracts the final
 // product and sum into one DFMA): 9 FP64 instructions + MUFU
@@ -981,11 +1051,19 @@ __global__ void __launch_bounds__(EVAL_THREADS, DT_EVAL_MINB) tree_eval_kernel(E
         // pending right siblings go on the warp's stack in shared memory
         // (depth <= 60).  Every lane stores the same entry and reads back
         // its own store, so no warp barrier is needed.
+#if DT_EVAL_SP
+        // sp points at the top entry; entry 0 is a sentinel with an empty
+        // mask (a pushed entry always has a lane), so the walk ends when it
+        // pops the sentinel and no base address or index stays live
+        uint2 *sp = stack_s[threadIdx.x >> 5];
+        *sp = make_uint2(0u, 0u);
+#else
         int top = -1;
+        uint2 *const stk = stack_s[threadIdx.x >> 5];
+#endif
 #if DT_EVAL_UTIL
         unsigned long long u_[12] = {0};
 #endif
-        uint2 *const stk = stack_s[threadIdx.x >> 5];
         int node = 0;
         unsigned mask = __ballot_sync(DT_FULL, live);
         while (true) {
@@ -1062,16 +1140,27 @@ __global__ void __launch_bounds__(EVAL_THREADS, DT_EVAL_MINB) tree_eval_kernel(E
                         }
                     }
                 } else {
-                    if (lr.x >= 0 && lr.y >= 0)  // right sibling waits on the stack
+                    if (lr.x >= 0 && lr.y >= 0) {  // right sibling waits on the stack
+#if DT_EVAL_SP
+                        *++sp = make_uint2((unsigned)lr.y, rest);
+#else
                         stk[++top] = make_uint2((unsigned)lr.y, rest);
+#endif
+                    }
                     node = lr.x >= 0 ? lr.x : lr.y;
                     mask = rest;
                     continue;
                 }
             }
+#if DT_EVAL_SP
+            const uint2 e = *sp--;
+            if (e.y == 0u)
+                break;
+#else
             if (top < 0)
                 break;
             const uint2 e = stk[top--];
+#endif
             node = (int)e.x;
             mask = e.y;
         }
