@@ -138,8 +138,8 @@ __device__ void write_node(const BuildArgs &a, int64_t c, double lo, double hi, 
         dt_node nd;
         nd.center = ctr;
         nd.half = hw;
-        nd.left = -1;
-        nd.right = -1;
+        nd.first = -1;
+        nd.second = -1;
         nd.start = (int32_t)s;
         nd.end = (int32_t)e;
         a.packed[c] = nd;
@@ -276,8 +276,7 @@ __device__ void emit_children(const BuildArgs &a, int64_t node, int64_t lev, int
     a.left[node] = l_slot;
     a.right[node] = r_slot;
     if (a.packed) {
-        a.packed[node].left = (int32_t)l_slot;
-        a.packed[node].right = (int32_t)r_slot;
+        dt_node_children(a.packed[node], l_slot, r_slot);
     }
 }
 
@@ -478,8 +477,7 @@ __device__ int64_t build_top(const BuildArgs &a, cg::grid_group &grid, int *warp
             a.left[c] = l_slot;
             a.right[c] = r_slot;
             if (a.packed) {
-                a.packed[c].left = (int32_t)l_slot;
-                a.packed[c].right = (int32_t)r_slot;
+                dt_node_children(a.packed[c], l_slot, r_slot);
             }
         }
     }

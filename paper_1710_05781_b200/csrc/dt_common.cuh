@@ -32,15 +32,24 @@ int dt_set_error(int code, const char *msg);
 static_assert(DT_META_LEVEL0 + DT_MAX_LEVELS + 1 <= DT_META_WORDS, "meta layout");
 
 // Packed node record consumed by the traversal kernel: one 32-byte sector.
+// The children are stored in visit order: `first` is the left child if there
+// is one, else the right one (-1: leaf); `second` is the right child when
+// both exist (the one the walk defers), else -1.
 struct __align__(16) dt_node {
     double center;
     double half;
-    int32_t left;
-    int32_t right;
+    int32_t first;
+    int32_t second;
     int32_t start;
     int32_t end;
 };
 static_assert(sizeof(dt_node) == 32, "dt_node must be one sector");
+
+__device__ __forceinline__ void dt_node_children(dt_node &nd, int64_t left, int64_t right)
+{
+    nd.first = (int32_t)(left >= 0 ? left : right);
+    nd.second = (int32_t)(left >= 0 && right >= 0 ? right : -1);
+}
 
 // Fast fp64 reciprocal square root: MUFU seed + one cubic Newton step.
 // Inputs are finite and > 0 on every call site (s = d^2 + r_d^2, r_d > 0).

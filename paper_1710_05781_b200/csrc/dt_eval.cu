@@ -58,6 +58,15 @@ static_assert(DT_EVAL_SEGMENTS * 4 <= DT_EVAL_COUNTER_BYTES, "counter slot too s
 #ifndef DT_EVAL_FAR2
 #define DT_EVAL_FAR2 1  // far field: orders 1 and 2 through the recurrence
 #endif
+#ifndef DT_EVAL_LANEBIT
+#define DT_EVAL_LANEBIT 1  // lane bit held in a register (asm, not rematerialised)
+#endif
+#ifndef DT_EVAL_PREFETCH
+#define DT_EVAL_PREFETCH 0  // claim the next task while the current one runs
+#endif
+#ifndef DT_EVAL_PBADDR
+#define DT_EVAL_PBADDR 0  // order bins read through a 32-bit shared address held in a register
+#endif
 #ifndef DT_EVAL_UTIL
 #define DT_EVAL_UTIL 0  // development: lane-utilisation counters (variant builds only)
 #endif
@@ -697,14 +706,24 @@ static_assert(PT_BINS_OFFSET + PT_LEVELS * PT_BINS <= DT_EVAL_COUNTER_BYTES,
 // p from the bins, or -1 (use psel_fast): integer arithmetic on the high
 // words of R and h (hi0 = hi(h0), jbase = pt_jbase(theta)), one shared-memory
 // byte, at most one double comparison
+#if DT_EVAL_PBADDR
+__device__ __forceinline__ int psel_table(double R, int hiR, double h, unsigned bins,
+                                          const double *bp, int hi0, int jbase)
+#else
 __device__ __forceinline__ int psel_table(double R, int hiR, double h, const unsigned char *bins,
                                           const double *bp, int hi0, int jbase)
+#endif
 {
     const int L = pt_level(hi0, h);
     const int j = ((hiR - (hi0 - (L << 20))) >> 13) - jbase;
     if (!((unsigned)L < (unsigned)PT_LEVELS && (unsigned)j < (unsigned)PT_BINS))
         return -1;
+#if DT_EVAL_PBADDR
+    unsigned e;
+    asm("ld.shared.u8 %0, [%1];" : "=r"(e) : "r"(bins + (unsigned)(L * PT_BINS + j)));
+#else
     const unsigned e = bins[L * PT_BINS + j];
+#endif
     if (e < PT_SPLIT)
         return (int)e;
     if (e == PT_FALLBACK)
@@ -989,7 +1008,15 @@ __global__ void __launch_bounds__(EVAL_THREADS, DT_EVAL_MINB) tree_eval_kernel(E
             dst[i] = src[i];
     }
     const int phi0 = __double2hiint(__ldg(&a.nodes[0].half));
-    const int pjb = pt_jbase(a.theta);
+    // without tables the bin index is pushed out of range (psel_table
+    // returns -1 for every pair), so the walk needs no table_ok branch
+    const int pjb = table_ok ? pt_jbase(a.theta) : -(1 << 30);
+#if DT_EVAL_PBADDR
+    unsigned pbins_a = (unsigned)__cvta_generic_to_shared(pbins_s);
+    asm volatile("" : "+r"(pbins_a));  // kept in a register, not rematerialised
+#else
+    const unsigned char *const pbins_a = pbins_s;
+#endif
     __syncthreads();
 
 #if DT_EVAL_SEGMENTS
@@ -1001,6 +1028,13 @@ __global__ void __launch_bounds__(EVAL_THREADS, DT_EVAL_MINB) tree_eval_kernel(E
     unsigned *const seg_ctr = reinterpret_cast<unsigned *>(a.counter);
     int seg = (int)(dt_smid() % DT_EVAL_SEGMENTS);
     int seg_left = DT_EVAL_SEGMENTS;
+#if DT_EVAL_PREFETCH
+    // lane 0 holds the task of segment seg claimed ahead, so the atomic's
+    // round trip overlaps the current task
+    unsigned pre = 0;
+    if (lane == 0)
+        pre = atomicAdd(seg_ctr + seg, 1u);
+#endif
 #endif
     while (true) {
         unsigned long long base = 0;
@@ -1008,6 +1042,19 @@ __global__ void __launch_bounds__(EVAL_THREADS, DT_EVAL_MINB) tree_eval_kernel(E
 #if DT_EVAL_SEGMENTS
             const int64_t s0 = n_tasks * seg / DT_EVAL_SEGMENTS;
             const int64_t s1 = n_tasks * (seg + 1) / DT_EVAL_SEGMENTS;
+#if DT_EVAL_PREFETCH
+            const unsigned t = __shfl_sync(DT_FULL, pre, 0);
+            if ((int64_t)t >= s1 - s0) {
+                if (--seg_left == 0)
+                    break;
+                seg = seg + 1 == DT_EVAL_SEGMENTS ? 0 : seg + 1;
+                if (lane == 0)
+                    pre = atomicAdd(seg_ctr + seg, 1u);
+                continue;
+            }
+            if (lane == 0)
+                pre = atomicAdd(seg_ctr + seg, 1u);
+#else
             unsigned t = 0;
             if (lane == 0)
                 t = atomicAdd(seg_ctr + seg, 1u);
@@ -1018,6 +1065,7 @@ __global__ void __launch_bounds__(EVAL_THREADS, DT_EVAL_MINB) tree_eval_kernel(E
                 seg = seg + 1 == DT_EVAL_SEGMENTS ? 0 : seg + 1;
                 continue;
             }
+#endif
             base = (unsigned long long)(s0 + t) * 32ull;
 #else
             if (lane == 0)
@@ -1066,12 +1114,19 @@ __global__ void __launch_bounds__(EVAL_THREADS, DT_EVAL_MINB) tree_eval_kernel(E
 #endif
         int node = 0;
         unsigned mask = __ballot_sync(DT_FULL, live);
+#if DT_EVAL_LANEBIT
+        unsigned lanebit;
+        asm volatile("mov.u32 %0, %%lanemask_eq;" : "=r"(lanebit));
+#define DT_LANE_IN(m) (((m) & lanebit) != 0u)
+#else
+#define DT_LANE_IN(m) ((((m) >> lane) & 1u) != 0u)
+#endif
         while (true) {
             const double4 raw0 = dt_ldg256(a.nodes + node);  // one 256-bit load
             const double center = raw0.x, half = raw0.y;
             const int2 lr = make_int2(__double2loint(raw0.z), __double2hiint(raw0.z));
             const int2 se = make_int2(__double2loint(raw0.w), __double2hiint(raw0.w));
-            const bool act = (mask >> lane) & 1u;
+            const bool act = DT_LANE_IN(mask);
             const double d = center - y;
             const double big_r = fabs(d);
             const bool far = act && big_r > 0.0 && half <= __dmul_rn(a.theta, big_r);
@@ -1081,9 +1136,8 @@ __global__ void __launch_bounds__(EVAL_THREADS, DT_EVAL_MINB) tree_eval_kernel(E
                 int pu = -1;
                 if (far) {
                     if (ADAPTIVE) {
-                        int r = table_ok ? psel_table(big_r, __double2hiint(d) & 0x7fffffff, half, pbins_s,
-                                                      a.pt_bp, phi0, pjb)
-                                         : -1;
+                        int r = psel_table(big_r, __double2hiint(d) & 0x7fffffff, half, pbins_a,
+                                           a.pt_bp, phi0, pjb);
                         UTIL_ADD(10, 1);
                         UTIL_ADD(11, r < 0);
                         if (r < 0)
@@ -1128,11 +1182,11 @@ __global__ void __launch_bounds__(EVAL_THREADS, DT_EVAL_MINB) tree_eval_kernel(E
             }
             const unsigned rest = mask & ~fm;
             if (rest) {
-                if (lr.x < 0 && lr.y < 0) {
+                if (lr.x < 0) {  // leaf (first child -1)
                     UTIL_ADD(6, 1);
                     UTIL_ADD(7, __popc(rest));
                     UTIL_ADD(8, se.y - se.x);
-                    if ((rest >> lane) & 1u) {
+                    if (DT_LANE_IN(rest)) {
                         acc += near_field(a.xq, se.x, se.y, y, a.rd2);
                         if (STATS) {
                             hh = mix64(hh ^ ((uint64_t)node * 256u + 255u));
@@ -1140,14 +1194,14 @@ __global__ void __launch_bounds__(EVAL_THREADS, DT_EVAL_MINB) tree_eval_kernel(E
                         }
                     }
                 } else {
-                    if (lr.x >= 0 && lr.y >= 0) {  // right sibling waits on the stack
+                    if (lr.y >= 0) {  // the right child waits on the stack
 #if DT_EVAL_SP
                         *++sp = make_uint2((unsigned)lr.y, rest);
 #else
                         stk[++top] = make_uint2((unsigned)lr.y, rest);
 #endif
                     }
-                    node = lr.x >= 0 ? lr.x : lr.y;
+                    node = lr.x;
                     mask = rest;
                     continue;
                 }
@@ -1229,8 +1283,7 @@ __global__ void pack_tree_kernel(const double *__restrict__ c, const double *__r
     dt_node nd;
     nd.center = c[i];
     nd.half = h[i];
-    nd.left = (int32_t)l[i];
-    nd.right = (int32_t)r[i];
+    dt_node_children(nd, l[i], r[i]);
     nd.start = (int32_t)s[i];
     nd.end = (int32_t)e[i];
     out[i] = nd;
