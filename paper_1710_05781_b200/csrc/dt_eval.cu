@@ -65,7 +65,7 @@ static_assert(DT_EVAL_SEGMENTS * 4 <= DT_EVAL_COUNTER_BYTES, "counter slot too s
 #define DT_EVAL_PREFETCH 0  // claim the next task while the current one runs
 #endif
 #ifndef DT_EVAL_PBADDR
-#define DT_EVAL_PBADDR 0  // order bins read through a 32-bit shared address held in a register
+#define DT_EVAL_PBADDR 1  // order bins read through a 32-bit shared address held in a register
 #endif
 #ifndef DT_EVAL_UTIL
 #define DT_EVAL_UTIL 0  // development: lane-utilisation counters (variant builds only)
