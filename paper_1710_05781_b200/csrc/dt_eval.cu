@@ -67,6 +67,9 @@ static_assert(DT_EVAL_SEGMENTS * 4 <= DT_EVAL_COUNTER_BYTES, "counter slot too s
 #ifndef DT_EVAL_PBADDR
 #define DT_EVAL_PBADDR 1  // order bins read through a 32-bit shared address held in a register
 #endif
+#ifndef DT_EVAL_ODD1
+#define DT_EVAL_ODD1 0  // an odd pmin's last order in the unmasked part
+#endif
 #ifndef DT_EVAL_UTIL
 #define DT_EVAL_UTIL 0  // development: lane-utilisation counters (variant builds only)
 #endif
@@ -789,6 +792,15 @@ __device__ __forceinline__ double far_field(double d, double rd2, const double2 
         }
         // the pairs above ran for kk = 1, 3, .. while kk + 1 <= min(pmin, 31)
         k = 1 + (min(pmin, 31) & ~1);
+#if DT_EVAL_ODD1
+        if (k <= pmin) {  // odd pmin: its last order unmasked too (k odd)
+            DT_FAR_STEP(k, hm2, hm1, v0)
+            acc1 = __fma_rn(v0, __ldg(reinterpret_cast<const double *>(M2) + k), acc1);
+            hm2 = hm1;
+            hm1 = v0;
+            ++k;
+        }
+#endif
     }
     const double *M = reinterpret_cast<const double *>(M2);
 #pragma unroll 1
@@ -1140,17 +1152,18 @@ __global__ void __launch_bounds__(EVAL_THREADS, DT_EVAL_MINB) tree_eval_kernel(E
                                            a.pt_bp, phi0, pjb);
                         UTIL_ADD(10, 1);
                         UTIL_ADD(11, r < 0);
-                        if (r < 0)
+                        if (r < 0) {  // one branch to the tiers behind the tables
                             r = fast_ok ? psel_fast(big_r, half, a, isig_s, fconst_s[0],
                                                     fconst_s[1])
                                         : -1;
-                        if (r < 0) {
-                            if (r <= -2 && fast_ok)
-                                r = psel_exact_bracket(big_r, half, -r - 2, a, cs, sn);
-                            else
-                                r = psel_exact_all(big_r, half, a, cs, sn);
-                            if (STATS)
-                                ++c_exact;
+                            if (r < 0) {
+                                if (r <= -2 && fast_ok)
+                                    r = psel_exact_bracket(big_r, half, -r - 2, a, cs, sn);
+                                else
+                                    r = psel_exact_all(big_r, half, a, cs, sn);
+                                if (STATS)
+                                    ++c_exact;
+                            }
                         }
                         pu = r;
                     } else {
