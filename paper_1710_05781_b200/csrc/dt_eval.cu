@@ -70,6 +70,9 @@ static_assert(DT_EVAL_SEGMENTS * 4 <= DT_EVAL_COUNTER_BYTES, "counter slot too s
 #ifndef DT_EVAL_ODD1
 #define DT_EVAL_ODD1 0  // an odd pmin's last order in the unmasked part
 #endif
+#ifndef DT_EVAL_PUSHU
+#define DT_EVAL_PUSHU 1  // branch-free push of the right child
+#endif
 #ifndef DT_EVAL_UTIL
 #define DT_EVAL_UTIL 0  // development: lane-utilisation counters (variant builds only)
 #endif
@@ -1171,7 +1174,9 @@ __global__ void __launch_bounds__(EVAL_THREADS, DT_EVAL_MINB) tree_eval_kernel(E
                     }
                 }
                 const int pmax = __reduce_max_sync(DT_FULL, pu);
-                const int pmin = __reduce_min_sync(DT_FULL, far ? pu : 1 << 20);
+                // lanes without a far interaction hold pu = -1: the unsigned
+                // minimum skips them
+                const int pmin = (int)__reduce_min_sync(DT_FULL, (unsigned)pu);
                 UTIL_ADD(1, 1);
                 UTIL_ADD(2, __popc(fm));
                 UTIL_ADD(3, pmax);
@@ -1207,6 +1212,12 @@ __global__ void __launch_bounds__(EVAL_THREADS, DT_EVAL_MINB) tree_eval_kernel(E
                         }
                     }
                 } else {
+#if DT_EVAL_SP && DT_EVAL_PUSHU
+                    // the right child waits on the stack: the entry is
+                    // always written and kept only if there is a right child
+                    sp[1] = make_uint2((unsigned)lr.y, rest);
+                    sp += lr.y >= 0 ? 1 : 0;
+#else
                     if (lr.y >= 0) {  // the right child waits on the stack
 #if DT_EVAL_SP
                         *++sp = make_uint2((unsigned)lr.y, rest);
@@ -1214,6 +1225,7 @@ __global__ void __launch_bounds__(EVAL_THREADS, DT_EVAL_MINB) tree_eval_kernel(E
                         stk[++top] = make_uint2((unsigned)lr.y, rest);
 #endif
                     }
+#endif
                     node = lr.x;
                     mask = rest;
                     continue;
