@@ -52,27 +52,6 @@ namespace {
 #define DT_EVAL_SEGMENTS 148  // per-SM task segments (0: one global counter)
 #endif
 static_assert(DT_EVAL_SEGMENTS * 4 <= DT_EVAL_COUNTER_BYTES, "counter slot too small");
-#ifndef DT_EVAL_SP
-#define DT_EVAL_SP 1  // the warp stack walked by a shared-memory pointer above a sentinel
-#endif
-#ifndef DT_EVAL_FAR2
-#define DT_EVAL_FAR2 1  // far field: orders 1 and 2 through the recurrence
-#endif
-#ifndef DT_EVAL_LANEBIT
-#define DT_EVAL_LANEBIT 1  // lane bit held in a register (asm, not rematerialised)
-#endif
-#ifndef DT_EVAL_PREFETCH
-#define DT_EVAL_PREFETCH 0  // claim the next task while the current one runs
-#endif
-#ifndef DT_EVAL_PBADDR
-#define DT_EVAL_PBADDR 1  // order bins read through a 32-bit shared address held in a register
-#endif
-#ifndef DT_EVAL_ODD1
-#define DT_EVAL_ODD1 0  // an odd pmin's last order in the unmasked part
-#endif
-#ifndef DT_EVAL_PUSHU
-#define DT_EVAL_PUSHU 1  // branch-free push of the right child
-#endif
 #ifndef DT_EVAL_UTIL
 #define DT_EVAL_UTIL 0  // development: lane-utilisation counters (variant builds only)
 #endif
@@ -712,24 +691,15 @@ static_assert(PT_BINS_OFFSET + PT_LEVELS * PT_BINS <= DT_EVAL_COUNTER_BYTES,
 // p from the bins, or -1 (use psel_fast): integer arithmetic on the high
 // words of R and h (hi0 = hi(h0), jbase = pt_jbase(theta)), one shared-memory
 // byte, at most one double comparison
-#if DT_EVAL_PBADDR
 __device__ __forceinline__ int psel_table(double R, int hiR, double h, unsigned bins,
                                           const double *bp, int hi0, int jbase)
-#else
-__device__ __forceinline__ int psel_table(double R, int hiR, double h, const unsigned char *bins,
-                                          const double *bp, int hi0, int jbase)
-#endif
 {
     const int L = pt_level(hi0, h);
     const int j = ((hiR - (hi0 - (L << 20))) >> 13) - jbase;
     if (!((unsigned)L < (unsigned)PT_LEVELS && (unsigned)j < (unsigned)PT_BINS))
         return -1;
-#if DT_EVAL_PBADDR
     unsigned e;
     asm("ld.shared.u8 %0, [%1];" : "=r"(e) : "r"(bins + (unsigned)(L * PT_BINS + j)));
-#else
-    const unsigned e = bins[L * PT_BINS + j];
-#endif
     if (e < PT_SPLIT)
         return (int)e;
     if (e == PT_FALLBACK)
@@ -759,7 +729,6 @@ __device__ __forceinline__ int psel_table(double R, int hiR, double h, const uns
 // the rest up to the warp maximum is masked per lane.  Even orders go to acc
 // and odd ones to acc1 on both paths, so a target's result depends on its
 // own p only, not on which warp (pmin, pmax) evaluated it.
-#if DT_EVAL_FAR2
 template <bool WIDE>
 __device__ __forceinline__ double far_field(double d, double rd2, const double2 *__restrict__ M2,
                                             int pu, int pmin, int pmax)
@@ -795,15 +764,6 @@ __device__ __forceinline__ double far_field(double d, double rd2, const double2 
         }
         // the pairs above ran for kk = 1, 3, .. while kk + 1 <= min(pmin, 31)
         k = 1 + (min(pmin, 31) & ~1);
-#if DT_EVAL_ODD1
-        if (k <= pmin) {  // odd pmin: its last order unmasked too (k odd)
-            DT_FAR_STEP(k, hm2, hm1, v0)
-            acc1 = __fma_rn(v0, __ldg(reinterpret_cast<const double *>(M2) + k), acc1);
-            hm2 = hm1;
-            hm1 = v0;
-            ++k;
-        }
-#endif
     }
     const double *M = reinterpret_cast<const double *>(M2);
 #pragma unroll 1
@@ -830,76 +790,6 @@ __device__ __forceinline__ double far_field(double d, double rd2, const double2 
 #undef DT_FAR_STEP
     return acc + acc1;
 }
-#else
-template <bool WIDE>
-__device__ __forceinline__ double far_field(double d, double rd2, const double2 *__restrict__ M2,
-                                            int pu, int pmin, int pmax)
-{
-    const double s2 = __fma_rn(d, d, rd2);
-    const double r = dt_rsqrt(s2);
-    const double w = r * r;
-    const double u = d * w;
-    const double2 m01 = __ldg(M2);
-    double acc = (d * r) * m01.x;
-    double acc1 = 0.0;
-    if (pmax < 1)
-        return acc;
-    const double h1 = rd2 * r * w;
-    if (pu >= 1)
-        acc1 = __fma_rn(h1, m01.y, acc1);
-    if (pmax < 2)
-        return acc + acc1;
-    const double h2 = (-3.0 * u) * h1;
-    if (pu >= 2)
-        acc = __fma_rn(h2, __ldg(M2 + 1).x, acc);
-    double hm2 = h1, hm1 = h2;
-    int k = 3;
-#define DT_FAR_STEP(KK, H2, H1, OUT)                                              \
-    const double OUT = __fma_rn(u * c_hcoef[(KK) + 1], H1, -(w * H2));
-    if (!WIDE) {
-        // unmasked pairs (odd, even): the two recurrence values swap roles
-        // every order, so each pair ends with them back in place
-#pragma unroll
-        for (int kk = 3; kk + 1 <= 31; kk += 2) {
-            if (kk + 1 > pmin)
-                break;
-            DT_FAR_STEP(kk, hm2, hm1, v0)
-            DT_FAR_STEP(kk + 1, hm1, v0, v1)
-            // kk odd: M_kk = M2[kk / 2].y, M_(kk+1) = M2[(kk + 1) / 2].x
-            acc1 = __fma_rn(v0, __ldg(M2 + kk / 2).y, acc1);
-            acc = __fma_rn(v1, __ldg(M2 + (kk + 1) / 2).x, acc);
-            hm2 = v0;
-            hm1 = v1;
-        }
-        // the pairs above ran for kk = 3, 5, .. while kk + 1 <= min(pmin, 31)
-        k = 3 + 2 * max(0, (min(pmin, 31) - 2) / 2);
-    }
-    const double *M = reinterpret_cast<const double *>(M2);
-#pragma unroll 1
-    for (; k <= pmax; k += 2) {
-        DT_FAR_STEP(k, hm2, hm1, t0)
-        if (k <= pu) {
-            if (k & 1)
-                acc1 = __fma_rn(t0, __ldg(M + k), acc1);
-            else
-                acc = __fma_rn(t0, __ldg(M + k), acc);
-        }
-        if (k + 1 > pmax)
-            break;
-        DT_FAR_STEP(k + 1, hm1, t0, t1)
-        if (k + 1 <= pu) {
-            if ((k + 1) & 1)
-                acc1 = __fma_rn(t1, __ldg(M + k + 1), acc1);
-            else
-                acc = __fma_rn(t1, __ldg(M + k + 1), acc);
-        }
-        hm2 = t0;
-        hm1 = t1;
-    }
-#undef DT_FAR_STEP
-    return acc + acc1;
-}
-#endif
 
 // acc + q (x - y) / sqrt((x - y)^2 + r_d^2) (nvcc contracts the final
 // product and sum into one DFMA): 9 FP64 instructions + MUFU
@@ -1026,12 +916,8 @@ __global__ void __launch_bounds__(EVAL_THREADS, DT_EVAL_MINB) tree_eval_kernel(E
     // without tables the bin index is pushed out of range (psel_table
     // returns -1 for every pair), so the walk needs no table_ok branch
     const int pjb = table_ok ? pt_jbase(a.theta) : -(1 << 30);
-#if DT_EVAL_PBADDR
     unsigned pbins_a = (unsigned)__cvta_generic_to_shared(pbins_s);
     asm volatile("" : "+r"(pbins_a));  // kept in a register, not rematerialised
-#else
-    const unsigned char *const pbins_a = pbins_s;
-#endif
     __syncthreads();
 
 #if DT_EVAL_SEGMENTS
@@ -1043,13 +929,6 @@ __global__ void __launch_bounds__(EVAL_THREADS, DT_EVAL_MINB) tree_eval_kernel(E
     unsigned *const seg_ctr = reinterpret_cast<unsigned *>(a.counter);
     int seg = (int)(dt_smid() % DT_EVAL_SEGMENTS);
     int seg_left = DT_EVAL_SEGMENTS;
-#if DT_EVAL_PREFETCH
-    // lane 0 holds the task of segment seg claimed ahead, so the atomic's
-    // round trip overlaps the current task
-    unsigned pre = 0;
-    if (lane == 0)
-        pre = atomicAdd(seg_ctr + seg, 1u);
-#endif
 #endif
     while (true) {
         unsigned long long base = 0;
@@ -1057,19 +936,6 @@ __global__ void __launch_bounds__(EVAL_THREADS, DT_EVAL_MINB) tree_eval_kernel(E
 #if DT_EVAL_SEGMENTS
             const int64_t s0 = n_tasks * seg / DT_EVAL_SEGMENTS;
             const int64_t s1 = n_tasks * (seg + 1) / DT_EVAL_SEGMENTS;
-#if DT_EVAL_PREFETCH
-            const unsigned t = __shfl_sync(DT_FULL, pre, 0);
-            if ((int64_t)t >= s1 - s0) {
-                if (--seg_left == 0)
-                    break;
-                seg = seg + 1 == DT_EVAL_SEGMENTS ? 0 : seg + 1;
-                if (lane == 0)
-                    pre = atomicAdd(seg_ctr + seg, 1u);
-                continue;
-            }
-            if (lane == 0)
-                pre = atomicAdd(seg_ctr + seg, 1u);
-#else
             unsigned t = 0;
             if (lane == 0)
                 t = atomicAdd(seg_ctr + seg, 1u);
@@ -1080,7 +946,6 @@ __global__ void __launch_bounds__(EVAL_THREADS, DT_EVAL_MINB) tree_eval_kernel(E
                 seg = seg + 1 == DT_EVAL_SEGMENTS ? 0 : seg + 1;
                 continue;
             }
-#endif
             base = (unsigned long long)(s0 + t) * 32ull;
 #else
             if (lane == 0)
@@ -1114,28 +979,19 @@ __global__ void __launch_bounds__(EVAL_THREADS, DT_EVAL_MINB) tree_eval_kernel(E
         // pending right siblings go on the warp's stack in shared memory
         // (depth <= 60).  Every lane stores the same entry and reads back
         // its own store, so no warp barrier is needed.
-#if DT_EVAL_SP
         // sp points at the top entry; entry 0 is a sentinel with an empty
         // mask (a pushed entry always has a lane), so the walk ends when it
         // pops the sentinel and no base address or index stays live
         uint2 *sp = stack_s[threadIdx.x >> 5];
         *sp = make_uint2(0u, 0u);
-#else
-        int top = -1;
-        uint2 *const stk = stack_s[threadIdx.x >> 5];
-#endif
 #if DT_EVAL_UTIL
         unsigned long long u_[12] = {0};
 #endif
         int node = 0;
         unsigned mask = __ballot_sync(DT_FULL, live);
-#if DT_EVAL_LANEBIT
-        unsigned lanebit;
+        unsigned lanebit;  // this lane's bit (asm: read once, not rematerialised)
         asm volatile("mov.u32 %0, %%lanemask_eq;" : "=r"(lanebit));
 #define DT_LANE_IN(m) (((m) & lanebit) != 0u)
-#else
-#define DT_LANE_IN(m) ((((m) >> lane) & 1u) != 0u)
-#endif
         while (true) {
             const double4 raw0 = dt_ldg256(a.nodes + node);  // one 256-bit load
             const double center = raw0.x, half = raw0.y;
@@ -1212,34 +1068,18 @@ __global__ void __launch_bounds__(EVAL_THREADS, DT_EVAL_MINB) tree_eval_kernel(E
                         }
                     }
                 } else {
-#if DT_EVAL_SP && DT_EVAL_PUSHU
                     // the right child waits on the stack: the entry is
                     // always written and kept only if there is a right child
                     sp[1] = make_uint2((unsigned)lr.y, rest);
                     sp += lr.y >= 0 ? 1 : 0;
-#else
-                    if (lr.y >= 0) {  // the right child waits on the stack
-#if DT_EVAL_SP
-                        *++sp = make_uint2((unsigned)lr.y, rest);
-#else
-                        stk[++top] = make_uint2((unsigned)lr.y, rest);
-#endif
-                    }
-#endif
                     node = lr.x;
                     mask = rest;
                     continue;
                 }
             }
-#if DT_EVAL_SP
             const uint2 e = *sp--;
             if (e.y == 0u)
                 break;
-#else
-            if (top < 0)
-                break;
-            const uint2 e = stk[top--];
-#endif
             node = (int)e.x;
             mask = e.y;
         }
