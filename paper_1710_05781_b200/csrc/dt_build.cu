@@ -58,6 +58,18 @@ struct BuildArgs {
     int p2m_kmax;                    // 0: off, else 8/16/24/32 (order + 1 rounded up)
     P2mArgs p2m;
     unsigned long long *p2m_ctr;     // next 32-node chunk to form (zeroed per launch)
+    // the nodes of level k_top that split, in BFS order, written by the
+    // one-pass top (count, or -1 when the top was not built in one pass)
+    int64_t *deep_count;
+    struct Front *deep_list;
+};
+
+// A frontier node of a block-0 run: kept in shared memory from one level to
+// the next, so a level reads no node fields back from global memory.
+struct Front {
+    double lo, hi;
+    int64_t node;
+    int32_t s, e;
 };
 
 // One warp forms leaves of 32-node chunks below `upto` (final nodes: the
@@ -87,7 +99,10 @@ __device__ void build_p2m_until(const BuildArgs &a, unsigned long long limit,
         if (c < 0)
             return;
         const int64_t c0 = (int64_t)c * 32, mine = c0 + lane;
-        const bool leaf = __ldcg(a.left + mine) < 0 && __ldcg(a.right + mine) < 0;
+        // the build's own leaf rule (final once the node is written; its
+        // child links may still be in flight for the first level of the run)
+        const bool leaf = __ldcg(a.end + mine) - __ldcg(a.start + mine) <= a.leaf_capacity ||
+                          __ldcg(a.level + mine) >= a.max_depth;
         unsigned leaves = __ballot_sync(DT_FULL, leaf);
         while (leaves) {
             unsigned m = leaves;
@@ -222,15 +237,11 @@ __device__ __forceinline__ int64_t sampled_lower_bound(const BuildArgs &a, const
     return g < s ? s : (g > e ? e : g);
 }
 
-__device__ __forceinline__ int node_children(const BuildArgs &a, int64_t node, int64_t lev,
-                                             int64_t *split_out,
-                                             const SplitSamples *sm = nullptr)
+// split = lower_bound(xs[s:e], mid) of a splitting node [lo, hi) of level lev
+__device__ __forceinline__ int64_t split_of(const BuildArgs &a, int64_t lev, double lo, double hi,
+                                            int64_t s, int64_t e, const SplitSamples *sm)
 {
-    int64_t s = ld_cg(a.start + node), e = ld_cg(a.end + node);
-    if (e - s <= a.leaf_capacity || lev >= a.max_depth)
-        return 0;
-    const double lo = ld_cg(a.lo + node), hi = ld_cg(a.hi + node);
-    double mid = mid_of(lo, hi);
+    const double mid = mid_of(lo, hi);
     int64_t split = -1;
     if (lev < DYADIC_LEVELS) {
         // dyadic position of the node from its lower bound; used only if the
@@ -249,6 +260,18 @@ __device__ __forceinline__ int node_children(const BuildArgs &a, int64_t node, i
     if (split < 0)
         split = sm && s >= sm->r0 && e <= sm->r1 ? sampled_lower_bound(a, *sm, s, e, mid)
                                                   : dt_lower_bound(a.xs, s, e, mid);
+    return split;
+}
+
+__device__ __forceinline__ int node_children(const BuildArgs &a, int64_t node, int64_t lev,
+                                             int64_t *split_out,
+                                             const SplitSamples *sm = nullptr)
+{
+    int64_t s = ld_cg(a.start + node), e = ld_cg(a.end + node);
+    if (e - s <= a.leaf_capacity || lev >= a.max_depth)
+        return 0;
+    const double lo = ld_cg(a.lo + node), hi = ld_cg(a.hi + node);
+    const int64_t split = split_of(a, lev, lo, hi, s, e, sm);
     *split_out = split;
     return (split > s) + (e > split);
 }
@@ -313,29 +336,63 @@ __device__ int block_excl_scan(int v, int *excl, int *warp_sums)
     return total;
 }
 
-// Process frontier [f0, f1) of level `lev` entirely inside the calling block.
+// One level of a block-0 run: the frontier `cur` (F nodes of level lev) is
+// in shared memory; the children are written to the node arrays at BFS
+// index g1 + rank and, while they fit, to the next frontier `nxt`.
 // Returns the number of children written (or -1 on capacity overflow).
-__device__ int64_t level_in_block(const BuildArgs &a, int64_t f0, int64_t f1, int64_t lev,
-                                  int *warp_sums, int64_t *leaves, const SplitSamples *sm)
+__device__ int64_t level_in_block(const BuildArgs &a, const Front *cur, int F, int64_t g1,
+                                  int64_t lev, int *warp_sums, int64_t *leaves,
+                                  const SplitSamples *sm, Front *nxt)
 {
-    int64_t next = f1;
+    int64_t next = g1;
     int64_t leaf_acc = 0;
-    for (int64_t t0 = f0; t0 < f1; t0 += blockDim.x) {
-        int64_t node = t0 + threadIdx.x;
+    for (int t0 = 0; t0 < F; t0 += blockDim.x) {
+        const int i = t0 + threadIdx.x;
+        int nc = 0;
         int64_t split = 0;
-        int nc = node < f1 ? node_children(a, node, lev, &split, sm) : 0;
-        if (node < f1 && nc == 0)
-            ++leaf_acc;
+        Front f{};
+        if (i < F) {
+            f = cur[i];
+            if (f.e - f.s > a.leaf_capacity && lev < a.max_depth) {
+                split = split_of(a, lev, f.lo, f.hi, f.s, f.e, sm);
+                nc = (split > f.s) + (f.e > split);
+            } else {
+                ++leaf_acc;
+            }
+        }
         int excl;
-        int tot = block_excl_scan(nc, &excl, warp_sums);
+        const int tot = block_excl_scan(nc, &excl, warp_sums);
         if (next + tot > a.capacity)
             return -1;
-        if (nc)
-            emit_children(a, node, lev, next + excl, split);
+        if (nc) {
+            const double mid = mid_of(f.lo, f.hi);
+            int64_t c = next + excl;
+            int64_t l_slot = -1, r_slot = -1;
+            if (split > f.s) {  // (lo, mid): child_hi == mid -> left
+                write_node(a, c, f.lo, mid, lev + 1, f.s, split);
+                if (c - g1 < SMALL_LEVEL)
+                    nxt[c - g1] = Front{f.lo, mid, c, f.s, (int32_t)split};
+                l_slot = c;
+                ++c;
+            }
+            if (f.e > split) {  // (mid, hi): left iff hi == mid (tree.py:205-208)
+                write_node(a, c, mid, f.hi, lev + 1, split, f.e);
+                if (c - g1 < SMALL_LEVEL)
+                    nxt[c - g1] = Front{mid, f.hi, c, (int32_t)split, f.e};
+                if (f.hi == mid)
+                    l_slot = c;
+                else
+                    r_slot = c;
+            }
+            a.left[f.node] = l_slot;
+            a.right[f.node] = r_slot;
+            if (a.packed)
+                dt_node_children(a.packed[f.node], l_slot, r_slot);
+        }
         next += tot;
     }
     *leaves += leaf_acc;
-    return next - f1;
+    return next - g1;
 }
 
 // ---- the top levels in one pass
@@ -406,7 +463,7 @@ __device__ __forceinline__ TopSlot top_slot(const BuildArgs &a, int64_t f, doubl
 // Returns the first level for the level-by-level loop (k_top, or 0 if the
 // top cannot be built in one pass).  Grid-uniform.
 __device__ int64_t build_top(const BuildArgs &a, cg::grid_group &grid, int *warp_sums,
-                             int64_t *bases_s)
+                             int64_t *bases_s, int64_t *bases2_s)
 {
     const int K = a.k_top;
     if (K <= 0 || *(volatile unsigned *)a.irregular)
@@ -417,24 +474,35 @@ __device__ int64_t build_top(const BuildArgs &a, cg::grid_group &grid, int *warp
     const int64_t S = ((int64_t)2 << K) - 1;  // slots of levels 0..K
     const int64_t chunk = (S + G - 1) / G;
     const int64_t b0 = (int64_t)blockIdx.x * chunk, b1 = min(S, b0 + chunk);
+    // the level-K nodes that split are also listed (in slot order, which is
+    // BFS order) with their intervals, so the level-by-level build continues
+    // from them alone instead of testing every level-K node; the two counts
+    // share one scan (16 bits each: a block chunk has < 2^15 slots)
+    const bool listing = chunk < (1 << 15) && G <= 1024;
     // pass 1: node flags, block-local exclusive offsets, leaves above level K
-    int64_t run = 0, leaves = 0;
+    int64_t run = 0, run2 = 0, leaves = 0;
     for (int64_t t0 = b0; t0 < b1; t0 += blockDim.x) {
         const int64_t f = t0 + threadIdx.x;
         int flag = 0;
         if (f < b1) {
             const TopSlot t = top_slot(a, f, lo0, hi0);
-            flag = t.node;
+            flag = t.node | ((listing && t.splits && t.L == K) ? 1 << 16 : 0);
             leaves += t.node && !t.splits && t.L < K;
         }
         int excl;
         const int tot = block_excl_scan(flag, &excl, warp_sums);
-        if (f < b1)
-            a.scratch_off[f] = (int32_t)(run + excl);
-        run += tot;
+        if (f < b1) {
+            a.scratch_off[f] = (int32_t)(run + (excl & 0xffff));
+            a.scratch_split[f] = (int32_t)(run2 + (excl >> 16));
+        }
+        run += tot & 0xffff;
+        run2 += tot >> 16;
     }
-    if (threadIdx.x == 0)
+    if (threadIdx.x == 0) {
         a.block_total[blockIdx.x] = run;
+        if (listing)
+            a.block_total[1024 + blockIdx.x] = run2;
+    }
     {
         int64_t lv = leaves;
         for (int o = 16; o > 0; o >>= 1)
@@ -451,6 +519,13 @@ __device__ int64_t build_top(const BuildArgs &a, cg::grid_group &grid, int *warp
             acc += ((volatile int64_t *)a.block_total)[b];
         }
         bases_s[G] = acc;
+    } else if (threadIdx.x == 32 && listing) {
+        int64_t acc = 0;
+        for (int b = 0; b < G; ++b) {
+            bases2_s[b] = acc;
+            acc += ((volatile int64_t *)a.block_total)[1024 + b];
+        }
+        bases2_s[G] = acc;
     }
     __syncthreads();
     const int64_t total = bases_s[G];
@@ -469,6 +544,9 @@ __device__ int64_t build_top(const BuildArgs &a, cg::grid_group &grid, int *warp
             continue;
         const int64_t c = index_of(f);
         write_node(a, c, t.lo, t.hi, t.L, t.s, t.e);
+        if (listing && t.splits && t.L == K)
+            a.deep_list[bases2_s[f / chunk] + __ldcg(a.scratch_split + f)] =
+                Front{t.lo, t.hi, c, (int32_t)t.s, (int32_t)t.e};
         if (t.splits && t.L < K) {
             const int64_t split = __ldcg(a.dy_split + f);  // this slot's own midpoint
             const int64_t fl = 2 * f + 1;                  // slot (L + 1, 2k)
@@ -486,6 +564,7 @@ __device__ int64_t build_top(const BuildArgs &a, cg::grid_group &grid, int *warp
         a.meta[DT_META_LEVEL0 + L] = index_of(((int64_t)1 << L) - 1);
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) {
+        *a.deep_count = listing ? bases2_s[G] : -1;
         a.meta[DT_META_NODES] = total;
         int depth = 0;
         for (int L = 0; L <= K; ++L)
@@ -503,7 +582,10 @@ __global__ void __launch_bounds__(BUILD_THREADS) build_kernel(BuildArgs a)
     __shared__ int warp_sums[BUILD_THREADS / 32];
     __shared__ int64_t sh_i64[4];
     __shared__ int64_t top_bases_s[BUILD_THREADS + 1];
-    extern __shared__ double samples_s[];  // BUILD_SAMPLES
+    __shared__ int64_t top_bases2_s[BUILD_THREADS + 1];
+    // BUILD_SAMPLES split samples, then two frontier buffers of SMALL_LEVEL
+    extern __shared__ double samples_s[];
+    Front *const front_s = reinterpret_cast<Front *>(samples_s + BUILD_SAMPLES);
     volatile int64_t *meta = a.meta;
     const int G = gridDim.x;
 
@@ -513,6 +595,7 @@ __global__ void __launch_bounds__(BUILD_THREADS) build_kernel(BuildArgs a)
         a.meta[DT_META_LEVEL0 + 0] = 0;
         a.meta[DT_META_LEVEL0 + 1] = 1;
         a.meta[DT_META_NODES] = 1;
+        *a.deep_count = -1;
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         // tree.py:173-175: pad = 1e-12 * max(1.0, |x0|, |x_last|)
@@ -543,7 +626,8 @@ __global__ void __launch_bounds__(BUILD_THREADS) build_kernel(BuildArgs a)
     dyadic_splits(a);
     grid.sync();
     BUILD_STAMP(71)
-    int64_t lev = build_top(a, grid, warp_sums, top_bases_s);
+    int64_t lev = build_top(a, grid, warp_sums, top_bases_s, top_bases2_s);
+    const int64_t k_listed = lev;  // the level whose splitting nodes are listed
     BUILD_STAMP(72)
     if (lev < 0)
         return;  // capacity overflow (flagged in meta)
@@ -560,19 +644,42 @@ __global__ void __launch_bounds__(BUILD_THREADS) build_kernel(BuildArgs a)
         int64_t F = f1 - f0;
         if (F == 0 || meta[DT_META_OVERFLOW])
             break;
-        if (F <= SMALL_LEVEL) {
-            // block 0 runs consecutive small levels; the others wait at the barrier
+        // level k_top continues from the listed nodes that split
+        const int64_t n_listed = lev == k_listed && k_listed > 0 ? *(volatile int64_t *)a.deep_count : -1;
+        const bool listed = n_listed >= 0 && n_listed <= SMALL_LEVEL;
+        if (F <= SMALL_LEVEL || listed) {
+            // block 0 runs consecutive small levels with the frontier in
+            // shared memory; the others wait (and form leaves, below)
             if (blockIdx.x == 0) {
                 int64_t leaves = 0;
-                int64_t l = lev;
-                // the run's nodes all lie inside the first level's source
+                int64_t l = lev, g1 = f1;
+                Front *cur = front_s, *nxt = front_s + SMALL_LEVEL;
+                int Fl;
+                if (listed) {
+                    Fl = (int)n_listed;
+                    for (int i = threadIdx.x; i < Fl; i += blockDim.x) {
+                        const double2 lh = __ldcg(reinterpret_cast<const double2 *>(a.deep_list + i));
+                        const double2 ns = __ldcg(reinterpret_cast<const double2 *>(a.deep_list + i) + 1);
+                        cur[i] = Front{lh.x, lh.y, (int64_t)__double_as_longlong(ns.x),
+                                       __double2loint(ns.y), __double2hiint(ns.y)};
+                    }
+                    if (threadIdx.x == 0)
+                        leaves += F - Fl;  // the level's other nodes are leaves
+                } else {
+                    Fl = (int)F;
+                    for (int i = threadIdx.x; i < Fl; i += blockDim.x) {
+                        const int64_t node = f0 + i;
+                        cur[i] = Front{ld_cg(a.lo + node), ld_cg(a.hi + node), node,
+                                       (int32_t)ld_cg(a.start + node), (int32_t)ld_cg(a.end + node)};
+                    }
+                }
+                __syncthreads();
+                // the run's nodes all lie inside the first frontier's source
                 // range: sample it once (below the dyadic levels only)
                 SplitSamples sm{samples_s, 0, 0, 1, 0};
-                if (lev >= DYADIC_LEVELS) {
-                    const int64_t g0 = meta[DT_META_LEVEL0 + lev];
-                    const int64_t g1 = meta[DT_META_LEVEL0 + lev + 1];
-                    sm.r0 = ld_cg(a.start + g0);
-                    sm.r1 = ld_cg(a.end + g1 - 1);
+                if (lev >= DYADIC_LEVELS && Fl > 0) {
+                    sm.r0 = cur[0].s;
+                    sm.r1 = cur[Fl - 1].e;
                     const int64_t len = sm.r1 - sm.r0;
                     sm.stride = len > BUILD_SAMPLES ? (len + BUILD_SAMPLES - 1) / BUILD_SAMPLES : 1;
                     sm.count = (int)((len + sm.stride - 1) / sm.stride);
@@ -581,11 +688,6 @@ __global__ void __launch_bounds__(BUILD_THREADS) build_kernel(BuildArgs a)
                     __syncthreads();
                 }
                 while (true) {
-                    int64_t g0 = meta[DT_META_LEVEL0 + l];
-                    int64_t g1 = meta[DT_META_LEVEL0 + l + 1];
-                    int64_t Fl = g1 - g0;
-                    if (Fl == 0 || Fl > SMALL_LEVEL || l > a.max_depth)
-                        break;
 #ifdef DT_BUILD_TRACE
                     if (threadIdx.x == 0) {
                         unsigned long long t;
@@ -593,8 +695,8 @@ __global__ void __launch_bounds__(BUILD_THREADS) build_kernel(BuildArgs a)
                         a.block_total[2048 + l] = (int64_t)t;
                     }
 #endif
-                    int64_t made = level_in_block(a, g0, g1, l, warp_sums, &leaves,
-                                                  lev >= DYADIC_LEVELS ? &sm : nullptr);
+                    const int64_t made = level_in_block(a, cur, Fl, g1, l, warp_sums, &leaves,
+                                                        lev >= DYADIC_LEVELS ? &sm : nullptr, nxt);
                     __syncthreads();
                     if (made < 0) {
                         if (threadIdx.x == 0)
@@ -610,6 +712,13 @@ __global__ void __launch_bounds__(BUILD_THREADS) build_kernel(BuildArgs a)
                     __threadfence_block();
                     __syncthreads();
                     ++l;
+                    if (made == 0 || made > SMALL_LEVEL || l > a.max_depth)
+                        break;
+                    Fl = (int)made;
+                    g1 += made;
+                    Front *t = cur;
+                    cur = nxt;
+                    nxt = t;
                 }
                 // leaves counted per thread: reduce
                 int64_t lv = leaves;
@@ -622,8 +731,11 @@ __global__ void __launch_bounds__(BUILD_THREADS) build_kernel(BuildArgs a)
                     a.meta[DT_META_CURLEVEL] = l;
                 __threadfence();
             }
-            if (blockIdx.x == 0 && a.p2m_kmax && p2m_limit == 0 && f0 >= 32)
-                p2m_limit = (unsigned long long)(f0 / 32);  // as the other blocks
+            // nodes below p2m_upto are final (the listed level's nodes too:
+            // the P2M leaf test reads only their ranges and levels)
+            const int64_t p2m_upto = listed ? f1 : f0;
+            if (blockIdx.x == 0 && a.p2m_kmax && p2m_limit == 0 && p2m_upto >= 32)
+                p2m_limit = (unsigned long long)(p2m_upto / 32);  // as the other blocks
 #if DT_BUILD_FLAGWAIT
             // block 0 announces the end of its run with a release store; the
             // other blocks wait on it with back-off instead of polling a grid
@@ -635,10 +747,10 @@ __global__ void __launch_bounds__(BUILD_THREADS) build_kernel(BuildArgs a)
                     asm volatile("st.release.gpu.u64 [%0], %1;" ::"l"(small_flag), "l"(small_phase)
                                  : "memory");
             } else {
-                if (a.p2m_kmax && p2m_limit == 0 && f0 >= 32) {
+                if (a.p2m_kmax && p2m_limit == 0 && p2m_upto >= 32) {
                     // meanwhile (the first run with whole chunks before it
                     // only): form the leaves of the levels before this run
-                    p2m_limit = (unsigned long long)(f0 / 32);
+                    p2m_limit = (unsigned long long)(p2m_upto / 32);
                     switch (a.p2m_kmax) {
                     case 8: build_p2m_until<8>(a, p2m_limit, small_phase, small_flag); break;
                     case 16: build_p2m_until<16>(a, p2m_limit, small_phase, small_flag); break;
@@ -747,7 +859,8 @@ extern "C" size_t dt_build_workspace(int64_t n, int64_t node_capacity)
 {
     (void)n;
     return (size_t)node_capacity * 2 * sizeof(int32_t) + 4096 * sizeof(int64_t) + 16 +
-           (size_t)DYADIC * (sizeof(int64_t) + sizeof(double)) + 32;
+           (size_t)DYADIC * (sizeof(int64_t) + sizeof(double)) + 32 + 64 +
+           ((size_t)1 << DYADIC_LEVELS) * sizeof(Front);
 }
 
 static int build_launch(const double *xs, int64_t n, int64_t leaf_capacity, int64_t max_depth,
@@ -807,6 +920,8 @@ static int build_launch(const double *xs, int64_t n, int64_t leaf_capacity, int6
                 break;
             }
     a.p2m_ctr = (unsigned long long *)(a.irregular + 2);
+    a.deep_count = (int64_t *)(a.p2m_ctr + 1);
+    a.deep_list = (Front *)(((uintptr_t)(a.deep_count + 1) + 31) & ~(uintptr_t)31);
     a.p2m_kmax = 0;
     if (p2m) {
         a.p2m = *p2m;
@@ -818,7 +933,7 @@ static int build_launch(const double *xs, int64_t n, int64_t leaf_capacity, int6
 
     int dev = 0, per_sm = 0;
     DT_CUDA_TRY(cudaGetDevice(&dev));
-    const size_t smem = (size_t)BUILD_SAMPLES * sizeof(double);
+    const size_t smem = (size_t)BUILD_SAMPLES * sizeof(double) + 2 * SMALL_LEVEL * sizeof(Front);
     DT_CUDA_TRY(cudaFuncSetAttribute((const void *)build_kernel,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     DT_CUDA_TRY(
