@@ -210,6 +210,9 @@ __device__ void dyadic_splits(const BuildArgs &a)
 // log2(e - s).  The result is the plain lower_bound's: samples[j - 1] < v <=
 // samples[j] bound the global lower bound to the window, and the split is
 // its clamp to [s, e) (xs is sorted).
+#ifndef DT_BUILD_WINCOUNT
+#define DT_BUILD_WINCOUNT 0
+#endif
 #ifndef DT_BUILD_SAMPLES
 #define DT_BUILD_SAMPLES 12288
 #endif
@@ -233,7 +236,22 @@ __device__ __forceinline__ int64_t sampled_lower_bound(const BuildArgs &a, const
     }
     const int64_t wlo = lo == 0 ? sm.r0 : sm.r0 + (int64_t)(lo - 1) * sm.stride + 1;
     const int64_t whi = lo == sm.count ? sm.r1 : sm.r0 + (int64_t)lo * sm.stride;
+#if DT_BUILD_WINCOUNT
+    int64_t g;
+    if (whi - wlo <= 32) {
+        // short window: independent loads and a count (one memory round
+        // trip instead of a chain of dependent probes); xs is sorted, so the
+        // number of values below v is the lower bound's offset
+        g = wlo;
+#pragma unroll 4
+        for (int64_t j = wlo; j < whi; ++j)
+            g += __ldg(a.xs + j) < v ? 1 : 0;
+    } else {
+        g = dt_lower_bound(a.xs, wlo, whi, v);
+    }
+#else
     const int64_t g = dt_lower_bound(a.xs, wlo, whi, v);
+#endif
     return g < s ? s : (g > e ? e : g);
 }
 
@@ -346,6 +364,12 @@ __device__ int64_t level_in_block(const BuildArgs &a, const Front *cur, int F, i
 {
     int64_t next = g1;
     int64_t leaf_acc = 0;
+#ifdef DT_BUILD_TRACE
+#define FINE(k) if (lev == 20 && threadIdx.x == 0) { a.block_total[2048 + 100 + (k)] = (int64_t)clock64(); }
+#else
+#define FINE(k)
+#endif
+    FINE(0)
     for (int t0 = 0; t0 < F; t0 += blockDim.x) {
         const int i = t0 + threadIdx.x;
         int nc = 0;
@@ -360,8 +384,11 @@ __device__ int64_t level_in_block(const BuildArgs &a, const Front *cur, int F, i
                 ++leaf_acc;
             }
         }
+        __syncthreads();
+        FINE(1)
         int excl;
         const int tot = block_excl_scan(nc, &excl, warp_sums);
+        FINE(2)
         if (next + tot > a.capacity)
             return -1;
         if (nc) {
@@ -369,14 +396,18 @@ __device__ int64_t level_in_block(const BuildArgs &a, const Front *cur, int F, i
             int64_t c = next + excl;
             int64_t l_slot = -1, r_slot = -1;
             if (split > f.s) {  // (lo, mid): child_hi == mid -> left
+#ifndef DT_BUILD_NOWRITE
                 write_node(a, c, f.lo, mid, lev + 1, f.s, split);
+#endif
                 if (c - g1 < SMALL_LEVEL)
                     nxt[c - g1] = Front{f.lo, mid, c, f.s, (int32_t)split};
                 l_slot = c;
                 ++c;
             }
             if (f.e > split) {  // (mid, hi): left iff hi == mid (tree.py:205-208)
+#ifndef DT_BUILD_NOWRITE
                 write_node(a, c, mid, f.hi, lev + 1, split, f.e);
+#endif
                 if (c - g1 < SMALL_LEVEL)
                     nxt[c - g1] = Front{mid, f.hi, c, (int32_t)split, f.e};
                 if (f.hi == mid)
@@ -391,6 +422,8 @@ __device__ int64_t level_in_block(const BuildArgs &a, const Front *cur, int F, i
         }
         next += tot;
     }
+    __syncthreads();
+    FINE(3)
     *leaves += leaf_acc;
     return next - g1;
 }
@@ -703,14 +736,15 @@ __global__ void __launch_bounds__(BUILD_THREADS) build_kernel(BuildArgs a)
                             a.meta[DT_META_OVERFLOW] = 1;
                         break;
                     }
+                    // (the next level reads its nodes from the frontier in
+                    // shared memory: no fence or second barrier per level)
                     if (threadIdx.x == 0) {
                         a.meta[DT_META_LEVEL0 + l + 2] = g1 + made;
                         a.meta[DT_META_NODES] = g1 + made;
                         if (made > 0)
                             a.meta[DT_META_DEPTH] = l + 1;
                     }
-                    __threadfence_block();
-                    __syncthreads();
+                    if (l == 20 && threadIdx.x == 0) { a.block_total[2048 + 104] = (int64_t)clock64(); }
                     ++l;
                     if (made == 0 || made > SMALL_LEVEL || l > a.max_depth)
                         break;

@@ -27,3 +27,7 @@ print("per-level us (level: nodes us):")
 for l in range(depth + 1):
     print(l, int(lv[l + 1] - lv[l]), round((t[l + 1] - t[l]) / 1e3, 1) if t[l + 1] > t[l] else None)
 
+fine = bt[2048 + 100: 2048 + 105]
+if fine[0] > 0:
+    print("level 20 inside (SM cycles): search %d, scan %d, emit %d, tail %d" %
+          tuple(int(fine[k + 1] - fine[k]) for k in range(4)))
