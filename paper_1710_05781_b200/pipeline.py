@@ -125,12 +125,10 @@ class TreePipeline:
         cfg = self.config
         ys_part = ys[i0:i1]
         out_part = out[i0:i1]
-        # side stream: the (x, q) interleave and the sign term overlap the
-        # latency-bound upward pass.  They start after the build: the build
-        # is a cooperative launch, which waits for co-residency with anything
-        # already running.
-        _lib.check(L.dt_prefix_scan(p(qs), p(self.prefix), self.n, p(self.scan_ws),
-                                    self.scan_ws_bytes, s), "dt_prefix_scan")
+        # side stream: the prefix scan, the (x, q) interleave and the sign
+        # term overlap the latency-bound upward pass (none of them feeds the
+        # tree).  They start after the build: the build is a cooperative
+        # launch, which waits for co-residency with anything already running.
         if self.shard is None and self.order + 1 <= 32:
             # the build's idle blocks start the P2M of the finished levels
             self.bufs.launch(xs, cfg.leaf_capacity, p2m=(qs, self.order, self.meval, self.xq))
@@ -139,6 +137,9 @@ class TreePipeline:
         self.ev_scan.record(main)
         self.side.wait_event(self.ev_scan)
         with torch.cuda.stream(self.side):
+            _lib.check(L.dt_prefix_scan(p(qs), p(self.prefix), self.n, p(self.scan_ws),
+                                        self.scan_ws_bytes, _lib.stream_handle()),
+                       "dt_prefix_scan")
             if self.shard is not None:  # the full upward pass writes xq itself
                 pack_sources(xs, qs, self.xq)
             if not self.fused_sign:
