@@ -42,7 +42,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--cells", type=int, default=1 << 22, help="GL cells (N = 4 * cells)")
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--cpu-seconds", type=float, default=12.0,
                     help="CPU-baseline eval sample budget (seconds)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -374,6 +374,7 @@ def run_ours(args):
     e2e = {"value": T / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(pairs.numel() * 8 +
                                                                       tgt.numel() * 8),
            "d2h_bytes_per_step": int(tgt.numel() * 8), "ms_per_step": e2e_s * 1e3,
+           "ms_per_call": [round(t * 1e3, 3) for t in e2e_times],
            "api": "from_particles(pinned (N,2)) -> build -> evaluate_all(pinned targets)"}
 
     flops_all = allsum(flops)
