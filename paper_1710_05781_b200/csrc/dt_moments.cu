@@ -309,6 +309,11 @@ __device__ __forceinline__ void shift_child(const double *__restrict__ row, int 
 // Node `node` (internal) formed by the lane pair (sub 0: left child, sub 1:
 // right child); each lane then stores half of the row.  Both lanes of the
 // pair must call it (inactive pairs with node < 0).
+#ifdef DT_UP_TRACE
+// development (tools/upward_levels.py): [0] kernel start (min over blocks),
+// [1 + L] the last formation of level L
+__device__ unsigned long long g_uptrace[72];
+#endif
 __device__ __forceinline__ void form_node_pair(const MomArgs &a, int64_t node, int sub)
 {
     const int o1 = (int)a.order + 1;
@@ -344,6 +349,16 @@ __device__ __forceinline__ void form_node_pair(const MomArgs &a, int64_t node, i
     }
     if (node < 0)
         return;
+#ifdef DT_UP_TRACE
+    if (sub == 0) {
+        unsigned long long t_;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
+        int L = 0;
+        while (L < 60 && __ldg(a.meta + DT_META_LEVEL0 + L + 1) <= node)
+            ++L;
+        atomicMax(g_uptrace + 1 + L, t_);
+    }
+#endif
     double2 *dst = reinterpret_cast<double2 *>(a.meval + node * es);
 #pragma unroll
     for (int k = 0; k < REG_ORDER / 2; k += 2) {
@@ -378,6 +393,13 @@ __global__ void __launch_bounds__(256, DT_UP_MINB) upward_kernel(MomArgs a)
     // leaves below this node index were formed by the build's idle blocks
     // (dt_build_tree_p2m); they only climb here
     const int64_t preformed = a.plan ? 0 : __ldg(a.meta + DT_META_P2M_UPTO);
+#ifdef DT_UP_TRACE
+    if (threadIdx.x == 0) {
+        unsigned long long t_;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
+        atomicMin(g_uptrace, t_);
+    }
+#endif
     const int64_t n = __ldg(a.meta + DT_META_NODES);
     int64_t cut_begin = 0, lo = 0, hi = 0;
     if (a.plan) {
@@ -881,3 +903,18 @@ extern "C" int dt_shard_finish(const int64_t *plan, int world, int64_t cut_level
     }
     return DT_OK;
 }
+
+#ifdef DT_UP_TRACE
+extern "C" int dt_debug_uptrace(unsigned long long *host, int reset)
+{
+    cudaMemcpyFromSymbol(host, g_uptrace, sizeof(g_uptrace));
+    if (reset) {
+        unsigned long long z[72];
+        for (int i = 0; i < 72; ++i)
+            z[i] = 0;
+        z[0] = ~0ull;
+        cudaMemcpyToSymbol(g_uptrace, z, sizeof(z));
+    }
+    return 0;
+}
+#endif

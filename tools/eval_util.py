@@ -41,3 +41,6 @@ print("mean pmax %.2f, mean pmin %.2f, mean pu %.2f" % (u[3] / u[1], u[5] / u[1]
 print("near lane util: %.3f" % (u[7] / (32 * u[6])))
 print("far events/target %.2f near pairs/target (executed lanes) %.1f" % (u[2] / T, u[8] * 32 / T))
 print("table calls (lane 0) %d, table misses (lane 0) %d" % (u[10], u[11]))
+print("two-child opens %.1f per task: all lanes accept the first child %.1f, accept both %.1f; "
+      "lanes accepting the first child %.1f per open" % (u[12] / u[9], u[13] / u[9], u[14] / u[9],
+                                                        u[15] / max(u[12], 1)))
