@@ -68,7 +68,19 @@ class ChargeSystem:
     xs: torch.Tensor
     qs: torch.Tensor
     prefix: torch.Tensor
-    total: float
+    total: float | None = None  # None: prefix[-1], read on first access
+
+    def __getattribute__(self, name):
+        # the total is read back from the device only when asked for, so
+        # building a system does not wait for its prefix scan
+        if name == "total":
+            v = object.__getattribute__(self, "total")
+            if v is None:
+                pre = object.__getattribute__(self, "prefix")
+                v = float(pre[-1]) if pre.numel() else 0.0
+                object.__setattr__(self, "total", v)
+            return v
+        return object.__getattribute__(self, name)
 
     def __post_init__(self) -> None:
         for name in ("xs", "qs", "prefix"):
@@ -95,9 +107,7 @@ def from_sorted(xs, qs) -> ChargeSystem:
     if they are float64 CUDA tensors)."""
     x = _to_device(xs)
     q = _to_device(qs)
-    pre = prefix_sum(q)
-    total = float(pre[-1]) if pre.numel() else 0.0
-    return ChargeSystem(xs=x, qs=q, prefix=pre, total=total)
+    return ChargeSystem(xs=x, qs=q, prefix=prefix_sum(q))
 
 
 def check_values(v: torch.Tensor, flags: torch.Tensor | None = None) -> torch.Tensor:
@@ -164,12 +174,16 @@ def from_particles(raw) -> ChargeSystem:
         _lib.check(_lib.load().dt_unpack_pairs(_lib.ptr(arr), n, _lib.ptr(x), _lib.ptr(q),
                                                _lib.ptr(flags), _lib.stream_handle()),
                    "dt_unpack_pairs")
+    # the prefix of the (usually already sorted) input is enqueued before the
+    # host reads the flags, so the scan runs while the host waits
+    pre = prefix_sum(q)
     bad, desc = flags.tolist()
     if bad:
         raise ValueError("positions and strengths must all be finite")
     if desc:  # stable sort by position (charges.py:127), q carried along
         x, _, q = sort_stable(x, q)
-    return from_sorted(x, q)
+        pre = prefix_sum(q)
+    return ChargeSystem(xs=x, qs=q, prefix=pre)
 
 
 def _sign_terms(system: ChargeSystem, targets: torch.Tensor) -> torch.Tensor:

@@ -11,10 +11,11 @@ in the reference's breadth-first layout and are bit-identical to it.
 from __future__ import annotations
 
 import ctypes as C
-import time
+import threading
 from dataclasses import dataclass, field
 
 import numpy as np
+
 import torch
 
 from . import _lib
@@ -71,7 +72,7 @@ class Tree:
     moment_order: int
     depth: int
     leaf_count: int
-    build_seconds: float
+    build_seconds: float  # given as (start, end) CUDA events, read when asked
     # device-side extras for the traversal kernel: meval holds the moments in
     # the traversal layout (dt_moments moments_eval), the only layout the
     # upward pass writes for moment order <= 31
@@ -80,6 +81,16 @@ class Tree:
     xq: torch.Tensor = field(repr=False, default=None)
     meta: torch.Tensor = field(repr=False, default=None)
     moments_ref: torch.Tensor | None = field(repr=False, default=None)
+
+    def __getattribute__(self, name):
+        if name == "build_seconds":
+            v = object.__getattribute__(self, "build_seconds")
+            if isinstance(v, tuple):  # events around the build on its stream
+                v[1].synchronize()
+                v = v[0].elapsed_time(v[1]) * 1e-3
+                object.__setattr__(self, "build_seconds", v)
+            return v
+        return object.__getattribute__(self, name)
 
     def __len__(self) -> int:
         return int(self.lo.shape[0])
@@ -280,8 +291,10 @@ def _build(system: ChargeSystem, config: EvalConfig, upward) -> Tree:
     order <= 31 only the traversal rows are formed (moments is None); the
     reference layout is derived on first access of Tree.moments."""
     dev = _lib.require_device()
-    torch.cuda.synchronize(dev)
-    t0 = time.perf_counter()
+    # build time from events on the stream: the host does not wait for the
+    # moments (Tree.build_seconds reads the events when asked)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record()
     n = len(system)
     order = moment_order_for(config)
     # orders <= 31 on one device: the build's idle blocks start the leaves'
@@ -309,15 +322,14 @@ def _build(system: ChargeSystem, config: EvalConfig, upward) -> Tree:
     else:
         upward(bufs, order, moments, meval)
         pack_sources(system.xs, system.qs, xq)
-    torch.cuda.synchronize(dev)
-    elapsed = time.perf_counter() - t0
+    ev1.record()
     return Tree(
         system=system,
         lo=bufs.lo[:n_nodes], hi=bufs.hi[:n_nodes], center=bufs.center[:n_nodes],
         half=bufs.half[:n_nodes], level=bufs.level[:n_nodes], start=bufs.start[:n_nodes],
         end=bufs.end[:n_nodes], left=bufs.left[:n_nodes], right=bufs.right[:n_nodes],
         moment_order=order, depth=int(meta[_lib.DT_META_DEPTH]),
-        leaf_count=int(meta[_lib.DT_META_LEAVES]), build_seconds=elapsed,
+        leaf_count=int(meta[_lib.DT_META_LEAVES]), build_seconds=(ev0, ev1),
         meval=meval[:n_nodes], packed=bufs.packed[: n_nodes * 32], xq=xq, meta=bufs.meta,
         moments_ref=moments,
     )
@@ -364,7 +376,7 @@ def tree_phi_sum(tree: Tree, kernel: DiscKernel, config: EvalConfig, ys: torch.T
         return
     cos_t, sin_t = contour_tables(ys.device)
     if workspace is None:
-        workspace = torch.empty(_lib.DT_EVAL_COUNTER_BYTES, dtype=torch.uint8, device=ys.device)
+        workspace = _workspace(ys.device, _lib.DT_EVAL_COUNTER_BYTES)
     p = _lib.ptr
     _lib.check(
         _lib.load().dt_tree_phi_sum_packed(
@@ -398,6 +410,38 @@ def evaluate_point(tree: Tree, kernel: DiscKernel, config: EvalConfig, y: float)
     return float(out[0])
 
 
+_WS = threading.local()
+
+
+def _workspace(dev, nbytes: int) -> torch.Tensor:
+    """A traversal workspace kept per thread and device: reusing it keeps the
+    cached adaptive-order tables (their key lives in the slot) and skips an
+    allocation per call.  Per thread, since a call owns it until it returns."""
+    cache = getattr(_WS, "d", None)
+    if cache is None:
+        cache = _WS.d = {}
+    key = str(dev)
+    ws = cache.get(key)
+    if ws is None or ws.numel() < nbytes:
+        ws = cache[key] = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    return ws
+
+
+def _timing_events():
+    """A start event recorded now on the current stream and its end event:
+    evaluation times are taken on the device, so the host does not have to
+    drain the stream before it starts enqueueing (no idle gap)."""
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    return ev0, ev1
+
+
+def _elapsed(ev0, ev1) -> float:
+    ev1.record()
+    ev1.synchronize()
+    return ev0.elapsed_time(ev1) * 1e-3
+
+
 def evaluate_all(tree: Tree, kernel: DiscKernel, config: EvalConfig, system: ChargeSystem,
                  targets, threads: int | None = 1) -> FieldResult:
     """Field at every target: sign term + tree-accelerated kernel sum
@@ -417,8 +461,7 @@ def evaluate_all(tree: Tree, kernel: DiscKernel, config: EvalConfig, system: Cha
         return _evaluate_host_pipelined(tree, kernel, config, system, host, numpy_out)
     t, back = as_targets(targets)
     dev = t.device
-    torch.cuda.synchronize(dev)
-    start = time.perf_counter()
+    ev0, ev1 = _timing_events()
     values = _sign_terms(system, t)
     T = t.numel()
     if T:
@@ -429,8 +472,7 @@ def evaluate_all(tree: Tree, kernel: DiscKernel, config: EvalConfig, system: Cha
             permute(vs, perm, scatter=True, out=values)
         else:
             tree_phi_sum(tree, kernel, config, t, values)
-    torch.cuda.synchronize(dev)
-    elapsed = time.perf_counter() - start
+    elapsed = _elapsed(ev0, ev1)
     return FieldResult(values=back(values), build_time=tree.build_seconds, eval_time=elapsed,
                        method="tree")
 
@@ -447,8 +489,7 @@ def _looks_sorted(host: torch.Tensor) -> bool:
     are ascending; unsorted targets take the sorting path.  Results never
     depend on it: the traversal is exact for targets in any order."""
     n = host.numel()
-    idx = torch.linspace(0, n - 1, min(n, 4097)).to(torch.int64)
-    s = host[idx]
+    s = host.numpy()[np.linspace(0, n - 1, min(n, 4097)).astype(np.int64)]
     return bool((s[1:] >= s[:-1]).all())
 
 
@@ -476,8 +517,7 @@ def _evaluate_host_pipelined(tree: Tree, kernel: DiscKernel, config: EvalConfig,
     ready = torch.cuda.Event()
     ready.record(main)
     comps[1].wait_event(ready)  # the tree and flags were made on the main stream
-    torch.cuda.synchronize(dev)
-    start = time.perf_counter()
+    ev0, ev1 = _timing_events()
     keep = []  # pinned staging buffers stay alive until the copies finish
     for c, (i0, i1) in enumerate(chunks):
         comp, k = comps[c % 2], c % 2
@@ -515,8 +555,8 @@ def _evaluate_host_pipelined(tree: Tree, kernel: DiscKernel, config: EvalConfig,
     fin = torch.cuda.Event()
     fin.record(comps[1])
     main.wait_event(fin)
+    elapsed = _elapsed(ev0, ev1)
     bad, _ = flags.tolist()
-    elapsed = time.perf_counter() - start
     if bad:
         raise ValueError("targets must all be finite")
     values = out_h.numpy() if numpy_out else out_h
@@ -534,11 +574,10 @@ def _evaluate_host_mapped(tree: Tree, kernel: DiscKernel, config: EvalConfig,
     T = host.numel()
     out_h = torch.empty(T, dtype=torch.float64, pin_memory=True)
     flags = _lib.zeros_i64(2, dev)
-    ws = torch.empty(int(_lib.load().dt_tree_field_workspace(T)), dtype=torch.uint8, device=dev)
+    ws = _workspace(dev, int(_lib.load().dt_tree_field_workspace(T)))
     cos_t, sin_t = contour_tables(dev)
     p = _lib.ptr
-    torch.cuda.synchronize(dev)
-    start = time.perf_counter()
+    ev0, ev1 = _timing_events()
     _lib.check(
         _lib.load().dt_tree_field_packed(
             p(tree.packed), len(tree), p(tree.meval), tree.meval.shape[1], p(tree.xq),
@@ -550,8 +589,8 @@ def _evaluate_host_mapped(tree: Tree, kernel: DiscKernel, config: EvalConfig,
         ),
         "dt_tree_field_packed",
     )
-    bad, _ = flags.tolist()  # synchronises
-    elapsed = time.perf_counter() - start
+    elapsed = _elapsed(ev0, ev1)  # synchronises
+    bad, _ = flags.tolist()
     if bad:
         raise ValueError("targets must all be finite")
     values = out_h.numpy() if numpy_out else out_h
