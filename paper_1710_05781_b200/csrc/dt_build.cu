@@ -62,6 +62,7 @@ struct BuildArgs {
     // one-pass top (count, or -1 when the top was not built in one pass)
     int64_t *deep_count;
     struct Front *deep_list;
+    double *dy_samples;      // every stride-th source (dyadic_splits)
 };
 
 // A frontier node of a block-0 run: kept in shared memory from one level to
@@ -178,28 +179,88 @@ __device__ __forceinline__ void root_interval(const BuildArgs &a, double *lo, do
 
 // Phase 0: dy_mid / dy_split for dyadic interval idx (level L = floor(log2(idx + 1)),
 // position k = idx + 1 - 2^L), following the same midpoint arithmetic as the build.
-__device__ void dyadic_splits(const BuildArgs &a)
+// The lower_bounds are found in two steps: every stride-th source is copied
+// to a sample array (<= 2^18 values, L2-resident), a grid barrier, then each
+// midpoint is bisected over the samples and finished inside one stride of xs
+// (the same index as one search over xs[0:n]: lower_bound is unique).  The
+// searches then touch one or two DRAM lines each instead of ~12.
+constexpr int64_t DY_SAMPLES = (int64_t)1 << 18;
+
+#ifdef DT_BUILD_TRACE
+#define DY_STAMP(slot)                                                                       \
+    if (blockIdx.x == 0 && threadIdx.x == 0) {                                               \
+        unsigned long long t_;                                                               \
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                              \
+        a.block_total[2048 + (slot)] = (int64_t)t_;                                          \
+    }
+#else
+#define DY_STAMP(slot)
+#endif
+
+__device__ void dyadic_splits(const BuildArgs &a, cg::grid_group &grid)
 {
+    const int64_t stride = (a.n + DY_SAMPLES - 1) / DY_SAMPLES;
+    const int64_t ns = (a.n + stride - 1) / stride;
+    const int tid = blockIdx.x * blockDim.x + threadIdx.x;
+    const int nth = gridDim.x * blockDim.x;
+    for (int64_t i = tid; i < ns; i += nth)
+        a.dy_samples[i] = __ldcs(a.xs + i * stride);
     double lo0, hi0;
     root_interval(a, &lo0, &hi0);
-    for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < DYADIC;
-         idx += gridDim.x * blockDim.x) {
+    DY_STAMP(73)
+    grid.sync();
+    DY_STAMP(74)
+    const double *smp = a.dy_samples;
+    for (int idx = tid; idx < DYADIC; idx += nth) {
         const int L = 31 - __clz(idx + 1);
         const int k = idx + 1 - (1 << L);
         double lo = lo0, hi = hi0;
         for (int b = L - 1; b >= 0; --b) {
-            const double mid = mid_of(lo, hi);
+            const double m = mid_of(lo, hi);
             if ((k >> b) & 1)
-                lo = mid;
+                lo = m;
             else
-                hi = mid;
+                hi = m;
         }
         const double mid = mid_of(lo, hi);
         a.dy_mid[idx] = mid;
-        a.dy_split[idx] = dt_lower_bound(a.xs, 0, a.n, mid);
         if (!(lo < mid && mid < hi))  // degenerate interval: no one-pass top
             atomicOr(a.irregular, 1u);
+        // first sample >= mid
+        int64_t l = 0, h = ns;
+        while (l < h) {
+            const int64_t m = (l + h) >> 1;
+            if (smp[m] < mid)
+                l = m + 1;
+            else
+                h = m;
+        }
+        // the answer lies in [s0, s1]: xs[s0 - 1] < mid <= xs[s1] (or s1 = n)
+        int64_t s0 = l == 0 ? 0 : (l - 1) * stride + 1;
+        int64_t s1 = l == ns ? a.n : l * stride;
+        if (l > 0 && l < ns && s1 - s0 > 1) {
+            // probe where the two bracketing samples put mid (on a locally
+            // smooth mesh usually next to the answer), then its neighbour;
+            // every outcome keeps the exact bracket
+            const double xa = smp[l - 1], xb = smp[l];
+            const double f = (mid - xa) / (xb - xa);
+            int64_t g = s0 + (int64_t)(f * (double)(s1 - s0));
+            g = g < s0 ? s0 : g > s1 - 1 ? s1 - 1 : g;
+            if (__ldg(a.xs + g) < mid)
+                s0 = g + 1;
+            else
+                s1 = g;
+            if (s0 < s1) {
+                const int64_t g2 = s0 == g + 1 ? s0 : s1 - 1;
+                if (__ldg(a.xs + g2) < mid)
+                    s0 = g2 + 1;
+                else
+                    s1 = g2;
+            }
+        }
+        a.dy_split[idx] = dt_lower_bound(a.xs, s0, s1, mid);
     }
+    DY_STAMP(75)
 }
 
 // Number of children of frontier node `node` (0 if it is a leaf) and split.
@@ -250,7 +311,28 @@ __device__ __forceinline__ int64_t sampled_lower_bound(const BuildArgs &a, const
         g = dt_lower_bound(a.xs, wlo, whi, v);
     }
 #else
-    const int64_t g = dt_lower_bound(a.xs, wlo, whi, v);
+    int64_t w0 = wlo, w1 = whi;
+    if (lo > 0 && lo < sm.count && w1 - w0 > 1) {
+        // probe where the bracketing samples put v (a locally smooth mesh
+        // puts the answer next to it), then the neighbour; every outcome
+        // keeps the exact bracket [w0, w1]
+        const double xa = sm.v[lo - 1], xb = sm.v[lo];
+        const double f = (v - xa) / (xb - xa);
+        int64_t g = w0 + (int64_t)(f * (double)(w1 - w0));
+        g = g < w0 ? w0 : g > w1 - 1 ? w1 - 1 : g;
+        if (__ldg(a.xs + g) < v)
+            w0 = g + 1;
+        else
+            w1 = g;
+        if (w0 < w1) {
+            const int64_t g2 = w0 == g + 1 ? w0 : w1 - 1;
+            if (__ldg(a.xs + g2) < v)
+                w0 = g2 + 1;
+            else
+                w1 = g2;
+        }
+    }
+    const int64_t g = dt_lower_bound(a.xs, w0, w1, v);
 #endif
     return g < s ? s : (g > e ? e : g);
 }
@@ -656,7 +738,7 @@ __global__ void __launch_bounds__(BUILD_THREADS) build_kernel(BuildArgs a)
 #define BUILD_STAMP(slot)
 #endif
     BUILD_STAMP(70)
-    dyadic_splits(a);
+    dyadic_splits(a, grid);
     grid.sync();
     BUILD_STAMP(71)
     int64_t lev = build_top(a, grid, warp_sums, top_bases_s, top_bases2_s);
@@ -894,7 +976,7 @@ extern "C" size_t dt_build_workspace(int64_t n, int64_t node_capacity)
     (void)n;
     return (size_t)node_capacity * 2 * sizeof(int32_t) + 4096 * sizeof(int64_t) + 16 +
            (size_t)DYADIC * (sizeof(int64_t) + sizeof(double)) + 32 + 64 +
-           ((size_t)1 << DYADIC_LEVELS) * sizeof(Front);
+           ((size_t)1 << DYADIC_LEVELS) * sizeof(Front) + (size_t)DY_SAMPLES * sizeof(double);
 }
 
 static int build_launch(const double *xs, int64_t n, int64_t leaf_capacity, int64_t max_depth,
@@ -956,6 +1038,7 @@ static int build_launch(const double *xs, int64_t n, int64_t leaf_capacity, int6
     a.p2m_ctr = (unsigned long long *)(a.irregular + 2);
     a.deep_count = (int64_t *)(a.p2m_ctr + 1);
     a.deep_list = (Front *)(((uintptr_t)(a.deep_count + 1) + 31) & ~(uintptr_t)31);
+    a.dy_samples = (double *)(a.deep_list + ((size_t)1 << DYADIC_LEVELS));
     a.p2m_kmax = 0;
     if (p2m) {
         a.p2m = *p2m;

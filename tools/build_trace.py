@@ -22,6 +22,10 @@ depth = int(bufs.meta[1])
 t = bt[2048: 2048 + depth + 2]
 ph = bt[2048 + 70: 2048 + 73]
 print("dyadic splits + barrier %.1f us, one-pass top %.1f us" % ((ph[1] - ph[0]) / 1e3, (ph[2] - ph[1]) / 1e3))
+dy = bt[2048 + 73: 2048 + 76]
+if dy.min() > 0:
+    print("  sample copy %.1f us, sample barrier %.1f us, searches %.1f us, final barrier %.1f us" % (
+        (dy[0] - ph[0]) / 1e3, (dy[1] - dy[0]) / 1e3, (dy[2] - dy[1]) / 1e3, (ph[1] - dy[2]) / 1e3))
 lv = bufs.meta[8: 8 + depth + 2].cpu().numpy()
 print("per-level us (level: nodes us):")
 for l in range(depth + 1):
