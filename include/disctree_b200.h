@@ -358,6 +358,28 @@ int dt_tree_eval_device(const void *packed_nodes, const int64_t *meta, int64_t n
                         int64_t i0, int64_t i1, int accumulate, void *workspace,
                         size_t workspace_bytes, void *stream);
 
+/* dt_tree_eval_device in two launches, so the order tables can be built on
+ * another stream while the moments are formed: dt_eval_prepare zeroes the
+ * workspace slot's task counters and builds the tables (same arguments;
+ * ys/out are not read); dt_tree_eval_device_prepared then runs only the
+ * traversal on that slot, after the prepare call in stream order (an event
+ * when the streams differ).  The result equals dt_tree_eval_device's. */
+int dt_eval_prepare(const void *packed_nodes, const int64_t *meta, int64_t node_capacity,
+                    const double *moments, int64_t moment_stride, const double *xq,
+                    int64_t n_src, double rd2, double theta, int64_t p, int adaptive,
+                    double tolerance, int64_t p_cap, const double *cos_tab,
+                    const double *sin_tab, int64_t n_samples, const double *ys, double *out,
+                    int64_t i0, int64_t i1, int accumulate, void *workspace,
+                    size_t workspace_bytes, void *stream);
+int dt_tree_eval_device_prepared(const void *packed_nodes, const int64_t *meta,
+                                 int64_t node_capacity, const double *moments,
+                                 int64_t moment_stride, const double *xq, int64_t n_src,
+                                 double rd2, double theta, int64_t p, int adaptive,
+                                 double tolerance, int64_t p_cap, const double *cos_tab,
+                                 const double *sin_tab, int64_t n_samples, const double *ys,
+                                 double *out, int64_t i0, int64_t i1, int accumulate,
+                                 void *workspace, size_t workspace_bytes, void *stream);
+
 /* Adaptive order for n (R, h) pairs (test hook for _kernels.py:212-231):
  * p_out[i] = order chosen; tier_out[i] (may be NULL) = 0 fast path, 1 exact. */
 int dt_choose_p_batch(const double *big_r, const double *h, int64_t n, double rd2,

@@ -134,6 +134,16 @@ SIGNATURES = {
         [_P, _P, _I64, _P, _I64, _P, _I64, _D, _D, _I64, C.c_int, _D, _I64, _P, _P, _I64, _P,
          _P, _I64, _I64, C.c_int, _P, _SZ, _P],
     ),
+    "dt_eval_prepare": (
+        C.c_int,
+        [_P, _P, _I64, _P, _I64, _P, _I64, _D, _D, _I64, C.c_int, _D, _I64, _P, _P, _I64, _P,
+         _P, _I64, _I64, C.c_int, _P, _SZ, _P],
+    ),
+    "dt_tree_eval_device_prepared": (
+        C.c_int,
+        [_P, _P, _I64, _P, _I64, _P, _I64, _D, _D, _I64, C.c_int, _D, _I64, _P, _P, _I64, _P,
+         _P, _I64, _I64, C.c_int, _P, _SZ, _P],
+    ),
     "dt_tree_field_device": (
         C.c_int,
         [_P, _P, _I64, _P, _I64, _P, _P, _P, _I64, _D, _D, _I64, C.c_int, _D, _I64, _P, _P,

@@ -1267,9 +1267,14 @@ int launch_fused(EvalArgs &a, bool adaptive, bool stats, cudaStream_t s, int64_t
 
 // a.counter: the DT_EVAL_COUNTER_BYTES task-counter slot at the start of the
 // caller's workspace (zeroed here, stream-ordered).
-int launch_eval(EvalArgs &a, bool adaptive, bool stats, cudaStream_t s)
+// Zero the task counters and build the order tables in the workspace slot
+// (when the tables apply); a.pt_bp / a.pt_bins point at them afterwards.
+// With build == false only the pointers are set: the tables were built
+// earlier in stream order (dt_eval_prepare, possibly on another stream).
+int prepare_eval(EvalArgs &a, bool adaptive, cudaStream_t s, bool build)
 {
-    DT_CUDA_TRY(cudaMemsetAsync(a.counter, 0, PT_BP_OFFSET, s));
+    if (build)
+        DT_CUDA_TRY(cudaMemsetAsync(a.counter, 0, PT_BP_OFFSET, s));
     a.pt_bp = nullptr;
     a.pt_bins = nullptr;
     if (adaptive && a.n_samples == 64 && a.psel_mode == DT_PSEL_FAST && a.p_cap <= PT_N - 1 &&
@@ -1278,13 +1283,24 @@ int launch_eval(EvalArgs &a, bool adaptive, bool stats, cudaStream_t s)
         unsigned char *bins = reinterpret_cast<unsigned char *>(a.counter) + PT_BINS_OFFSET;
         unsigned *bad = reinterpret_cast<unsigned *>(reinterpret_cast<char *>(a.counter) + PT_BAD_OFFSET);
         PtKey *key = reinterpret_cast<PtKey *>(reinterpret_cast<char *>(a.counter) + PT_KEY_OFFSET);
-        psel_breakpoints_kernel<<<(PT_LEVELS * PT_N * 32 + 255) / 256, 256, 0, s>>>(a, bp, bad,
-                                                                                   key);
-        psel_bins_kernel<<<(PT_LEVELS * PT_BINS + 255) / 256, 256, 0, s>>>(a, bp, bad, bins, key);
-        DT_CUDA_TRY(cudaGetLastError());
+        if (build) {
+            psel_breakpoints_kernel<<<(PT_LEVELS * PT_N * 32 + 255) / 256, 256, 0, s>>>(a, bp, bad,
+                                                                                       key);
+            psel_bins_kernel<<<(PT_LEVELS * PT_BINS + 255) / 256, 256, 0, s>>>(a, bp, bad, bins,
+                                                                               key);
+            DT_CUDA_TRY(cudaGetLastError());
+        }
         a.pt_bp = bp;
         a.pt_bins = bins;
     }
+    return DT_OK;
+}
+
+int launch_eval(EvalArgs &a, bool adaptive, bool stats, cudaStream_t s, bool prepared = false)
+{
+    const int rc = prepare_eval(a, adaptive, s, !prepared);
+    if (rc != DT_OK)
+        return rc;
     return launch_fused(a, adaptive, stats, s, 0);
 }
 
@@ -1499,14 +1515,13 @@ extern "C" int dt_tree_field_packed(const void *packed_nodes, int64_t n_nodes,
     return launch_eval(a, adaptive != 0, false, (cudaStream_t)stream);
 }
 
-extern "C" int dt_tree_eval_device(const void *packed_nodes, const int64_t *meta,
-                                   int64_t node_capacity, const double *moments,
-                                   int64_t moment_stride, const double *xq, int64_t n_src,
-                                   double rd2, double theta, int64_t p, int adaptive,
-                                   double tolerance, int64_t p_cap, const double *cos_tab,
-                                   const double *sin_tab, int64_t n_samples, const double *ys,
-                                   double *out, int64_t i0, int64_t i1, int accumulate,
-                                   void *workspace, size_t workspace_bytes, void *stream)
+static int tree_eval_device(const void *packed_nodes, const int64_t *meta,
+                            int64_t node_capacity, const double *moments, int64_t moment_stride,
+                            const double *xq, int64_t n_src, double rd2, double theta, int64_t p,
+                            int adaptive, double tolerance, int64_t p_cap, const double *cos_tab,
+                            const double *sin_tab, int64_t n_samples, const double *ys,
+                            double *out, int64_t i0, int64_t i1, int accumulate, void *workspace,
+                            size_t workspace_bytes, void *stream, int mode)
 {
     DT_CHECK_ARG(meta != nullptr, "null meta");
     int rc = check_eval_args(node_capacity, n_src, p, adaptive, tolerance, p_cap, n_samples, rd2,
@@ -1548,7 +1563,52 @@ extern "C" int dt_tree_eval_device(const void *packed_nodes, const int64_t *meta
     a.psel_mode = DT_PSEL_FAST;
     a.stats = dt_eval_stats{nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
     a.counter = (unsigned long long *)workspace;
-    return launch_eval(a, adaptive != 0, false, (cudaStream_t)stream);
+    if (mode == 1)  // tables only (dt_eval_prepare)
+        return prepare_eval(a, adaptive != 0, (cudaStream_t)stream, true);
+    return launch_eval(a, adaptive != 0, false, (cudaStream_t)stream, mode == 2);
+}
+
+extern "C" int dt_tree_eval_device(const void *packed_nodes, const int64_t *meta,
+                                   int64_t node_capacity, const double *moments,
+                                   int64_t moment_stride, const double *xq, int64_t n_src,
+                                   double rd2, double theta, int64_t p, int adaptive,
+                                   double tolerance, int64_t p_cap, const double *cos_tab,
+                                   const double *sin_tab, int64_t n_samples, const double *ys,
+                                   double *out, int64_t i0, int64_t i1, int accumulate,
+                                   void *workspace, size_t workspace_bytes, void *stream)
+{
+    return tree_eval_device(packed_nodes, meta, node_capacity, moments, moment_stride, xq, n_src,
+                            rd2, theta, p, adaptive, tolerance, p_cap, cos_tab, sin_tab,
+                            n_samples, ys, out, i0, i1, accumulate, workspace, workspace_bytes,
+                            stream, 0);
+}
+
+extern "C" int dt_eval_prepare(const void *packed_nodes, const int64_t *meta,
+                               int64_t node_capacity, const double *moments,
+                               int64_t moment_stride, const double *xq, int64_t n_src,
+                               double rd2, double theta, int64_t p, int adaptive, double tolerance,
+                               int64_t p_cap, const double *cos_tab, const double *sin_tab,
+                               int64_t n_samples, const double *ys, double *out, int64_t i0,
+                               int64_t i1, int accumulate, void *workspace,
+                               size_t workspace_bytes, void *stream)
+{
+    return tree_eval_device(packed_nodes, meta, node_capacity, moments, moment_stride, xq, n_src,
+                            rd2, theta, p, adaptive, tolerance, p_cap, cos_tab, sin_tab,
+                            n_samples, ys, out, i0, i1, accumulate, workspace, workspace_bytes,
+                            stream, 1);
+}
+
+extern "C" int dt_tree_eval_device_prepared(
+    const void *packed_nodes, const int64_t *meta, int64_t node_capacity, const double *moments,
+    int64_t moment_stride, const double *xq, int64_t n_src, double rd2, double theta, int64_t p,
+    int adaptive, double tolerance, int64_t p_cap, const double *cos_tab, const double *sin_tab,
+    int64_t n_samples, const double *ys, double *out, int64_t i0, int64_t i1, int accumulate,
+    void *workspace, size_t workspace_bytes, void *stream)
+{
+    return tree_eval_device(packed_nodes, meta, node_capacity, moments, moment_stride, xq, n_src,
+                            rd2, theta, p, adaptive, tolerance, p_cap, cos_tab, sin_tab,
+                            n_samples, ys, out, i0, i1, accumulate, workspace, workspace_bytes,
+                            stream, 2);
 }
 
 extern "C" int dt_tree_field_device(const void *packed_nodes, const int64_t *meta,

@@ -77,7 +77,11 @@ class TreePipeline:
         self.sign_ws = torch.empty(self.sign_ws_bytes, dtype=torch.uint8, device=self.dev)
         self.cos_t, self.sin_t = contour_tables(self.dev)
         self.side = torch.cuda.Stream(self.dev)
+        # a third stream builds the traversal's order tables beside the upward
+        # pass (dt_eval_prepare) instead of in front of the traversal
+        self.tabs = torch.cuda.Stream(self.dev)
         self.ev_scan, self.ev_side = torch.cuda.Event(), torch.cuda.Event()
+        self.ev_tabs = torch.cuda.Event()
         # world > 1: sharded upward pass (one all-gather of cut-level rows)
         self.shard = None
         if world > 1 and self.order + 1 <= 32:  # higher orders: replicated moments
@@ -148,6 +152,19 @@ class TreePipeline:
                                            self.sign_ws_bytes, _lib.stream_handle()),
                            "dt_sign_terms")
             self.ev_side.record(self.side)
+        eval_args = None
+        if not self.fused_sign:
+            eval_args = (p(self.bufs.packed), p(self.bufs.meta), self.bufs.capacity,
+                         p(self.meval), self.estride, p(self.xq), self.n,
+                         self.kernel.r_d * self.kernel.r_d, float(cfg.theta), int(cfg.p),
+                         int(bool(cfg.adaptive)), float(cfg.tolerance), self.order,
+                         p(self.cos_t), p(self.sin_t), self.cos_t.numel(), p(ys), p(out),
+                         int(i0), int(i1), 1, p(self.eval_ws), self.eval_ws.numel())
+            # the tables need only the tree's node records and depth
+            self.tabs.wait_event(self.ev_scan)
+            with torch.cuda.stream(self.tabs):
+                _lib.check(L.dt_eval_prepare(*eval_args, _lib.stream_handle()), "dt_eval_prepare")
+                self.ev_tabs.record(self.tabs)
         if self.shard is None:  # moments + the traversal's (x, q) pairs (dt_moments_pack)
             launch_moments(self.bufs, xs, qs, self.order, self.moments, self.meval, xq=self.xq)
         else:  # this rank's subtrees + all-gather of the cut-level rows
@@ -168,17 +185,9 @@ class TreePipeline:
                 "dt_tree_field_device",
             )
         else:
-            _lib.check(
-                L.dt_tree_eval_device(
-                    p(self.bufs.packed), p(self.bufs.meta), self.bufs.capacity, p(self.meval),
-                    self.estride, p(self.xq), self.n, self.kernel.r_d * self.kernel.r_d,
-                    float(cfg.theta), int(cfg.p), int(bool(cfg.adaptive)),
-                    float(cfg.tolerance), self.order, p(self.cos_t), p(self.sin_t),
-                    self.cos_t.numel(), p(ys), p(out), int(i0), int(i1), 1, p(self.eval_ws),
-                    self.eval_ws.numel(), s,
-                ),
-                "dt_tree_eval_device",
-            )
+            main.wait_event(self.ev_tabs)
+            _lib.check(L.dt_tree_eval_device_prepared(*eval_args, s),
+                       "dt_tree_eval_device_prepared")
         if eval_events is not None:
             eval_events[1].record()
 
