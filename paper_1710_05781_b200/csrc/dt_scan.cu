@@ -283,7 +283,7 @@ __global__ void __launch_bounds__(SCAN_THREADS, DT_SCAN_MINB) scan_onepass_kerne
 // the range is staged in shared memory and every target is located there;
 // otherwise each target is searched in global memory.
 #ifndef DT_SIGN_PER_THREAD
-#define DT_SIGN_PER_THREAD 2  // 512-target tiles: 0.159 ms at configs[2] (8: 0.201, 4: 0.171, 1: 0.206)
+#define DT_SIGN_PER_THREAD 2  // 512-target tiles: 0.154 ms at configs[2] (4: 0.166, 1: 0.193)
 #endif
 #ifndef DT_SIGN_SMEM
 #define DT_SIGN_SMEM 1024
@@ -314,6 +314,24 @@ __global__ void __launch_bounds__(SIGN_THREADS) sign_terms_kernel(
     __shared__ double xsm[SIGN_SMEM];
     const int64_t t0 = (int64_t)blockIdx.x * SIGN_TILE;
     const int64_t t1 = min(t, t0 + SIGN_TILE);
+    if (n == 0) {
+#pragma unroll
+        for (int k = 0; k < SIGN_PER_THREAD; ++k) {
+            const int64_t i = t0 + (int64_t)k * SIGN_THREADS + threadIdx.x;
+            if (i < t1)
+                e[i] = 0.0;
+        }
+        return;
+    }
+    // the bracket is read with the targets, and the source range staged
+    // before the sortedness of the tile is known (discarded if it is not):
+    // two dependent rounds of global loads before the searches instead of four
+    int64_t blo = 0, bhi = n;
+    if (bracket) {
+        // the next tile's first target bounds this tile's last one from above
+        blo = __ldg(bracket + blockIdx.x);
+        bhi = min(n, __ldg(bracket + blockIdx.x + 1) + 1);
+    }
     double y[SIGN_PER_THREAD];
     bool ok = true;
 #pragma unroll
@@ -325,28 +343,17 @@ __global__ void __launch_bounds__(SIGN_THREADS) sign_terms_kernel(
         if (i < t1 && i + 1 < t && !(y[k] <= __ldg(ys + i + 1)))
             ok = false;
     }
-    const bool sorted = __syncthreads_and(ok);
-    if (n == 0) {
-#pragma unroll
-        for (int k = 0; k < SIGN_PER_THREAD; ++k) {
-            const int64_t i = t0 + (int64_t)k * SIGN_THREADS + threadIdx.x;
-            if (i < t1)
-                e[i] = 0.0;
-        }
-        return;
-    }
+    const bool fits = bracket && blo <= bhi && bhi - blo <= SIGN_SMEM;
+    if (fits)
+        for (int64_t j = blo + threadIdx.x; j < bhi; j += SIGN_THREADS)
+            xsm[j - blo] = __ldg(xs + j);
+    const bool sorted = __syncthreads_and(ok);  // also orders the staging
     int64_t lo = 0, hi = n;
     if (sorted && bracket) {
-        // the next tile's first target bounds this tile's last one from above
-        lo = __ldg(bracket + blockIdx.x);
-        hi = min(n, __ldg(bracket + blockIdx.x + 1) + 1);
+        lo = blo;
+        hi = bhi;
     }
-    const bool staged = sorted && bracket && hi - lo <= SIGN_SMEM;
-    if (staged) {
-        for (int64_t j = lo + threadIdx.x; j < hi; j += SIGN_THREADS)
-            xsm[j - lo] = __ldg(xs + j);
-        __syncthreads();
-    }
+    const bool staged = sorted && fits;
     const double total = __ldg(prefix + n - 1);
 #pragma unroll
     for (int k = 0; k < SIGN_PER_THREAD; ++k) {
