@@ -89,6 +89,16 @@ size_t dt_sign_terms_workspace(int64_t n_targets);
 int dt_sign_terms(const double *xs, const double *prefix, int64_t n, const double *ys,
                   double *e_out, int64_t n_targets, void *workspace, size_t workspace_bytes,
                   void *stream);
+/* dt_sign_terms in two launches (the first needs no prefix, so a caller can
+ * run it beside other work): dt_sign_bracket writes the tile brackets into
+ * the workspace (dt_sign_terms_workspace(n_targets) bytes, required), and
+ * dt_sign_terms_bracketed, after it in stream order, computes e from them.
+ * The result equals dt_sign_terms'. */
+int dt_sign_bracket(const double *xs, int64_t n, const double *ys, int64_t n_targets,
+                    void *workspace, size_t workspace_bytes, void *stream);
+int dt_sign_terms_bracketed(const double *xs, const double *prefix, int64_t n, const double *ys,
+                            double *e_out, int64_t n_targets, void *workspace,
+                            size_t workspace_bytes, void *stream);
 
 /* Input validation in one pass (charges.py:114-132 rejects non-finite
  * positions/strengths; direct.py:43-49 non-finite targets; charges.py:200

@@ -69,6 +69,8 @@ SIGNATURES = {
     "dt_prefix_scan": (C.c_int, [_P, _P, _I64, _P, _SZ, _P]),
     "dt_sign_terms_workspace": (_SZ, [_I64]),
     "dt_sign_terms": (C.c_int, [_P, _P, _I64, _P, _P, _I64, _P, _SZ, _P]),
+    "dt_sign_bracket": (C.c_int, [_P, _I64, _P, _I64, _P, _SZ, _P]),
+    "dt_sign_terms_bracketed": (C.c_int, [_P, _P, _I64, _P, _P, _I64, _P, _SZ, _P]),
     "dt_check_values": (C.c_int, [_P, _I64, _P, _P]),
     "dt_unpack_pairs": (C.c_int, [_P, _I64, _P, _P, _P, _P]),
     "dt_density_nodes": (C.c_int, [_D, _D, _I64, _P, _I64, _I64, _P, _P, _D, _P, _P]),

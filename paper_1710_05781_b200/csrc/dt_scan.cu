@@ -452,26 +452,52 @@ extern "C" size_t dt_sign_terms_workspace(int64_t n_targets)
     return (size_t)((n_targets + SIGN_TILE - 1) / SIGN_TILE + 2) * sizeof(int64_t);
 }
 
-extern "C" int dt_sign_terms(const double *xs, const double *prefix, int64_t n, const double *ys,
-                             double *e_out, int64_t n_targets, void *workspace,
-                             size_t workspace_bytes, void *stream)
+static int sign_terms(const double *xs, const double *prefix, int64_t n, const double *ys,
+                      double *e_out, int64_t n_targets, void *workspace, size_t workspace_bytes,
+                      void *stream, int mode)
 {
     DT_CHECK_ARG(n >= 0 && n_targets >= 0, "negative size");
     if (n_targets == 0)
         return DT_OK;
-    DT_CHECK_ARG(ys && e_out && (n == 0 || (xs && prefix)), "null pointer");
+    DT_CHECK_ARG(ys && (mode == 1 || e_out) && (n == 0 || xs) && (mode == 1 || n == 0 || prefix),
+                 "null pointer");
     cudaStream_t s = (cudaStream_t)stream;
     const int64_t nb = (n_targets + SIGN_TILE - 1) / SIGN_TILE;
     int64_t *bracket = nullptr;
     if (workspace && workspace_bytes >= dt_sign_terms_workspace(n_targets) && n > 0) {
         bracket = (int64_t *)workspace;
-        sign_bracket_kernel<<<(unsigned)((nb + 1 + 127) / 128), 128, 0, s>>>(xs, n, ys, n_targets,
-                                                                         bracket, nb);
+        if (mode != 2)
+            sign_bracket_kernel<<<(unsigned)((nb + 1 + 127) / 128), 128, 0, s>>>(xs, n, ys,
+                                                                             n_targets, bracket, nb);
+    } else if (mode != 0 && n > 0) {
+        return dt_set_error(DT_ERR_WORKSPACE, "sign-term workspace too small");
     }
-    sign_terms_kernel<<<(unsigned)nb, SIGN_THREADS, 0, s>>>(xs, prefix, n, ys, e_out, n_targets,
-                                                            bracket, nb);
+    if (mode != 1)
+        sign_terms_kernel<<<(unsigned)nb, SIGN_THREADS, 0, s>>>(xs, prefix, n, ys, e_out,
+                                                                n_targets, bracket, nb);
     DT_CUDA_TRY(cudaGetLastError());
     return DT_OK;
+}
+
+extern "C" int dt_sign_terms(const double *xs, const double *prefix, int64_t n, const double *ys,
+                             double *e_out, int64_t n_targets, void *workspace,
+                             size_t workspace_bytes, void *stream)
+{
+    return sign_terms(xs, prefix, n, ys, e_out, n_targets, workspace, workspace_bytes, stream, 0);
+}
+
+extern "C" int dt_sign_bracket(const double *xs, int64_t n, const double *ys, int64_t n_targets,
+                               void *workspace, size_t workspace_bytes, void *stream)
+{
+    return sign_terms(xs, nullptr, n, ys, nullptr, n_targets, workspace, workspace_bytes, stream,
+                      1);
+}
+
+extern "C" int dt_sign_terms_bracketed(const double *xs, const double *prefix, int64_t n,
+                                       const double *ys, double *e_out, int64_t n_targets,
+                                       void *workspace, size_t workspace_bytes, void *stream)
+{
+    return sign_terms(xs, prefix, n, ys, e_out, n_targets, workspace, workspace_bytes, stream, 2);
 }
 
 // ---- input validation (charges.py:114-132 from_particles, direct.py:43-49

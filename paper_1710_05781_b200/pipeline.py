@@ -139,19 +139,6 @@ class TreePipeline:
         else:
             self.bufs.launch(xs, cfg.leaf_capacity)
         self.ev_scan.record(main)
-        self.side.wait_event(self.ev_scan)
-        with torch.cuda.stream(self.side):
-            _lib.check(L.dt_prefix_scan(p(qs), p(self.prefix), self.n, p(self.scan_ws),
-                                        self.scan_ws_bytes, _lib.stream_handle()),
-                       "dt_prefix_scan")
-            if self.shard is not None:  # the full upward pass writes xq itself
-                pack_sources(xs, qs, self.xq)
-            if not self.fused_sign:
-                _lib.check(L.dt_sign_terms(p(xs), p(self.prefix), self.n, p(ys_part),
-                                           p(out_part), i1 - i0, p(self.sign_ws),
-                                           self.sign_ws_bytes, _lib.stream_handle()),
-                           "dt_sign_terms")
-            self.ev_side.record(self.side)
         eval_args = None
         if not self.fused_sign:
             eval_args = (p(self.bufs.packed), p(self.bufs.meta), self.bufs.capacity,
@@ -164,7 +151,25 @@ class TreePipeline:
             self.tabs.wait_event(self.ev_scan)
             with torch.cuda.stream(self.tabs):
                 _lib.check(L.dt_eval_prepare(*eval_args, _lib.stream_handle()), "dt_eval_prepare")
+                # the sign term's tile brackets need no prefix either
+                _lib.check(L.dt_sign_bracket(p(xs), self.n, p(ys_part), i1 - i0,
+                                             p(self.sign_ws), self.sign_ws_bytes,
+                                             _lib.stream_handle()), "dt_sign_bracket")
                 self.ev_tabs.record(self.tabs)
+        self.side.wait_event(self.ev_scan)
+        with torch.cuda.stream(self.side):
+            _lib.check(L.dt_prefix_scan(p(qs), p(self.prefix), self.n, p(self.scan_ws),
+                                        self.scan_ws_bytes, _lib.stream_handle()),
+                       "dt_prefix_scan")
+            if self.shard is not None:  # the full upward pass writes xq itself
+                pack_sources(xs, qs, self.xq)
+            if not self.fused_sign:
+                self.side.wait_event(self.ev_tabs)  # the brackets (third stream)
+                _lib.check(L.dt_sign_terms_bracketed(p(xs), p(self.prefix), self.n, p(ys_part),
+                                                     p(out_part), i1 - i0, p(self.sign_ws),
+                                                     self.sign_ws_bytes, _lib.stream_handle()),
+                           "dt_sign_terms_bracketed")
+            self.ev_side.record(self.side)
         if self.shard is None:  # moments + the traversal's (x, q) pairs (dt_moments_pack)
             launch_moments(self.bufs, xs, qs, self.order, self.moments, self.meval, xq=self.xq)
         else:  # this rank's subtrees + all-gather of the cut-level rows
