@@ -928,7 +928,6 @@ __global__ void __launch_bounds__(EVAL_THREADS, DT_EVAL_MINB) tree_eval_kernel(E
     const int64_t n_tasks = (a.i1 - a.i0 + 31) / 32;
     unsigned *const seg_ctr = reinterpret_cast<unsigned *>(a.counter);
     int seg = (int)(dt_smid() % DT_EVAL_SEGMENTS);
-    int seg_left = DT_EVAL_SEGMENTS;
 #endif
     while (true) {
         unsigned long long base = 0;
@@ -941,9 +940,31 @@ __global__ void __launch_bounds__(EVAL_THREADS, DT_EVAL_MINB) tree_eval_kernel(E
                 t = atomicAdd(seg_ctr + seg, 1u);
             t = __shfl_sync(DT_FULL, t, 0);
             if ((int64_t)t >= s1 - s0) {
-                if (--seg_left == 0)
+                // this segment is drained: read every segment's counter at
+                // once (lanes in parallel, plain L2 loads) and move to the
+                // first one after it that still has tasks, instead of probing
+                // the segments one atomic at a time (up to 147 round trips
+                // per warp at the end of a launch)
+                int next = -1;
+#pragma unroll 1
+                for (int r0 = 1; r0 < DT_EVAL_SEGMENTS && next < 0; r0 += 32) {
+                    const int off = r0 + lane;
+                    bool has = false;
+                    int sg = 0;
+                    if (off < DT_EVAL_SEGMENTS) {
+                        sg = seg + off;
+                        sg -= sg >= DT_EVAL_SEGMENTS ? DT_EVAL_SEGMENTS : 0;
+                        const int64_t size = n_tasks * (sg + 1) / DT_EVAL_SEGMENTS -
+                                             n_tasks * sg / DT_EVAL_SEGMENTS;
+                        has = (int64_t)__ldcg(seg_ctr + sg) < size;
+                    }
+                    const unsigned hb = __ballot_sync(DT_FULL, has);
+                    if (hb)
+                        next = __shfl_sync(DT_FULL, sg, __ffs(hb) - 1);
+                }
+                if (next < 0)
                     break;
-                seg = seg + 1 == DT_EVAL_SEGMENTS ? 0 : seg + 1;
+                seg = next;
                 continue;
             }
             base = (unsigned long long)(s0 + t) * 32ull;

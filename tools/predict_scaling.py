@@ -1,5 +1,6 @@
 """Predict the G-GPU step of bench.py from per-rank components measured on
-one GPU (configs[2]).  Per rank the step is
+one GPU (configs[2]).  The traversal of a slice is timed without its
+order-table build, which the pipeline runs on a third stream.  Per rank the step is
     scan + build + max(sharded upward pass + all-gather, pack + sign term of
     the slice) + traversal of the slice
 (pipeline.TreePipeline.step: the pack and the sign term run on a side stream
@@ -57,11 +58,38 @@ def timeit(fn, reps=5):
     return min(ts[1:])
 
 
+from paper_1710_05781_b200.tree import contour_tables
+
+cos_t, sin_t = contour_tables(ys.device)
+eval_ws = torch.empty(_lib.DT_EVAL_COUNTER_BYTES, dtype=torch.uint8, device="cuda")
+
+
+def traverse(i0, i1):
+    """The pipeline's traversal of one slice: the order tables are built on
+    a third stream beside the upward pass (dt_eval_prepare), so only the
+    traversal kernel (dt_tree_eval_device_prepared) is on the step's path."""
+    args = (p(tree.packed), p(tree.meta), tree.packed.numel() // 32, p(tree.meval),
+            tree.meval.shape[1], p(tree.xq), len(xs), w.r_d * w.r_d, float(cfg.theta),
+            int(cfg.p), 1, float(cfg.tolerance), tree.moment_order, p(cos_t), p(sin_t),
+            cos_t.numel(), p(ys), p(out), i0, i1, 0, p(eval_ws), eval_ws.numel(),
+            _lib.stream_handle())
+    ts = []
+    for _ in range(6):  # the prepare call also zeroes the slot's task counters
+        _lib.check(L.dt_eval_prepare(*args), "dt_eval_prepare")
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        _lib.check(L.dt_tree_eval_device_prepared(*args), "dt_tree_eval_device_prepared")
+        b.record()
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b))
+    return min(ts[1:])
+
+
 res = {"workload": "configs[2] (2^24 sources = targets)", "allgather_us_assumed": ALLGATHER_US}
 res["scan_ms"] = timeit(lambda: prefix_sum(qs))
 res["build_ms"] = timeit(lambda: bufs.launch(xs, 64))
 res["moments_full_ms"] = timeit(lambda: launch_moments(bufs, xs, qs, order, None, me))
-res["eval_full_ms"] = timeit(lambda: tree_phi_sum(tree, k, cfg, ys, out, accumulate=False))
+res["eval_full_ms"] = traverse(0, T)
 per_g = {}
 for G in (1, 2, 4, 8):
     mom, ev, side = 0.0, 0.0, 0.0
@@ -79,8 +107,7 @@ for G in (1, 2, 4, 8):
             mom = max(mom, timeit(go) + ALLGATHER_US * 1e-3)
         else:
             mom = res["moments_full_ms"]
-        ev = max(ev, timeit(lambda: tree_phi_sum(tree, k, cfg, ys, out, i0=i0, i1=i1,
-                                                 accumulate=False)))
+        ev = max(ev, traverse(i0, i1))
 
         def sidework():
             pack_sources(xs, qs, xq)
