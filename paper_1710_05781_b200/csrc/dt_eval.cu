@@ -924,7 +924,7 @@ __global__ void __launch_bounds__(EVAL_THREADS, DT_EVAL_MINB) tree_eval_kernel(E
     // Locality-aware scheduling: the 32-target tasks are split into
     // DT_EVAL_SEGMENTS contiguous segments; an SM's warps drain the segment
     // of their SM id first (neighbouring targets share nodes and moment rows
-    // in L1), then move on to the following segments.
+    // in L1), then move on to the next segment that still has tasks.
     const int64_t n_tasks = (a.i1 - a.i0 + 31) / 32;
     unsigned *const seg_ctr = reinterpret_cast<unsigned *>(a.counter);
     int seg = (int)(dt_smid() % DT_EVAL_SEGMENTS);
