@@ -485,12 +485,12 @@ PIPELINE_CHUNK = 1 << 21
 
 
 def _looks_sorted(host: torch.Tensor) -> bool:
-    """Cheap host-side guess (257 evenly spaced samples: each is a cache miss
+    """Cheap host-side guess (65 evenly spaced samples: each is a cache miss
     in a large pinned array, and the guess sits before the first launch) that
     the targets are ascending; unsorted targets take the sorting path.
     Results never depend on it: the traversal is exact in any order."""
     n = host.numel()
-    s = host.numpy()[np.linspace(0, n - 1, min(n, 257)).astype(np.int64)]
+    s = host.numpy()[np.linspace(0, n - 1, min(n, 65)).astype(np.int64)]
     return bool((s[1:] >= s[:-1]).all())
 
 
