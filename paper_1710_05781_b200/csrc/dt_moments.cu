@@ -192,6 +192,8 @@ __device__ void m2m_node(const MomArgs &a, int64_t node, int64_t left, int64_t r
 
 __global__ void moments_prep_kernel(MomArgs a)
 {
+    if (__ldg(a.meta + DT_META_OVERFLOW))
+        return;  // the build ran out of node capacity: the caller rebuilds
     const int64_t n = __ldg(a.meta + DT_META_NODES);
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
@@ -400,6 +402,8 @@ __global__ void __launch_bounds__(256, DT_UP_MINB) upward_kernel(MomArgs a)
         atomicMin(g_uptrace, t_);
     }
 #endif
+    if (__ldg(a.meta + DT_META_OVERFLOW))
+        return;  // the build ran out of node capacity: the caller rebuilds
     const int64_t n = __ldg(a.meta + DT_META_NODES);
     int64_t cut_begin = 0, lo = 0, hi = 0;
     if (a.plan) {

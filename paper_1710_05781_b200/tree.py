@@ -302,13 +302,23 @@ def _build(system: ChargeSystem, config: EvalConfig, upward) -> Tree:
     fused = upward is None and order + 1 <= 32
     xq = torch.empty(2 * n, dtype=torch.float64, device=dev)
     cap = initial_node_capacity(n, config.leaf_capacity)
+    meta_h = torch.empty(8, dtype=torch.int64, pin_memory=True)
     while True:
         bufs = TreeBuffers(n, cap, dev)
         meval = (torch.empty((cap, eval_stride(order)), dtype=torch.float64, device=dev)
                  if fused else None)
         bufs.launch(system.xs, config.leaf_capacity,
                     p2m=(system.qs, order, meval, xq) if fused else None)
-        meta = bufs.meta[:8].cpu().tolist()
+        # the host needs the node count; the fused path enqueues the moments
+        # first (they read the count on the device and do nothing if the build
+        # overflowed), so the GPU does not idle while the host reads it
+        meta_h.copy_(bufs.meta[:8], non_blocking=True)
+        counted = torch.cuda.Event()
+        counted.record()
+        if fused:  # moments and the traversal's (x, q) pairs in one pass
+            launch_moments(bufs, system.xs, system.qs, order, None, meval, xq=xq)
+        counted.synchronize()
+        meta = meta_h.tolist()
         if not meta[_lib.DT_META_OVERFLOW]:
             break
         cap *= 4
@@ -317,9 +327,9 @@ def _build(system: ChargeSystem, config: EvalConfig, upward) -> Tree:
                if order + 1 > 32 else None)
     if meval is None:
         meval = torch.empty((n_nodes, eval_stride(order)), dtype=torch.float64, device=dev)
-    if upward is None:  # moments and the traversal's (x, q) pairs in one pass
+    if upward is None and not fused:  # higher orders: both layouts, then the pairs
         launch_moments(bufs, system.xs, system.qs, order, moments, meval, xq=xq)
-    else:
+    elif upward is not None:
         upward(bufs, order, moments, meval)
         pack_sources(system.xs, system.qs, xq)
     ev1.record()
