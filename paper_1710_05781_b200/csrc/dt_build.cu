@@ -1048,13 +1048,19 @@ static int build_launch(const double *xs, int64_t n, int64_t leaf_capacity, int6
     // the irregular flag and the chunk counter
     DT_CUDA_TRY(cudaMemsetAsync(a.irregular, 0, 16, (cudaStream_t)stream));
 
-    int dev = 0, per_sm = 0;
+    // the attribute and the occupancy are per device and fixed: queried once
+    // (they sit in front of every launch otherwise)
+    static int cached_dev = -1, per_sm = 0;
+    int dev = 0;
     DT_CUDA_TRY(cudaGetDevice(&dev));
     const size_t smem = (size_t)BUILD_SAMPLES * sizeof(double) + 2 * SMALL_LEVEL * sizeof(Front);
-    DT_CUDA_TRY(cudaFuncSetAttribute((const void *)build_kernel,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    DT_CUDA_TRY(
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, build_kernel, BUILD_THREADS, smem));
+    if (dev != cached_dev) {
+        DT_CUDA_TRY(cudaFuncSetAttribute((const void *)build_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        DT_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, build_kernel,
+                                                                  BUILD_THREADS, smem));
+        cached_dev = dev;
+    }
     if (per_sm < 1)
         return dt_set_error(DT_ERR_CUDA, "build kernel cannot be resident");
 #ifndef DT_BUILD_PER_SM

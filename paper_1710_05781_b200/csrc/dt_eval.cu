@@ -1269,7 +1269,28 @@ int launch_fused(EvalArgs &a, bool adaptive, bool stats, cudaStream_t s, int64_t
                                        : pick_kernel<true, false>(wide))
                               : (stats ? pick_kernel<false, true>(wide)
                                        : pick_kernel<false, false>(wide));
-    DT_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, EVAL_THREADS, 0));
+    {
+        // occupancy per (kernel, device), queried once: it sits in front of
+        // every launch otherwise
+        static const void *c_fn[8];
+        static int c_dev[8], c_per_sm[8], c_n = 0;
+        int dev = 0;
+        DT_CUDA_TRY(cudaGetDevice(&dev));
+        int k = 0;
+        while (k < c_n && !(c_fn[k] == fn && c_dev[k] == dev))
+            ++k;
+        if (k == c_n) {
+            DT_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, EVAL_THREADS, 0));
+            if (c_n < 8) {
+                c_fn[c_n] = fn;
+                c_dev[c_n] = dev;
+                c_per_sm[c_n] = per_sm;
+                ++c_n;
+            }
+        } else {
+            per_sm = c_per_sm[k];
+        }
+    }
     if (per_sm < 1)
         per_sm = 1;
     int64_t warps_needed = (a.i1 - a.i0 + 31) / 32;
