@@ -143,3 +143,33 @@ def test_sign_terms_tile_aligned_sorted_runs(dt):
     assert np.max(np.abs(f - fw)) <= 1e-12 * np.abs(q).sum()
     d = dt.evaluate_direct(s, k, t).values
     assert np.max(np.abs(d - O.evaluate_direct(x, q, 0.01, t))) <= 1e-13 * np.abs(q).sum()
+
+
+def test_capacity_overflow_rebuild(dt):
+    """Clusters of leaf_capacity + 1 coincident sources split down to the
+    depth limit, so the tree needs far more nodes than the initial capacity
+    estimate: build() detects the overflow after the moments were already
+    enqueued (they return at once on an overflowed tree), rebuilds with a
+    larger capacity, and the result matches the oracle's structure and the
+    direct sum."""
+    from oracle import oracle as O
+    from paper_1710_05781_b200.tree import initial_node_capacity
+
+    rng = np.random.default_rng(11)
+    m, lc = 100, 64
+    centers = np.sort(rng.uniform(-1, 1, m))
+    x = np.repeat(centers, lc + 1)
+    q = rng.normal(size=x.size)
+    s = dt.from_sorted(x, q)
+    k = dt.DiscKernel(0.01)
+    cfg = dt.EvalConfig(p=10, leaf_capacity=lc)
+    tree = dt.build(s, k, cfg)
+    assert len(tree) > initial_node_capacity(x.size, lc)  # the first build overflowed
+    ref = O.build_structure(x, lc)
+    for f in O.NODE_FIELDS:
+        np.testing.assert_array_equal(getattr(tree, f).cpu().numpy(), getattr(ref, f), err_msg=f)
+    assert np.isfinite(tree.meval.cpu().numpy()).all()
+    t = np.sort(rng.uniform(-1.1, 1.1, 2000))
+    got = dt.evaluate_all(tree, k, cfg, s, t).values
+    want = dt.evaluate_direct(s, k, t).values
+    assert np.max(np.abs(got - want)) <= 1e-8 * np.abs(q).sum()
