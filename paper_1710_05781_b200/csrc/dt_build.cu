@@ -49,8 +49,11 @@ struct BuildArgs {
     int32_t *scratch_off;    // [capacity] local exclusive offset within the block chunk
     int32_t *scratch_split;  // [capacity] split index found in phase A
     int64_t *block_total;    // [gridDim]
-    int64_t *dy_split;       // [DYADIC] global lower_bound of each top dyadic midpoint
-    double *dy_mid;          // [DYADIC] that midpoint
+    // [2^DYADIC_LEVELS + 1] the dyadic points of the root interval in
+    // position order, point j = (value, lower_bound in xs): the bounds of node
+    // (L, k) are points k 2^(DYADIC_LEVELS - L) and (k + 1) 2^(DYADIC_LEVELS - L),
+    // its midpoint (2k + 1) 2^(DYADIC_LEVELS - L - 1)
+    double2 *dy_point;
     int k_top;               // levels 0..k_top built in one pass (0: level by level)
     unsigned *irregular;     // set if some top dyadic interval has mid not strictly inside
     // optional (dt_build_tree_p2m): while block 0 runs a sparse level run,
@@ -131,13 +134,20 @@ __device__ void build_p2m_until(const BuildArgs &a, unsigned long long limit,
 constexpr int DYADIC_LEVELS = DT_DYADIC_LEVELS;  // levels 0..DYADIC_LEVELS-1
 constexpr int DYADIC = (1 << DYADIC_LEVELS) - 1;
 
+// point j of the dyadic table: value and lower bound
+__device__ __forceinline__ double2 dy_load(const BuildArgs &a, int64_t j)
+{
+    return __ldcg(a.dy_point + j);
+}
+__device__ __forceinline__ int64_t dy_lb(double2 p) { return __double_as_longlong(p.y); }
+
 __device__ __forceinline__ double mid_of(double lo, double hi)
 {
     return __dmul_rn(0.5, __dadd_rn(lo, hi));
 }
 
 __device__ void write_node(const BuildArgs &a, int64_t c, double lo, double hi, int64_t lev,
-                           int64_t s, int64_t e)
+                           int64_t s, int64_t e, int64_t l_slot = -1, int64_t r_slot = -1)
 {
     double ctr = __dmul_rn(0.5, __dadd_rn(lo, hi));
     double hw = __dmul_rn(0.5, __dsub_rn(hi, lo));
@@ -148,14 +158,13 @@ __device__ void write_node(const BuildArgs &a, int64_t c, double lo, double hi, 
     a.level[c] = lev;
     a.start[c] = s;
     a.end[c] = e;
-    a.left[c] = -1;
-    a.right[c] = -1;
+    a.left[c] = l_slot;
+    a.right[c] = r_slot;
     if (a.packed) {
         dt_node nd;
         nd.center = ctr;
         nd.half = hw;
-        nd.first = -1;
-        nd.second = -1;
+        dt_node_children(nd, l_slot, r_slot);
         nd.start = (int32_t)s;
         nd.end = (int32_t)e;
         a.packed[c] = nd;
@@ -177,7 +186,8 @@ __device__ __forceinline__ void root_interval(const BuildArgs &a, double *lo, do
     *hi = __dadd_rn(xl, pad);
 }
 
-// Phase 0: dy_mid / dy_split for dyadic interval idx (level L = floor(log2(idx + 1)),
+// Phase 0: the dyadic point table (dy_point) for the midpoint of every
+// dyadic interval idx of levels < DYADIC_LEVELS (level L = floor(log2(idx + 1)),
 // position k = idx + 1 - 2^L), following the same midpoint arithmetic as the build.
 // The lower_bounds are found in two steps: every stride-th source is copied
 // to a sample array (<= 2^18 values, L2-resident), a grid barrier, then each
@@ -223,7 +233,7 @@ __device__ void dyadic_splits(const BuildArgs &a, cg::grid_group &grid)
                 hi = m;
         }
         const double mid = mid_of(lo, hi);
-        a.dy_mid[idx] = mid;
+        const int64_t j = (int64_t)(2 * k + 1) << (DYADIC_LEVELS - L - 1);
         if (!(lo < mid && mid < hi))  // degenerate interval: no one-pass top
             atomicOr(a.irregular, 1u);
         // first sample >= mid
@@ -258,7 +268,11 @@ __device__ void dyadic_splits(const BuildArgs &a, cg::grid_group &grid)
                     s1 = g2;
             }
         }
-        a.dy_split[idx] = dt_lower_bound(a.xs, s0, s1, mid);
+        a.dy_point[j] = make_double2(mid, __longlong_as_double(dt_lower_bound(a.xs, s0, s1, mid)));
+    }
+    if (tid == 0) {
+        a.dy_point[0] = make_double2(lo0, __longlong_as_double(0));
+        a.dy_point[(int64_t)1 << DYADIC_LEVELS] = make_double2(hi0, __longlong_as_double(a.n));
     }
     DY_STAMP(75)
 }
@@ -350,9 +364,9 @@ __device__ __forceinline__ int64_t split_of(const BuildArgs &a, int64_t lev, dou
         const double pos = (lo - lo0) / (hi0 - lo0) * (double)(1 << lev);
         const int k = (int)rint(pos);
         if (k >= 0 && k < (1 << lev)) {
-            const int idx = (1 << lev) - 1 + k;
-            if (__ldcg(a.dy_mid + idx) == mid) {
-                const int64_t g = __ldcg(a.dy_split + idx);
+            const double2 pt = dy_load(a, (int64_t)(2 * k + 1) << (DYADIC_LEVELS - lev - 1));
+            if (pt.x == mid) {
+                const int64_t g = dy_lb(pt);
                 split = g < s ? s : (g > e ? e : g);
             }
         }
@@ -510,6 +524,17 @@ __device__ int64_t level_in_block(const BuildArgs &a, const Front *cur, int F, i
     return next - g1;
 }
 
+#ifdef DT_BUILD_TRACE
+#define BUILD_STAMP(slot)                                                                    \
+    if (blockIdx.x == 0 && threadIdx.x == 0) {                                               \
+        unsigned long long t_;                                                               \
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                              \
+        a.block_total[2048 + (slot)] = (int64_t)t_;                                          \
+    }
+#else
+#define BUILD_STAMP(slot)
+#endif
+
 // ---- the top levels in one pass
 //
 // Every node of level L <= k_top is a dyadic interval [k/2^L, (k+1)/2^L) of
@@ -526,26 +551,13 @@ __device__ int64_t level_in_block(const BuildArgs &a, const Front *cur, int F, i
 // Requires every top interval to be regular (lo < mid < hi, else the
 // reference's one-child cases apply and the build goes level by level).
 
-// Bound k of level L (0 <= k <= 2^L): its value and lower_bound in xs.
-__device__ __forceinline__ void top_point(const BuildArgs &a, int L, int64_t k, double lo0,
-                                          double hi0, double *v, int64_t *lb)
-{
-    if (k == 0) {
-        *v = lo0;
-        *lb = 0;
-        return;
-    }
-    if (k == ((int64_t)1 << L)) {
-        *v = hi0;
-        *lb = a.n;
-        return;
-    }
-    const int z = __ffsll(k) - 1;               // k = (2 kp + 1) 2^z
-    const int Lp = L - z - 1;                   // the midpoint of node (Lp, kp)
-    const int64_t idx = ((int64_t)1 << Lp) - 1 + (k >> (z + 1));
-    *v = __ldcg(a.dy_mid + idx);
-    *lb = __ldcg(a.dy_split + idx);
-}
+#ifndef DT_TOP_R1
+#define DT_TOP_R1 4
+#endif
+#ifndef DT_TOP_R2
+#define DT_TOP_R2 2
+#endif
+constexpr int TOP_R1 = DT_TOP_R1, TOP_R2 = DT_TOP_R2;  // rows per group in the top's passes
 
 struct TopSlot {
     int L;
@@ -555,19 +567,25 @@ struct TopSlot {
     bool node, splits;
 };
 
-__device__ __forceinline__ TopSlot top_slot(const BuildArgs &a, int64_t f, double lo0, double hi0)
+// Slot f of the top (level L, position k): bounds, source range, and whether
+// it is a node / splits.  Three point loads: its two bounds and the parent's
+// other bound (the parent shares one bound with the slot).
+__device__ __forceinline__ TopSlot top_slot(const BuildArgs &a, int64_t f)
 {
     TopSlot t;
     t.L = 63 - __clzll(f + 1);
     t.k = f + 1 - ((int64_t)1 << t.L);
-    top_point(a, t.L, t.k, lo0, hi0, &t.lo, &t.s);
-    top_point(a, t.L, t.k + 1, lo0, hi0, &t.hi, &t.e);
+    const int sh = DYADIC_LEVELS - t.L;
+    const double2 p0 = dy_load(a, t.k << sh), p1 = dy_load(a, (t.k + 1) << sh);
+    const int64_t kx = (t.k & 1) ? t.k - 1 : t.k + 2;  // the parent's other bound
+    const int64_t px = t.L > 0 ? dy_lb(dy_load(a, kx << sh)) : 0;
+    t.lo = p0.x;
+    t.hi = p1.x;
+    t.s = dy_lb(p0);
+    t.e = dy_lb(p1);
     bool parent_splits = true;
     if (t.L > 0) {
-        double v;
-        int64_t ps, pe;
-        top_point(a, t.L - 1, t.k >> 1, lo0, hi0, &v, &ps);
-        top_point(a, t.L - 1, (t.k >> 1) + 1, lo0, hi0, &v, &pe);
+        const int64_t ps = (t.k & 1) ? px : t.s, pe = (t.k & 1) ? t.e : px;
         parent_splits = pe - ps > a.leaf_capacity && t.L - 1 < a.max_depth;
     }
     t.node = t.e > t.s && parent_splits;
@@ -583,8 +601,6 @@ __device__ int64_t build_top(const BuildArgs &a, cg::grid_group &grid, int *warp
     const int K = a.k_top;
     if (K <= 0 || *(volatile unsigned *)a.irregular)
         return 0;
-    double lo0, hi0;
-    root_interval(a, &lo0, &hi0);
     const int G = gridDim.x;
     const int64_t S = ((int64_t)2 << K) - 1;  // slots of levels 0..K
     const int64_t chunk = (S + G - 1) / G;
@@ -595,23 +611,36 @@ __device__ int64_t build_top(const BuildArgs &a, cg::grid_group &grid, int *warp
     // share one scan (16 bits each: a block chunk has < 2^15 slots)
     const bool listing = chunk < (1 << 15) && G <= 1024;
     // pass 1: node flags, block-local exclusive offsets, leaves above level K
+    // (TOP_R1 rows of blockDim.x slots at a time: their point loads are all
+    // in flight together, then one block scan per row)
     int64_t run = 0, run2 = 0, leaves = 0;
-    for (int64_t t0 = b0; t0 < b1; t0 += blockDim.x) {
-        const int64_t f = t0 + threadIdx.x;
-        int flag = 0;
-        if (f < b1) {
-            const TopSlot t = top_slot(a, f, lo0, hi0);
-            flag = t.node | ((listing && t.splits && t.L == K) ? 1 << 16 : 0);
-            leaves += t.node && !t.splits && t.L < K;
+    for (int64_t g0 = b0; g0 < b1; g0 += (int64_t)TOP_R1 * blockDim.x) {
+        int flag[TOP_R1];
+#pragma unroll
+        for (int r = 0; r < TOP_R1; ++r) {
+            const int64_t f = g0 + (int64_t)r * blockDim.x + threadIdx.x;
+            flag[r] = 0;
+            if (f < b1) {
+                const TopSlot t = top_slot(a, f);
+                flag[r] = t.node | ((listing && t.splits && t.L == K) ? 1 << 16 : 0);
+                leaves += t.node && !t.splits && t.L < K;
+            }
         }
-        int excl;
-        const int tot = block_excl_scan(flag, &excl, warp_sums);
-        if (f < b1) {
-            a.scratch_off[f] = (int32_t)(run + (excl & 0xffff));
-            a.scratch_split[f] = (int32_t)(run2 + (excl >> 16));
+#pragma unroll
+        for (int r = 0; r < TOP_R1; ++r) {
+            const int64_t t0 = g0 + (int64_t)r * blockDim.x;
+            if (t0 >= b1)
+                break;  // block-uniform
+            const int64_t f = t0 + threadIdx.x;
+            int excl;
+            const int tot = block_excl_scan(flag[r], &excl, warp_sums);
+            if (f < b1) {
+                a.scratch_off[f] = (int32_t)(run + (excl & 0xffff));
+                a.scratch_split[f] = (int32_t)(run2 + (excl >> 16));
+            }
+            run += tot & 0xffff;
+            run2 += tot >> 16;
         }
-        run += tot & 0xffff;
-        run2 += tot >> 16;
     }
     if (threadIdx.x == 0) {
         a.block_total[blockIdx.x] = run;
@@ -625,53 +654,84 @@ __device__ int64_t build_top(const BuildArgs &a, cg::grid_group &grid, int *warp
         if (dt_lane() == 0 && lv)
             atomicAdd((unsigned long long *)&a.meta[DT_META_LEAVES], (unsigned long long)lv);
     }
+    BUILD_STAMP(76)
     grid.sync();
-    // every block's base, fixed order (G <= blockDim.x)
-    if (threadIdx.x == 0) {
-        int64_t acc = 0;
+    BUILD_STAMP(77)
+    // every block's base: exclusive scans over the block totals (integer
+    // sums, so any order gives the same bases)
+    if (G <= (int)blockDim.x) {
+        const int b = threadIdx.x;
+        const int v1 = b < G ? (int)__ldcg(a.block_total + b) : 0;
+        const int v2 = listing && b < G ? (int)__ldcg(a.block_total + 1024 + b) : 0;
+        int e1, e2;
+        const int t1 = block_excl_scan(v1, &e1, warp_sums);
+        const int t2 = block_excl_scan(v2, &e2, warp_sums);
+        if (b < G) {
+            bases_s[b] = e1;
+            bases2_s[b] = e2;
+        }
+        if (b == 0) {
+            bases_s[G] = t1;
+            bases2_s[G] = t2;
+        }
+    } else if (threadIdx.x == 0) {
+        int64_t acc = 0, acc2 = 0;
         for (int b = 0; b < G; ++b) {
             bases_s[b] = acc;
-            acc += ((volatile int64_t *)a.block_total)[b];
+            bases2_s[b] = acc2;
+            acc += __ldcg(a.block_total + b);
+            acc2 += listing ? __ldcg(a.block_total + 1024 + b) : 0;
         }
         bases_s[G] = acc;
-    } else if (threadIdx.x == 32 && listing) {
-        int64_t acc = 0;
-        for (int b = 0; b < G; ++b) {
-            bases2_s[b] = acc;
-            acc += ((volatile int64_t *)a.block_total)[1024 + b];
-        }
-        bases2_s[G] = acc;
+        bases2_s[G] = acc2;
     }
     __syncthreads();
+    BUILD_STAMP(78)
     const int64_t total = bases_s[G];
     if (total > a.capacity) {  // every block sees the same total
         if (blockIdx.x == 0 && threadIdx.x == 0)
             a.meta[DT_META_OVERFLOW] = 1;
         return -1;
     }
+    const unsigned uchunk = (unsigned)chunk;  // S < 2^31: 32-bit divisions
     auto index_of = [&](int64_t f) -> int64_t {  // exclusive node count before slot f
-        return f >= S ? total : bases_s[f / chunk] + __ldcg(a.scratch_off + f);
+        return f >= S ? total : bases_s[(unsigned)f / uchunk] + __ldcg(a.scratch_off + f);
     };
-    // pass 2: write the nodes and their child slots
-    for (int64_t f = b0 + threadIdx.x; f < b1; f += blockDim.x) {
-        const TopSlot t = top_slot(a, f, lo0, hi0);
-        if (!t.node)
-            continue;
-        const int64_t c = index_of(f);
-        write_node(a, c, t.lo, t.hi, t.L, t.s, t.e);
-        if (listing && t.splits && t.L == K)
-            a.deep_list[bases2_s[f / chunk] + __ldcg(a.scratch_split + f)] =
-                Front{t.lo, t.hi, c, (int32_t)t.s, (int32_t)t.e};
-        if (t.splits && t.L < K) {
-            const int64_t split = __ldcg(a.dy_split + f);  // this slot's own midpoint
-            const int64_t fl = 2 * f + 1;                  // slot (L + 1, 2k)
-            const int64_t l_slot = split > t.s ? index_of(fl) : -1;
-            const int64_t r_slot = t.e > split ? index_of(fl + 1) : -1;
-            a.left[c] = l_slot;
-            a.right[c] = r_slot;
-            if (a.packed) {
-                dt_node_children(a.packed[c], l_slot, r_slot);
+    // pass 2: write the nodes with their child links.  Every global load of
+    // a slot is issued before any of them is used: one L2 round trip per slot
+    // instead of a chain of three
+    for (int64_t g0 = b0 + threadIdx.x; g0 < b1; g0 += (int64_t)TOP_R2 * blockDim.x) {
+#pragma unroll
+        for (int r = 0; r < TOP_R2; ++r) {
+            const int64_t f = g0 + (int64_t)r * blockDim.x;
+            if (f >= b1)
+                break;
+            const int64_t fl = 2 * f + 1;  // slot (L + 1, 2k)
+            const int32_t off = __ldcg(a.scratch_off + f);
+            const int32_t offl = fl < S ? __ldcg(a.scratch_off + fl) : 0;
+            const int32_t offr = fl + 1 < S ? __ldcg(a.scratch_off + fl + 1) : 0;
+            const int32_t off2 = listing ? __ldcg(a.scratch_split + f) : 0;
+            const TopSlot t = top_slot(a, f);
+            // this slot's own midpoint (levels < K only)
+            const int64_t split =
+                t.L < K ? dy_lb(dy_load(a, (2 * t.k + 1) << (DYADIC_LEVELS - t.L - 1))) : 0;
+            if (!t.node)
+                continue;
+            const int64_t c = bases_s[blockIdx.x] + off;
+            int64_t l_slot = -1, r_slot = -1;
+            if (t.splits && t.L < K) {
+                if (split > t.s)
+                    l_slot = fl >= S ? total : bases_s[(unsigned)fl / uchunk] + offl;
+                if (t.e > split)
+                    r_slot = fl + 1 >= S ? total : bases_s[(unsigned)(fl + 1) / uchunk] + offr;
             }
+#ifdef DT_TOP_NOWRITE
+            if (c == -12345)
+#endif
+            write_node(a, c, t.lo, t.hi, t.L, t.s, t.e, l_slot, r_slot);
+            if (listing && t.splits && t.L == K)
+                a.deep_list[bases2_s[blockIdx.x] + off2] =
+                    Front{t.lo, t.hi, c, (int32_t)t.s, (int32_t)t.e};
         }
     }
     if (blockIdx.x == 0 && threadIdx.x <= K + 1) {
@@ -687,6 +747,7 @@ __device__ int64_t build_top(const BuildArgs &a, cg::grid_group &grid, int *warp
                 depth = L;
         a.meta[DT_META_DEPTH] = depth;
     }
+    BUILD_STAMP(79)
     grid.sync();
     return K;
 }
@@ -726,16 +787,6 @@ __global__ void __launch_bounds__(BUILD_THREADS) build_kernel(BuildArgs a)
     unsigned long long p2m_limit = 0;  // chunks of the first sparse run (0: none yet)
     if (blockIdx.x == 0 && threadIdx.x == 0)
         *small_flag = 0;
-#endif
-#ifdef DT_BUILD_TRACE
-#define BUILD_STAMP(slot)                                                                    \
-    if (blockIdx.x == 0 && threadIdx.x == 0) {                                               \
-        unsigned long long t_;                                                               \
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                              \
-        a.block_total[2048 + (slot)] = (int64_t)t_;                                          \
-    }
-#else
-#define BUILD_STAMP(slot)
 #endif
     BUILD_STAMP(70)
     dyadic_splits(a, grid);
@@ -975,7 +1026,7 @@ extern "C" size_t dt_build_workspace(int64_t n, int64_t node_capacity)
 {
     (void)n;
     return (size_t)node_capacity * 2 * sizeof(int32_t) + 4096 * sizeof(int64_t) + 16 +
-           (size_t)DYADIC * (sizeof(int64_t) + sizeof(double)) + 32 + 64 +
+           (((size_t)1 << DYADIC_LEVELS) + 2) * sizeof(double2) + 32 + 64 +
            ((size_t)1 << DYADIC_LEVELS) * sizeof(Front) + (size_t)DY_SAMPLES * sizeof(double);
 }
 
@@ -1020,9 +1071,8 @@ static int build_launch(const double *xs, int64_t n, int64_t leaf_capacity, int6
     a.block_total = (int64_t *)((char *)workspace + (size_t)node_capacity * 2 * sizeof(int32_t));
     // 8-byte align block_total
     a.block_total = (int64_t *)(((uintptr_t)a.block_total + 7) & ~(uintptr_t)7);
-    a.dy_split = a.block_total + 4096;
-    a.dy_mid = (double *)(a.dy_split + DYADIC);
-    a.irregular = (unsigned *)(a.dy_mid + DYADIC);
+    a.dy_point = (double2 *)(((uintptr_t)(a.block_total + 4096) + 15) & ~(uintptr_t)15);
+    a.irregular = (unsigned *)(a.dy_point + ((size_t)1 << DYADIC_LEVELS) + 1);
     // one-pass top: levels 0..k_top need 2^(k_top+1) - 1 scratch slots and
     // the dyadic midpoints of levels < k_top
     a.k_top = 0;

@@ -26,6 +26,11 @@ dy = bt[2048 + 73: 2048 + 76]
 if dy.min() > 0:
     print("  sample copy %.1f us, sample barrier %.1f us, searches %.1f us, final barrier %.1f us" % (
         (dy[0] - ph[0]) / 1e3, (dy[1] - dy[0]) / 1e3, (dy[2] - dy[1]) / 1e3, (ph[1] - dy[2]) / 1e3))
+tp = bt[2048 + 76: 2048 + 80]
+if tp.min() > 0:
+    print("  top: pass 1 %.1f us, barrier %.1f us, bases %.1f us, pass 2 %.1f us, barrier %.1f us" % (
+        (tp[0] - ph[1]) / 1e3, (tp[1] - tp[0]) / 1e3, (tp[2] - tp[1]) / 1e3, (tp[3] - tp[2]) / 1e3,
+        (ph[2] - tp[3]) / 1e3))
 lv = bufs.meta[8: 8 + depth + 2].cpu().numpy()
 print("per-level us (level: nodes us):")
 for l in range(depth + 1):
