@@ -32,6 +32,9 @@ constexpr int BUILD_THREADS = DT_BUILD_THREADS;
 #define DT_BUILD_SMALL (2 * BUILD_THREADS)
 #endif
 constexpr int SMALL_LEVEL = DT_BUILD_SMALL;
+#ifndef DT_BUILD_STAGE
+#define DT_BUILD_STAGE 1  // block-0 runs write staged 32-byte records (expand_stage)
+#endif
 #ifndef DT_BUILD_FLAGWAIT
 #define DT_BUILD_FLAGWAIT 1
 #endif  // nodes handled by block 0 alone
@@ -75,6 +78,20 @@ struct Front {
     int64_t node;
     int32_t s, e;
 };
+
+// A node created by a block-0 run, staged in the workspace (32 bytes instead
+// of the 104 bytes of node arrays and packed record): one SM's store
+// bandwidth bounds a run level, so block 0 writes only these, and after the
+// run every block expands them into the node arrays (expand_stage).
+struct StageRec {
+    double lo, hi;
+    int32_t s, e, l, r;  // source range, child links (-1: none)
+};
+struct Stage {
+    StageRec *rec;
+    int64_t base, cap;  // rec[i] is node base + i, for i < cap
+};
+
 
 // One warp forms leaves of 32-node chunks below `upto` (final nodes: the
 // levels before block 0's current run), claimed with one atomicAdd each,
@@ -450,13 +467,39 @@ __device__ int block_excl_scan(int v, int *excl, int *warp_sums)
     return total;
 }
 
+__device__ __forceinline__ void stage_node(const Stage &st, int64_t c, double lo, double hi,
+                                           int64_t s, int64_t e)
+{
+    StageRec *r = st.rec + (c - st.base);
+    *reinterpret_cast<double2 *>(r) = make_double2(lo, hi);
+    *reinterpret_cast<int4 *>(&r->s) = make_int4((int)s, (int)e, -1, -1);
+}
+
+// All blocks: the staged nodes [st.base, min(n_nodes, st.base + st.cap))
+// into the node arrays; node levels from the level offsets in meta (levels
+// lev0 + 1 .. of the run).
+__device__ void expand_stage(const BuildArgs &a, const Stage &st, int64_t n_nodes, int64_t lev0)
+{
+    const int64_t n = min(n_nodes - st.base, st.cap);
+    const int64_t nth = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += nth) {
+        const int64_t node = st.base + i;
+        int64_t l = lev0 + 1;
+        while (node >= ((volatile int64_t *)a.meta)[DT_META_LEVEL0 + l + 1])
+            ++l;
+        const double2 lh = __ldcg(reinterpret_cast<const double2 *>(st.rec + i));
+        const int4 se = __ldcg(reinterpret_cast<const int4 *>(&st.rec[i].s));
+        write_node(a, node, lh.x, lh.y, l, se.x, se.y, se.z, se.w);
+    }
+}
+
 // One level of a block-0 run: the frontier `cur` (F nodes of level lev) is
 // in shared memory; the children are written to the node arrays at BFS
 // index g1 + rank and, while they fit, to the next frontier `nxt`.
 // Returns the number of children written (or -1 on capacity overflow).
 __device__ int64_t level_in_block(const BuildArgs &a, const Front *cur, int F, int64_t g1,
                                   int64_t lev, int *warp_sums, int64_t *leaves,
-                                  const SplitSamples *sm, Front *nxt)
+                                  const SplitSamples *sm, Front *nxt, const Stage &st)
 {
     int64_t next = g1;
     int64_t leaf_acc = 0;
@@ -492,18 +535,20 @@ __device__ int64_t level_in_block(const BuildArgs &a, const Front *cur, int F, i
             int64_t c = next + excl;
             int64_t l_slot = -1, r_slot = -1;
             if (split > f.s) {  // (lo, mid): child_hi == mid -> left
-#ifndef DT_BUILD_NOWRITE
-                write_node(a, c, f.lo, mid, lev + 1, f.s, split);
-#endif
+                if (c - st.base < st.cap)
+                    stage_node(st, c, f.lo, mid, f.s, split);
+                else
+                    write_node(a, c, f.lo, mid, lev + 1, f.s, split);
                 if (c - g1 < SMALL_LEVEL)
                     nxt[c - g1] = Front{f.lo, mid, c, f.s, (int32_t)split};
                 l_slot = c;
                 ++c;
             }
             if (f.e > split) {  // (mid, hi): left iff hi == mid (tree.py:205-208)
-#ifndef DT_BUILD_NOWRITE
-                write_node(a, c, mid, f.hi, lev + 1, split, f.e);
-#endif
+                if (c - st.base < st.cap)
+                    stage_node(st, c, mid, f.hi, split, f.e);
+                else
+                    write_node(a, c, mid, f.hi, lev + 1, split, f.e);
                 if (c - g1 < SMALL_LEVEL)
                     nxt[c - g1] = Front{mid, f.hi, c, (int32_t)split, f.e};
                 if (f.hi == mid)
@@ -511,10 +556,15 @@ __device__ int64_t level_in_block(const BuildArgs &a, const Front *cur, int F, i
                 else
                     r_slot = c;
             }
-            a.left[f.node] = l_slot;
-            a.right[f.node] = r_slot;
-            if (a.packed)
-                dt_node_children(a.packed[f.node], l_slot, r_slot);
+            if (f.node >= st.base && f.node - st.base < st.cap) {
+                *reinterpret_cast<int2 *>(&st.rec[f.node - st.base].l) =
+                    make_int2((int)l_slot, (int)r_slot);
+            } else {
+                a.left[f.node] = l_slot;
+                a.right[f.node] = r_slot;
+                if (a.packed)
+                    dt_node_children(a.packed[f.node], l_slot, r_slot);
+            }
         }
         next += tot;
     }
@@ -815,7 +865,14 @@ __global__ void __launch_bounds__(BUILD_THREADS) build_kernel(BuildArgs a)
         const bool listed = n_listed >= 0 && n_listed <= SMALL_LEVEL;
         if (F <= SMALL_LEVEL || listed) {
             // block 0 runs consecutive small levels with the frontier in
-            // shared memory; the others wait (and form leaves, below)
+            // shared memory; the others wait (and form leaves, below).  The
+            // run's nodes are staged in the scratch slots (free until the
+            // next big level) and expanded by every block after the run.
+            const int64_t lev0_of_run = lev;
+            Stage st;
+            st.rec = reinterpret_cast<StageRec *>(a.scratch_off);
+            st.base = f1;
+            st.cap = DT_BUILD_STAGE ? a.capacity * 2 * (int64_t)sizeof(int32_t) / (int64_t)sizeof(StageRec) : 0;
             if (blockIdx.x == 0) {
                 int64_t leaves = 0;
                 int64_t l = lev, g1 = f1;
@@ -862,7 +919,7 @@ __global__ void __launch_bounds__(BUILD_THREADS) build_kernel(BuildArgs a)
                     }
 #endif
                     const int64_t made = level_in_block(a, cur, Fl, g1, l, warp_sums, &leaves,
-                                                        lev >= DYADIC_LEVELS ? &sm : nullptr, nxt);
+                                                        lev >= DYADIC_LEVELS ? &sm : nullptr, nxt, st);
                     __syncthreads();
                     if (made < 0) {
                         if (threadIdx.x == 0)
@@ -941,6 +998,13 @@ __global__ void __launch_bounds__(BUILD_THREADS) build_kernel(BuildArgs a)
             grid.sync();
 #endif
             lev = meta[DT_META_CURLEVEL];
+            if (st.cap > 0) {
+                expand_stage(a, st, meta[DT_META_NODES], lev0_of_run);
+                // a following level reads the run's last nodes from the arrays
+                if (lev <= a.max_depth && !meta[DT_META_OVERFLOW] &&
+                    meta[DT_META_LEVEL0 + lev + 1] > meta[DT_META_LEVEL0 + lev])
+                    grid.sync();
+            }
             continue;
         }
         // ---- big level: all blocks, contiguous chunk per block
