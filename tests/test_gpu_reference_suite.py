@@ -412,3 +412,15 @@ def test_direct_compensated(dt):
     a = dt.evaluate_direct(s, k, ys, compensated=True, threads=1).values
     b = dt.evaluate_direct(s, k, ys, compensated=True, threads=3).values
     np.testing.assert_array_equal(a, b)
+
+
+def test_random_instance_reproducible_and_in_interval(dt):
+    """TestRandomInstance (test_metrics.py:73-86): same seed, same charges;
+    positions inside the interval and sorted, strengths non-negative."""
+    a, b = dt.random_instance(100, seed=5), dt.random_instance(100, seed=5)
+    np.testing.assert_array_equal(_np(a.xs), _np(b.xs))
+    np.testing.assert_array_equal(_np(a.qs), _np(b.qs))
+    s = dt.random_instance(200, seed=6, interval=(2.0, 3.0))
+    xs, qs = _np(s.xs), _np(s.qs)
+    assert np.all(xs >= 2.0) and np.all(xs <= 3.0)
+    assert np.all(np.diff(xs) >= 0) and np.all(qs >= 0)
