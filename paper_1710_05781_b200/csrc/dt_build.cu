@@ -224,19 +224,20 @@ constexpr int64_t DY_SAMPLES = (int64_t)1 << 18;
 #define DY_STAMP(slot)
 #endif
 
-__device__ void dyadic_splits(const BuildArgs &a, cg::grid_group &grid)
+__device__ __forceinline__ void dyadic_samples(const BuildArgs &a, int tid, int nth)
 {
     const int64_t stride = (a.n + DY_SAMPLES - 1) / DY_SAMPLES;
     const int64_t ns = (a.n + stride - 1) / stride;
-    const int tid = blockIdx.x * blockDim.x + threadIdx.x;
-    const int nth = gridDim.x * blockDim.x;
     for (int64_t i = tid; i < ns; i += nth)
         a.dy_samples[i] = __ldcs(a.xs + i * stride);
+}
+
+__device__ __forceinline__ void dyadic_search(const BuildArgs &a, int tid, int nth)
+{
+    const int64_t stride = (a.n + DY_SAMPLES - 1) / DY_SAMPLES;
+    const int64_t ns = (a.n + stride - 1) / stride;
     double lo0, hi0;
     root_interval(a, &lo0, &hi0);
-    DY_STAMP(73)
-    grid.sync();
-    DY_STAMP(74)
     const double *smp = a.dy_samples;
     for (int idx = tid; idx < DYADIC; idx += nth) {
         const int L = 31 - __clz(idx + 1);
@@ -291,7 +292,35 @@ __device__ void dyadic_splits(const BuildArgs &a, cg::grid_group &grid)
         a.dy_point[0] = make_double2(lo0, __longlong_as_double(0));
         a.dy_point[(int64_t)1 << DYADIC_LEVELS] = make_double2(hi0, __longlong_as_double(a.n));
     }
+}
+
+// In the cooperative build (16 warps per SM there) or, by default, as two
+// small kernels ahead of it at full occupancy: the searches are latency
+// chains (~20 dependent L2 probes each), so they want all the warps an SM
+// can hold rather than the build's 128-register blocks.
+#ifndef DT_BUILD_DYADIC_KERNELS
+#define DT_BUILD_DYADIC_KERNELS 1
+#endif
+__device__ void dyadic_splits(const BuildArgs &a, cg::grid_group &grid)
+{
+    const int tid = blockIdx.x * blockDim.x + threadIdx.x;
+    const int nth = gridDim.x * blockDim.x;
+    dyadic_samples(a, tid, nth);
+    DY_STAMP(73)
+    grid.sync();
+    DY_STAMP(74)
+    dyadic_search(a, tid, nth);
     DY_STAMP(75)
+}
+
+constexpr int DY_THREADS = 256;
+__global__ void __launch_bounds__(DY_THREADS) dyadic_samples_kernel(BuildArgs a)
+{
+    dyadic_samples(a, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x);
+}
+__global__ void __launch_bounds__(DY_THREADS) dyadic_search_kernel(BuildArgs a)
+{
+    dyadic_search(a, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x);
 }
 
 // Number of children of frontier node `node` (0 if it is a leaf) and split.
@@ -839,8 +868,10 @@ __global__ void __launch_bounds__(BUILD_THREADS) build_kernel(BuildArgs a)
         *small_flag = 0;
 #endif
     BUILD_STAMP(70)
-    dyadic_splits(a, grid);
-    grid.sync();
+    if (!DT_BUILD_DYADIC_KERNELS) {
+        dyadic_splits(a, grid);
+        grid.sync();
+    }
     BUILD_STAMP(71)
     int64_t lev = build_top(a, grid, warp_sums, top_bases_s, top_bases2_s);
     const int64_t k_listed = lev;  // the level whose splitting nodes are listed
@@ -1183,6 +1214,12 @@ static int build_launch(const double *xs, int64_t n, int64_t leaf_capacity, int6
     int grid = dt_num_sms() * (per_sm > DT_BUILD_PER_SM ? DT_BUILD_PER_SM : per_sm);
     if (grid > 3000)
         grid = 3000;
+    if (DT_BUILD_DYADIC_KERNELS) {
+        const int dy_blocks = (int)((DY_SAMPLES + DY_THREADS - 1) / DY_THREADS);
+        dyadic_samples_kernel<<<dy_blocks, DY_THREADS, 0, (cudaStream_t)stream>>>(a);
+        dyadic_search_kernel<<<dy_blocks, DY_THREADS, 0, (cudaStream_t)stream>>>(a);
+        DT_CUDA_TRY(cudaGetLastError());
+    }
     void *args[] = {&a};
     DT_CUDA_TRY(cudaLaunchCooperativeKernel((const void *)build_kernel, grid, BUILD_THREADS, args,
                                             smem, (cudaStream_t)stream));

@@ -35,10 +35,11 @@ from .tree import (
 )
 
 # kernels launched per step (memset of the work counter not counted):
-# scan(2) sign(2) build moments(2) eval, plus the two order-table kernels
+# scan(2) sign(2) build(3: dyadic samples, dyadic searches, the cooperative
+# build) moments(2) eval, plus the two order-table kernels
 # ahead of an adaptive evaluation with moment order <= 31, theta <= 1/2 (the
 # sharded pass adds its own launches and the separate pack)
-LAUNCHES_PER_STEP = 2 + 2 + 1 + 2 + 1
+LAUNCHES_PER_STEP = 2 + 2 + 3 + 2 + 1
 ORDER_TABLE_LAUNCHES = 2
 
 
